@@ -1,0 +1,479 @@
+"""Seer-selected SpMV benchmark (BASELINE.json metric) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C2]
+
+One STEP = the Seer hot path over one matrix (T_seer): fused selection
+(selector tree -> gathered feature pass -> gathered/known tree, one kernel), the chosen
+kernel's preprocessing (not cached across steps: charged every step), then k SpMV
+iterations.  Default workload = BASELINE configs[1] (C2: R-MAT scale 20, edge factor 16,
+permuted, fp32, k = 1), generated on the device with a counter-based hash (synthetic).
+
+value      = CSR algorithmic bytes x k / device time of the step   [GB/s]
+             (bytes = nnz*(4+4) + (R+1)*4 + C*4 + R*4, x counted once; inputs resident)
+e2e        = same metric through the public API with HOST buffers: pinned host CSR + x
+             copied H2D, the Seer pipeline, y copied D2H, all inside the timed region
+roofline   = the chosen SpMV op's own byte model / its CUDA-event duration vs the
+             measured HBM copy bandwidth (MEASURED_PEAKS.json)
+sweep      = every fixed kernel's prep + k*SpMV on the same matrix; geomean and best-fixed
+             speedups of Seer against them (the paper's 6.5x / 2x metrics)
+cpu_baseline = the oracle port on this host (OpenMP CPU SpMV + compiled reference
+             length_stats + restated predict), bounded ~10 s sample, rank 0 only
+L2: the 141 MB matrix exceeds the 126 MB L2 and a 512 MB buffer is rewritten between
+steps (outside the timed events) -> config["l2"] = "flushed".
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+
+
+def _peak_hbm():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md)"
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--iters", type=int, default=None, help="SpMV iterations k (default per config)")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    return ap.parse_args()
+
+
+CFG = {  # BASELINE.json configs -> (k, dtype, description)
+    "C1": (1, "float32", "uniform-random CSR 10k x 10k, ~100k nnz, fp32, k=1"),
+    "C2": (1, "float32", "R-MAT s20 ef16 (0.57/0.19/0.19/0.05) permuted CSR 1M x 1M, ~16.1M nnz, fp32, k=1"),
+    "C3": (100, "float32", "27-point stencil 159^3 (R=4,019,679, 107.2M nnz), fp32, k=100"),
+    "C4": (1, "float64", "skewed 2M rows: Poisson(8) + 4 rows x 1M nnz, fp64, k=1"),
+}
+
+
+def csr_bytes(R, C, Z, sv, so):
+    return Z * (4 + sv) + (R + 1) * so + C * sv + R * sv
+
+
+# ------------------------------------------------------------------------ clocks
+class ClockSampler:
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), "--query-gpu=clocks.sm,clocks.max.sm,"
+                 "clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap", "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            p = [v.strip() for v in ln.split(",")]
+            if len(p) < 7:
+                continue
+            try:
+                sm.append(float(p[0]))
+                mx = float(p[1])
+            except ValueError:
+                continue
+            for n, v in zip(names, p[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------ helpers
+def _load_model():
+    from paper_2403_17017_b200 import seer
+    path = os.path.join(ROOT, "paper_2403_17017_b200", "models", "seer_b200.json")
+    if os.path.exists(path):
+        return seer.SeerModel.load(path), "paper_2403_17017_b200/models/seer_b200.json"
+    return seer.bootstrap_model(), "bootstrap rules (no B200 bundle yet)"
+
+
+def _make_matrix(name, device):
+    from paper_2403_17017_b200 import gen
+    return gen.config(name, device=device)
+
+
+# ------------------------------------------------------------------------ our arm
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2403_17017_b200 import _lib, kernels, seer
+    from paper_2403_17017_b200.features import decode_outcome
+    from paper_2403_17017_b200.device import DeviceCSR
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    L = _lib.load()
+
+    k_default, dt_name, desc = CFG[a.workload]
+    k = a.iters or k_default
+    dtype = getattr(torch, dt_name)
+    m = _make_matrix(a.workload, dev)
+    A = m.to_device_csr(dtype, device=dev)
+    del m
+    R, C, Z = A.n_rows, A.n_cols, A.nnz
+    sv, so = A.values.element_size(), A.row_offsets.element_size()
+    bytes_csr = csr_bytes(R, C, Z, sv, so)
+    model, model_src = _load_model()
+    g = torch.Generator(device=dev).manual_seed(1234)
+    x = (torch.rand(C, device=dev, dtype=torch.float64, generator=g) * 2 - 1).to(dtype)
+    y = torch.empty(R, device=dev, dtype=dtype)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+    obuf = torch.empty(_lib.OUTCOME_BYTES, dtype=torch.uint8, device=dev)
+    ohost = torch.empty(_lib.OUTCOME_BYTES, dtype=torch.uint8, pin_memory=True)
+
+    def read_outcome():
+        ohost.copy_(obuf, non_blocking=True)
+        stream.synchronize()
+        return decode_outcome(ohost)
+
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+
+    def seer_step(AA, xx, yy, marks=None):
+        seer.select_async(model, AA, k, out=obuf)
+        o = read_outcome()
+        kern = int(o.kernel)
+        P = kernels.prepare(AA, kern, cache=False) if kern in kernels.NEEDS_PREP else None
+        if marks is not None:
+            marks[0].record()
+        for _ in range(k):
+            kernels.spmv(AA, xx, kern, y=yy, prepared=P)
+        if marks is not None:
+            marks[1].record()
+        return o, P
+
+    def fixed_step(kern, marks=None):
+        P = kernels.prepare(A, kern, cache=False) if kern in kernels.NEEDS_PREP else None
+        if marks is not None:
+            marks[0].record()
+        for _ in range(k):
+            kernels.spmv(A, x, kern, y=y, prepared=P)
+        if marks is not None:
+            marks[1].record()
+        return P
+
+    def timed(fn, steps, warm):
+        for _ in range(warm):
+            fn(None)
+        torch.cuda.synchronize()
+        tot, inner = [], []
+        for _ in range(steps):
+            flush.zero_()
+            e0, e1, m0, m1 = ev(), ev(), ev(), ev()
+            e0.record()
+            fn((m0, m1))
+            e1.record()
+            e1.synchronize()
+            tot.append(e0.elapsed_time(e1) * 1e-3)
+            inner.append(m0.elapsed_time(m1) * 1e-3)
+        return tot, inner
+
+    # ---------------------------------------------------------------- warmup + timed (value)
+    for _ in range(a.warmup):
+        seer_step(A, x, y)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    n_launch0 = L.kp_launch_count()
+    step_t, spmv_t = [], []
+    outcome, prepared = None, None
+    for _ in range(a.steps):
+        flush.zero_()
+        e0, e1, m0, m1 = ev(), ev(), ev(), ev()
+        e0.record()
+        outcome, prepared = seer_step(A, x, y, (m0, m1))
+        e1.record()
+        e1.synchronize()
+        step_t.append(e0.elapsed_time(e1) * 1e-3)
+        spmv_t.append(m0.elapsed_time(m1) * 1e-3)
+    launches = L.kp_launch_count() - n_launch0
+    torch.cuda.synchronize()
+    total = sum(step_t)
+    if world > 1:
+        dist.barrier()
+        tt = torch.tensor([total], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total = float(tt.item())
+    kern = int(outcome.kernel)
+    value = world * a.steps * k * bytes_csr / total / 1e9
+
+    # ---------------------------------------------------------------- roofline of the chosen SpMV op
+    peak, peak_src = _peak_hbm()
+    ell_w = None
+    if kern == kernels.ELL_TM:
+        hdr = prepared.buf[:64].cpu().view(torch.int64)
+        ell_w = int(min(int(hdr[3]), prepared.ell_cap))
+    kbytes = A.byte_model(kern, ell_w)
+    per_launch = statistics.mean(spmv_t) / k
+    achieved = kbytes / per_launch / 1e9
+    traffic = _traffic_from_profiles(a.workload, kernels.KERNELS[kern])
+
+    # ---------------------------------------------------------------- e2e through the public API
+    e2e = _e2e(a, A, x, dtype, dev, model, k, seer_step, stream)
+    clk = clocks.stop()
+
+    # ---------------------------------------------------------------- per-kernel sweep
+    sweep, geo, vs_best = None, None, None
+    if not a.no_sweep and rank == 0:
+        sweep = {}
+        seer_mean = total / a.steps if world == 1 else sum(step_t) / a.steps
+        for kk in range(len(kernels.KERNELS)):
+            tot, inner = timed(lambda mk, kk=kk: fixed_step(kk, mk), max(3, a.steps // 2), 2)
+            t_tot, t_sp = statistics.mean(tot), statistics.mean(inner) / k
+            w = None
+            if kk == kernels.ELL_TM:
+                P = kernels.prepare(A, kk, cache=False)
+                w = int(min(int(P.buf[:64].cpu().view(torch.int64)[3]), P.ell_cap))
+            sweep[kernels.KERNELS[kk]] = {
+                "total_us": round(t_tot * 1e6, 2), "spmv_us": round(t_sp * 1e6, 2),
+                "prep_us": round((t_tot - t_sp * k) * 1e6, 2),
+                "spmv_gbs": round(A.byte_model(kk, w) / t_sp / 1e9, 1),
+                "spmv_frac_of_peak": round(A.byte_model(kk, w) / t_sp / 1e9 / peak, 3)}
+        ratios = [sweep[n]["total_us"] * 1e-6 / seer_mean for n in kernels.KERNELS]
+        geo = math.exp(sum(math.log(r) for r in ratios) / len(ratios))
+        vs_best = min(ratios)
+
+    # ---------------------------------------------------------------- CPU baseline (rank 0, N=1)
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu:
+        cpu = _cpu_baseline(A, x, k, model, bytes_csr, a.cpu_seconds)
+
+    if rank == 0:
+        line = {
+            "metric": "Seer-selected SpMV GB/s (% HBM roofline) and geomean speedup vs best fixed kernel",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(total / a.steps * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32" if dtype == torch.float32 else "f64",
+            "data": "synthetic (counter-hash generated on device)",
+            "config": {"workload": a.workload, "desc": desc, "rows": R, "cols": C, "nnz": Z, "iterations": k,
+                       "offsets": str(A.row_offsets.dtype).replace("torch.", ""), "l2": "flushed (512 MB write "
+                       "between steps; matrix > L2)", "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
+                       "model": model_src, "byte_model": "nnz*(4+sv)+(R+1)*so+C*sv+R*sv"},
+            "seer": {"kernel": kernels.KERNELS[kern], "path": "gathered" if outcome.path else "known",
+                     "features": [outcome.max_d, outcome.min_d, outcome.mean_d, outcome.var_d] if outcome.path else None,
+                     "step_us_median": round(statistics.median(step_t) * 1e6, 2),
+                     "spmv_us_mean": round(per_launch * 1e6, 2)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kernels.KERNELS[kern],
+                         "algorithmic_bytes_per_launch": kbytes, "peak_source": peak_src},
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "geomean_speedup_vs_fixed": None if geo is None else round(geo, 3),
+            "speedup_vs_best_fixed": None if vs_best is None else round(vs_best, 3),
+            "sweep": sweep,
+            "cpu_baseline": cpu,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _traffic_from_profiles(workload, kernel_label):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f).get(workload, {}).get(kernel_label)
+    except Exception:
+        return None
+
+
+def _e2e(a, A, x, dtype, dev, model, k, seer_step, stream):
+    """Public-API end to end: pinned host CSR + x -> H2D -> Seer -> y D2H."""
+    import torch
+    from paper_2403_17017_b200.device import DeviceCSR
+    h_off = A.row_offsets.cpu().pin_memory()
+    h_col = A.col_indices.cpu().pin_memory()
+    h_val = A.values.cpu().pin_memory()
+    h_x = x.cpu().pin_memory()
+    h_y = torch.empty(A.n_rows, dtype=dtype, pin_memory=True)
+    d_off, d_col, d_val = torch.empty_like(A.row_offsets), torch.empty_like(A.col_indices), torch.empty_like(A.values)
+    d_x, d_y = torch.empty_like(x), torch.empty(A.n_rows, dtype=dtype, device=dev)
+    B = DeviceCSR(A.n_rows, A.n_cols, d_off, d_col, d_val)  # views the staging buffers
+    bi = sum(t.numel() * t.element_size() for t in (h_off, h_col, h_val, h_x))
+    bo = h_y.numel() * h_y.element_size()
+
+    def step():
+        d_off.copy_(h_off, non_blocking=True)
+        d_col.copy_(h_col, non_blocking=True)
+        d_val.copy_(h_val, non_blocking=True)
+        d_x.copy_(h_x, non_blocking=True)
+        seer_step(B, d_x, d_y)
+        h_y.copy_(d_y, non_blocking=True)
+
+    for _ in range(max(2, a.warmup)):
+        step()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(3, a.steps // 2)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    e1.synchronize()
+    t = e0.elapsed_time(e1) * 1e-3 / steps
+    bytes_csr = csr_bytes(A.n_rows, A.n_cols, A.nnz, A.values.element_size(), A.row_offsets.element_size())
+    return {"value": round(k * bytes_csr / t / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": int(bi),
+            "d2h_bytes_per_step": int(bo), "ms_per_step": round(t * 1e3, 4),
+            "api": "DeviceCSR staging + seer.select_async/kernels.prepare/kernels.spmv (C-ABI) from pinned host"}
+
+
+def _cpu_baseline(A, x, k, model, bytes_csr, seconds):
+    """Oracle port on this host: compiled reference length_stats (oracle/_ref) +
+    restated epilogue/predict + OpenMP CPU SpMV, looped for ~``seconds``."""
+    import numpy as np
+    from oracle import oracle as orc
+    off32, col, val = A.to_host()
+    xh = x.cpu().numpy()
+    off64 = off32.astype(np.int64)
+    core = orc.ref_core()
+    mdict = {n: t.to_dict() for n, t in (("selector", model.selector_tree), ("known", model.known_tree),
+                                          ("gathered", model.gathered_tree))}
+
+    def one():
+        if core is not None:
+            lo, hi, s1, s2 = core.length_stats(off64)
+        else:
+            lo, hi, s1, s2 = orc.length_stats(off64)
+        f = orc.features_epilogue(lo, hi, s1, s2, A.n_rows, A.n_cols)
+        kern, _ = orc.infer(mdict, A.n_rows, A.n_cols, A.nnz, k, f)
+        for _ in range(k):
+            orc.spmv_native(off32, col, val, xh)
+        return kern
+
+    one()
+    t0 = time.perf_counter()
+    reps = 0
+    while True:
+        one()
+        reps += 1
+        el = time.perf_counter() - t0
+        if el >= seconds or reps >= 10000:
+            break
+    return {"value": round(reps * k * bytes_csr / el / 1e9, 3), "unit": "GB/s", "cores": orc.threads(),
+            "kind": "port", "sample": f"{reps} full pipelines (features via "
+            f"{'compiled reference _core' if core else 'oracle C'} + predict + {k} OpenMP SpMV) on the same matrix, "
+            f"{el:.1f} s", "ms_per_step": round(el / reps * 1e3, 3)}
+
+
+# ------------------------------------------------------------------------ reference arm
+def run_reference(a):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import torch
+    k_default, dt_name, desc = CFG[a.workload]
+    k = a.iters or k_default
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    m = _make_matrix(a.workload, dev)  # generation only (torch); nothing of ours computes below
+    import numpy as np
+    from oracle import oracle as orc
+    off64, col64, val64 = m.numpy()
+    dtype = np.float32 if dt_name == "float32" else np.float64
+    off32 = off64.astype(np.int32) if m.nnz < 2**31 - 1 else off64
+    col, val = col64.astype(np.int32), val64.astype(dtype)
+    xh = (np.random.default_rng(1234).uniform(-1, 1, m.n_cols)).astype(dtype)
+    sv = np.dtype(dtype).itemsize
+    bytes_csr = csr_bytes(m.n_rows, m.n_cols, m.nnz, sv, off32.itemsize)
+    model, _ = _load_model()
+    mdict = {n: t.to_dict() for n, t in (("selector", model.selector_tree), ("known", model.known_tree),
+                                          ("gathered", model.gathered_tree))}
+    core = orc.ref_core()
+
+    def step():
+        lo, hi, s1, s2 = (core.length_stats(off64) if core is not None else orc.length_stats(off64))
+        f = orc.features_epilogue(lo, hi, s1, s2, m.n_rows, m.n_cols)
+        orc.infer(mdict, m.n_rows, m.n_cols, m.nnz, k, f)
+        for _ in range(k):
+            orc.spmv_native(off32, col, val, xh)
+
+    for _ in range(a.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        step()
+    el = time.perf_counter() - t0
+    v = a.steps * k * bytes_csr / el / 1e9
+    print(json.dumps({
+        "impl": "reference",
+        "metric": "Seer-selected SpMV GB/s (% HBM roofline) and geomean speedup vs best fixed kernel",
+        "value": round(v, 3), "unit": "GB/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(el / a.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32" if dtype == np.float32 else "f64",
+        "data": "synthetic (counter-hash generated)",
+        "config": {"workload": a.workload, "desc": desc, "rows": m.n_rows, "cols": m.n_cols, "nnz": m.nnz,
+                   "iterations": k},
+        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": orc.threads(), "kind": "port",
+                         "sample": f"{a.steps} full pipelines: features via "
+                                   f"{'compiled reference _core (oracle/_ref)' if core else 'oracle C restatement'}"
+                                   f", restated predict, {k} OpenMP CPU SpMV (the reference has no SpMV)"},
+        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def main():
+    a = _args()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,181 @@
+/*
+ * kernelpick_b200.h -- C-ABI of the B200-native Seer hot path (libkpb200.so).
+ *
+ * Drop-in boundary for the reference's `kernelpick._kernels` backend
+ * (/root/reference/pkg/src/kernelpick/_kernels/__init__.py:1-28) plus the SPEC-only
+ * surfaces on the north-star path (dtree.predict, seer-core.infer, the SpMV kernel
+ * family of PAPER.md:263-273 and its preprocessing).
+ *
+ * Conventions (all entry points):
+ *   - return int status: KP_OK (0) or a negative KP_E* code; no exceptions cross the ABI;
+ *   - every buffer argument named d_* is a DEVICE pointer owned by the caller;
+ *   - work is enqueued asynchronously on `stream` (a cudaStream_t; NULL = legacy default);
+ *   - no host synchronisation happens inside any call below;
+ *   - scratch memory comes from the caller through *_workspace_bytes() queries.
+ *
+ * Offset arrays may be int32 (KP_I32, valid while nnz < 2^31) or int64 (KP_I64, the
+ * reference layout, sparse.py:37); column indices are int32; values / x / y are fp32
+ * (KP_F32) or fp64 (KP_F64).
+ */
+#ifndef KERNELPICK_B200_H
+#define KERNELPICK_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define KP_API __attribute__((visibility("default")))
+#else
+#define KP_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---------------------------------------------------------------- status codes */
+#define KP_OK 0
+#define KP_EINVAL (-1)      /* bad argument (reference: ValueError)                */
+#define KP_ECUDA (-2)       /* a CUDA launch / runtime call failed                  */
+#define KP_ENOMEM (-3)      /* caller workspace too small                           */
+#define KP_EUNSUPPORTED (-4)
+#define KP_ERANGE (-5)      /* value outside the exactly-representable range        */
+
+/* ---------------------------------------------------------------- type codes   */
+#define KP_I32 0
+#define KP_I64 1
+#define KP_F32 0
+#define KP_F64 1
+
+/* Kernel vocabulary, fixed order = PAPER.md Table III (:311-318); tree class indices
+ * and lowest-index tie-breaks depend on it.  Never reorder. */
+#define KP_ADAPTIVE_CSR 0
+#define KP_CSR_BM 1
+#define KP_CSR_MP 2
+#define KP_CSR_WM 3
+#define KP_CSR_WO 4
+#define KP_CSR_TM 5
+#define KP_COO_WM 6
+#define KP_ELL_TM 7
+#define KP_NUM_KERNELS 8
+
+/* Seer path. */
+#define KP_USE_KNOWN 0
+#define KP_USE_GATHERED 1
+
+/* Device CSR view (host struct holding device pointers).  Mirrors SparseMatrixCSR
+ * (sparse.py:33-39) with device-width index/value types. */
+typedef struct kp_csr {
+    int64_t n_rows, n_cols, nnz;
+    int32_t off_type;          /* KP_I32 | KP_I64 */
+    int32_t val_type;          /* KP_F32 | KP_F64 */
+    const void *row_offsets;   /* [n_rows + 1] */
+    const int32_t *col_indices;/* [nnz] */
+    const void *values;        /* [nnz] */
+} kp_csr;
+
+/* Result of the fused feature pass / selection, written to DEVICE memory.
+ * lo/hi/s1/s2 = _kernels.length_stats (_core.pyx:15-33, wrapping int64);
+ * max/min/mean/var = GatheredFeatures.as_vector() (features.py:46-52, 74-85). */
+typedef struct kp_outcome {
+    int64_t lo, hi, s1, s2;
+    double max_d, min_d, mean_d, var_d;
+    int32_t kernel;            /* chosen kernel index (seer) or -1            */
+    int32_t path;              /* KP_USE_KNOWN / KP_USE_GATHERED              */
+    int32_t status;            /* KP_OK or KP_ERANGE from the epilogue guard  */
+    int32_t reserved;
+} kp_outcome;
+
+/* Packed decision tree, DEVICE memory, 8-byte aligned:
+ *   kp_tree_header followed by n_nodes kp_tree_node records.
+ * feature < 0 marks a leaf whose class is `value`. Left iff x[feature] <= threshold. */
+typedef struct kp_tree_header {
+    int32_t n_nodes, n_features, n_classes, max_depth;
+} kp_tree_header;
+typedef struct kp_tree_node {
+    double threshold;
+    int32_t feature, left, right, value;
+} kp_tree_node;
+
+/* Prepared-format view produced by kp_prepare() inside a caller buffer. */
+typedef struct kp_prepared {
+    int32_t kernel;            /* KP_* kernel id this preparation serves            */
+    int32_t group;             /* CSR,WM lanes per row (2..32), chosen from nnz/rows */
+    int64_t n_units;           /* MP tiles / adaptive units / COO chunks            */
+    int64_t ell_cap;           /* ELL: allocated width (columns)                    */
+    void *buf;                 /* base of the caller buffer                         */
+    size_t bytes;
+} kp_prepared;
+
+/* ------------------------------------------------------- drop-in backend (K1, K2) */
+/* Scratch for every reduction entry point; must be zeroed ONCE at allocation
+ * (cudaMemset); the kernels leave it zeroed again after each call. */
+KP_API size_t kp_reduce_workspace_bytes(void);
+
+/* _kernels.length_stats (_core.pyx:15-33 / _pure.py:11-21):
+ * d_out4 <- (min, max, sum, sum of squares) of diff(row_offsets), int64 wrapping.
+ * n_off = len(row_offsets); n_off <= 1 gives (0, 0, 0, 0). */
+KP_API int kp_length_stats(const void *d_off, int32_t off_type, int64_t n_off,
+                    int64_t *d_out4, void *d_ws, void *stream);
+
+/* _kernels.wave_ceil_max_sum (_core.pyx:36-56 / _pure.py:24-38):
+ * d_out1 <- sum over consecutive waves of `wave_rows` rows of max ceil(len/divisor).
+ * divisor <= 0 or wave_rows <= 0 -> KP_EINVAL (the reference backends diverge). */
+KP_API int kp_wave_ceil_max_sum(const void *d_off, int32_t off_type, int64_t n_off,
+                         int64_t divisor, int64_t wave_rows, int64_t *d_out1,
+                         void *d_ws, void *stream);
+
+/* features.gather_features (features.py:64-87) minus the clock: the integer pass
+ * and the bit-exact fp64 epilogue in one launch.  n_rows == 0 or n_cols == 0 ->
+ * KP_EINVAL (features.py:67-70). */
+KP_API int kp_gather_features(const void *d_off, int32_t off_type, int64_t n_rows,
+                       int64_t n_cols, kp_outcome *d_out, void *d_ws, void *stream);
+
+/* ------------------------------------------------------------ trees / selection */
+/* dtree.predict over a batch: d_out[i] = predict(tree, d_x[i*n_feat:]). */
+KP_API int kp_tree_predict(const void *d_tree, const double *d_x, int64_t n, int32_t n_feat,
+                    int32_t *d_out, void *stream);
+
+/* seer-core.infer fused on device: selector tree on
+ * (rows, cols, nnz, iterations) -> USE_KNOWN: known tree; USE_GATHERED: the
+ * gather_features pass + gathered tree on known + (max, min, mean, var).
+ * Writes the kp_outcome (kernel, path, features) to d_out; no host sync. */
+KP_API int kp_seer_select(const void *d_off, int32_t off_type, int64_t n_rows, int64_t n_cols,
+                   int64_t nnz, int64_t iterations, const void *d_selector,
+                   const void *d_known, const void *d_gathered, kp_outcome *d_out,
+                   void *d_ws, void *stream);
+
+/* ------------------------------------------------------------ preprocessing */
+/* Bytes the caller must provide for kp_prepare(kernel, A).  ell_cap (ELL only) is
+ * the width reserved for the padded part; rows longer than the actual width
+ * continue from CSR (hybrid tail), so any cap >= 1 is correct. */
+KP_API int kp_prepare_bytes(int32_t kernel, const kp_csr *A, int64_t ell_cap, size_t *bytes);
+/* Builds the kernel's preprocessed format (MP partition K10, COO row ids K11,
+ * ELL K12, adaptive row blocks K13) into d_buf.  Kernels without preprocessing
+ * (BM, WM, WO, TM) just fill *out.  The prepared data stays valid while A lives. */
+KP_API int kp_prepare(int32_t kernel, const kp_csr *A, int64_t ell_cap, void *d_buf, size_t bytes,
+               kp_prepared *out, void *stream);
+
+/* ------------------------------------------------------------ SpMV */
+KP_API int kp_spmv_workspace_bytes(int32_t kernel, const kp_csr *A, size_t *bytes);
+/* y = A . x with kernel `kernel` (KP_*).  d_x has n_cols entries, d_y n_rows, both of
+ * A->val_type.  Deterministic: no floating-point atomics; repeated calls give
+ * identical bits. */
+KP_API int kp_spmv(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x,
+            void *d_y, void *d_ws, size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------ multi-GPU (K14) */
+/* nnz-balanced row cut: d_cuts[p] = lower_bound(row_offsets, p*nnz/parts), p = 0..parts
+ * (d_cuts[parts] = n_rows). */
+KP_API int kp_shard_partition(const void *d_off, int32_t off_type, int64_t n_rows, int32_t parts,
+                       int64_t *d_cuts, void *stream);
+
+/* Library identification: "kpb200 <version> sm_100a". */
+KP_API const char *kp_version(void);
+/* Number of kernel launches issued by this library since load (instrumentation). */
+KP_API uint64_t kp_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* KERNELPICK_B200_H */

@@ -1,0 +1,124 @@
+"""ctypes binding of libkpb200.so (the C-ABI in include/kernelpick_b200.h).
+
+There is deliberately no CPU fallback: if the shared library is missing or no CUDA
+device is present, every compute entry point raises ``BackendUnavailable``.
+PyTorch is used only as the device-memory / stream allocator (plumbing).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import KernelPickError
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libkpb200.so")
+
+# status codes (kernelpick_b200.h)
+KP_OK, KP_EINVAL, KP_ECUDA, KP_ENOMEM, KP_EUNSUPPORTED, KP_ERANGE = 0, -1, -2, -3, -4, -5
+KP_I32, KP_I64 = 0, 1
+KP_F32, KP_F64 = 0, 1
+KP_USE_KNOWN, KP_USE_GATHERED = 0, 1
+
+EXPORTS = (
+    "kp_reduce_workspace_bytes", "kp_length_stats", "kp_wave_ceil_max_sum", "kp_gather_features",
+    "kp_tree_predict", "kp_seer_select", "kp_prepare_bytes", "kp_prepare",
+    "kp_spmv_workspace_bytes", "kp_spmv", "kp_shard_partition", "kp_version", "kp_launch_count",
+)
+
+
+class BackendUnavailable(KernelPickError):
+    """The sm_100a backend (libkpb200.so + a CUDA device) is not available."""
+
+
+class KernelError(KernelPickError):
+    """A C-ABI call returned a non-zero status."""
+
+
+class kp_csr(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64), ("nnz", ctypes.c_int64),
+                ("off_type", ctypes.c_int32), ("val_type", ctypes.c_int32),
+                ("row_offsets", ctypes.c_void_p), ("col_indices", ctypes.c_void_p),
+                ("values", ctypes.c_void_p)]
+
+
+class kp_outcome(ctypes.Structure):
+    _fields_ = [("lo", ctypes.c_int64), ("hi", ctypes.c_int64), ("s1", ctypes.c_int64),
+                ("s2", ctypes.c_int64), ("max_d", ctypes.c_double), ("min_d", ctypes.c_double),
+                ("mean_d", ctypes.c_double), ("var_d", ctypes.c_double), ("kernel", ctypes.c_int32),
+                ("path", ctypes.c_int32), ("status", ctypes.c_int32), ("reserved", ctypes.c_int32)]
+
+
+class kp_prepared(ctypes.Structure):
+    _fields_ = [("kernel", ctypes.c_int32), ("group", ctypes.c_int32), ("n_units", ctypes.c_int64),
+                ("ell_cap", ctypes.c_int64), ("buf", ctypes.c_void_p), ("bytes", ctypes.c_size_t)]
+
+
+OUTCOME_BYTES = ctypes.sizeof(kp_outcome)  # 96
+_lib = None
+
+
+def load(require: bool = True):
+    """Load libkpb200.so (no CUDA context needed).  Raises BackendUnavailable."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        if not require:
+            return None
+        raise BackendUnavailable(
+            f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(or make -C paper_2403_17017_b200/csrc); there is no CPU fallback")
+    L = ctypes.CDLL(LIB_PATH)
+    i32, i64, p, sz = ctypes.c_int32, ctypes.c_int64, ctypes.c_void_p, ctypes.c_size_t
+    P = ctypes.POINTER
+    sig = {
+        "kp_reduce_workspace_bytes": (sz, []),
+        "kp_length_stats": (ctypes.c_int, [p, i32, i64, p, p, p]),
+        "kp_wave_ceil_max_sum": (ctypes.c_int, [p, i32, i64, i64, i64, p, p, p]),
+        "kp_gather_features": (ctypes.c_int, [p, i32, i64, i64, p, p, p]),
+        "kp_tree_predict": (ctypes.c_int, [p, p, i64, i32, p, p]),
+        "kp_seer_select": (ctypes.c_int, [p, i32, i64, i64, i64, i64, p, p, p, p, p, p]),
+        "kp_prepare_bytes": (ctypes.c_int, [i32, P(kp_csr), i64, P(sz)]),
+        "kp_prepare": (ctypes.c_int, [i32, P(kp_csr), i64, p, sz, P(kp_prepared), p]),
+        "kp_spmv_workspace_bytes": (ctypes.c_int, [i32, P(kp_csr), P(sz)]),
+        "kp_spmv": (ctypes.c_int, [i32, P(kp_csr), P(kp_prepared), p, p, p, sz, p]),
+        "kp_shard_partition": (ctypes.c_int, [p, i32, i64, i32, p, p]),
+        "kp_version": (ctypes.c_char_p, []),
+        "kp_launch_count": (ctypes.c_uint64, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = L
+    return L
+
+
+def check(rc: int, what: str) -> None:
+    if rc == KP_OK:
+        return
+    if rc == KP_EINVAL:
+        raise ValueError(f"{what}: invalid argument (KP_EINVAL)")
+    if rc == KP_ERANGE:
+        raise OverflowError(f"{what}: value outside the exactly representable range (KP_ERANGE)")
+    if rc == KP_ENOMEM:
+        raise MemoryError(f"{what}: workspace too small (KP_ENOMEM)")
+    raise KernelError(f"{what}: status {rc}")
+
+
+def require_cuda():
+    """Import torch and check a CUDA device is present; returns the torch module."""
+    import torch
+    if not torch.cuda.is_available():
+        raise BackendUnavailable("no CUDA device: the kernelpick-b200 backend runs only on sm_100a GPUs "
+                                 "(there is no CPU fallback)")
+    load()
+    return torch
+
+
+def stream_handle(stream=None) -> int:
+    import torch
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)

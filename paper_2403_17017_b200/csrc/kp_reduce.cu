@@ -1,0 +1,550 @@
+// kp_reduce.cu -- K1 row_stats (+ bit-exact fp64 epilogue + device tree eval),
+// K2 wave_ceil_max_sum, dtree.predict batch, fused seer_select (K15).
+//
+// Reference counterparts:
+//   K1  _kernels.length_stats     /root/reference/pkg/src/kernelpick/_kernels/_core.pyx:15-33
+//   K1e gather_features epilogue  features.py:74-85 (compiled with -fmad=false AND explicit
+//       __d*_rn intrinsics: Python float math never contracts to FMA)
+//   K2  wave_ceil_max_sum         _core.pyx:36-56
+//   predict                       SPEC.md:296-301 ; infer SPEC.md:376-384
+//
+// One pass over row_offsets: every CTA streams 16-byte vectors (4 x int32 or 2 x int64
+// offsets per lane, neighbour offset via shuffle), reduces (min, max, sum of squares)
+// in registers -> warp -> CTA, writes one partial; the last CTA to finish (ticket
+// counter) folds the partials in fixed order, runs the epilogue and the tree, and
+// resets the ticket so the workspace is reusable without a memset.  Integer sums are
+// uint64 (wrap exactly like the reference's int64); sum = off[n] - off[0] telescopes.
+#include "kp_internal.cuh"
+
+namespace kp {
+
+unsigned long long g_launches = 0;
+
+int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0)
+            n = kNumSMs;
+    }
+    return n;
+}
+
+namespace {
+
+constexpr int kRedThreads = 256;
+constexpr int kMaxRedBlocks = 148 * 8;
+
+struct Partial {
+    int64_t lo, hi;
+    uint64_t s2, aux;
+};
+struct RedWorkspace {
+    unsigned int ticket;
+    unsigned int pad[3];
+    Partial part[kMaxRedBlocks];
+};
+
+enum Mode : int { kModeStats = 0, kModeFeatures = 1, kModeSeer = 2 };
+
+// ------------------------------------------------------------------ trees in smem
+constexpr int kMaxTreeNodes = 1023;  // depth <= 9 complete tree; SPEC default depth 5 -> 63
+
+struct SmemTree {
+    int32_t n;
+    kp_tree_node node[kMaxTreeNodes];
+};
+
+__device__ __forceinline__ void load_tree(SmemTree &t, const void *d_tree) {
+    const kp_tree_header *h = reinterpret_cast<const kp_tree_header *>(d_tree);
+    const kp_tree_node *src = reinterpret_cast<const kp_tree_node *>(h + 1);
+    int n = h->n_nodes;
+    if (n > kMaxTreeNodes) n = kMaxTreeNodes;
+    if (threadIdx.x == 0) t.n = n;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) t.node[i] = src[i];
+}
+
+// root-to-leaf, x[f] <= thr goes left.
+__device__ __forceinline__ int32_t predict_smem(const SmemTree &t, const double *x) {
+    int32_t i = 0;
+    while (t.node[i].feature >= 0) i = (x[t.node[i].feature] <= t.node[i].threshold) ? t.node[i].left : t.node[i].right;
+    return t.node[i].value;
+}
+
+__device__ __forceinline__ int32_t predict_global(const void *d_tree, const double *x) {
+    const kp_tree_node *nd = reinterpret_cast<const kp_tree_node *>(
+        reinterpret_cast<const kp_tree_header *>(d_tree) + 1);
+    int32_t i = 0;
+    for (;;) {
+        kp_tree_node v = nd[i];
+        if (v.feature < 0) return v.value;
+        i = (x[v.feature] <= v.threshold) ? v.left : v.right;
+    }
+}
+
+// ------------------------------------------------------------------ fp64 epilogue
+// features.py:74-85 restated with explicit round-to-nearest intrinsics (no FMA).
+constexpr int64_t kExact53 = (int64_t)1 << 53;
+
+__device__ void epilogue(int64_t lo, int64_t hi, int64_t s1, int64_t s2, int64_t n, int64_t c,
+                         kp_outcome *o) {
+    o->lo = lo; o->hi = hi; o->s1 = s1; o->s2 = s2;
+    // Python int/int true division is the single correctly-rounded double division
+    // only while both operands are <= 2**53 (CPython long_true_divide fast path).
+    bool exact = (c <= kExact53) && (hi <= kExact53) && (hi >= -kExact53) &&
+                 (lo <= kExact53) && (lo >= -kExact53);
+    double dc = __ll2double_rn(c);
+    double max_d = __ddiv_rn(__ll2double_rn(hi), dc);
+    double min_d = __ddiv_rn(__ll2double_rn(lo), dc);
+    double denom = __dmul_rn(__ll2double_rn(n), dc);
+    double mean_d = __ddiv_rn(__ll2double_rn(s1), denom);
+    double var_d;
+    if (hi == lo) {
+        var_d = 0.0;
+    } else {
+        var_d = __dsub_rn(__ddiv_rn(__ll2double_rn(s2), __dmul_rn(denom, dc)), __dmul_rn(mean_d, mean_d));
+        if (var_d < 0.0) var_d = 0.0;
+    }
+    o->max_d = max_d; o->min_d = min_d; o->mean_d = mean_d; o->var_d = var_d;
+    o->status = exact ? KP_OK : KP_ERANGE;
+}
+
+// ------------------------------------------------------------------ K1 body
+template <typename O>
+struct Vec16;
+template <>
+struct Vec16<int32_t> {
+    static constexpr int V = 4;
+    using T = int4;
+    __device__ static void load(const int32_t *p, int64_t (&o)[4]) {
+        int4 v = ld_stream4(reinterpret_cast<const int4 *>(p));
+        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
+    }
+};
+template <>
+struct Vec16<int64_t> {
+    static constexpr int V = 2;
+    __device__ static void load(const int64_t *p, int64_t (&o)[2]) {
+        longlong2 v = ld_stream2ll(reinterpret_cast<const longlong2 *>(p));
+        o[0] = v.x; o[1] = v.y;
+    }
+};
+
+__device__ __forceinline__ void acc_len(int64_t a, int64_t b, int64_t &lo, int64_t &hi, uint64_t &s2) {
+    uint64_t u = (uint64_t)b - (uint64_t)a;
+    int64_t ln = (int64_t)u;
+    lo = ln < lo ? ln : lo;
+    hi = ln > hi ? ln : hi;
+    s2 += u * u;
+}
+
+// Accumulates rows [0, n_rows) handled by this thread (grid-wide distribution).
+template <typename O, bool kVec>
+__device__ __forceinline__ void stats_accum(const O *__restrict__ off, int64_t n_rows,
+                                            int64_t &lo, int64_t &hi, uint64_t &s2) {
+    const int lane = threadIdx.x & 31;
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    if constexpr (kVec) {
+        constexpr int V = Vec16<O>::V;
+        const int64_t nvec = n_rows / V;  // vector v covers rows v*V .. v*V+V-1
+        for (int64_t base = gwarp * 32; base < nvec; base += nwarps * 32) {
+            const int64_t v = base + lane;
+            const bool act = v < nvec;
+            int64_t e[V];
+            if (act) Vec16<O>::load(off + v * V, e);
+            else {
+#pragma unroll
+                for (int k = 0; k < V; ++k) e[k] = 0;
+            }
+            int64_t nxt = __shfl_down_sync(0xffffffffu, e[0], 1);
+            if (act && (lane == 31 || v + 1 >= nvec)) nxt = ldo(off + (v + 1) * V);
+            if (act) {
+#pragma unroll
+                for (int k = 0; k < V - 1; ++k) acc_len(e[k], e[k + 1], lo, hi, s2);
+                acc_len(e[V - 1], nxt, lo, hi, s2);
+            }
+        }
+        // scalar tail rows [nvec*V, n_rows)
+        const int64_t t0 = nvec * V;
+        const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (gt < n_rows - t0) acc_len(ldo(off + t0 + gt), ldo(off + t0 + gt + 1), lo, hi, s2);
+    } else {
+        const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        const int64_t st = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t i = gt; i < n_rows; i += st) acc_len(ldo(off + i), ldo(off + i + 1), lo, hi, s2);
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) { T w = __shfl_xor_sync(0xffffffffu, v, o); v = w < v ? w : v; }
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) { T w = __shfl_xor_sync(0xffffffffu, v, o); v = w > v ? w : v; }
+    return v;
+}
+__device__ __forceinline__ uint64_t warp_sum_u64(uint64_t v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Block-reduce (lo, hi, s2) into thread 0.
+__device__ __forceinline__ void block_reduce(int64_t &lo, int64_t &hi, uint64_t &s2) {
+    __shared__ int64_t slo[32], shi[32];
+    __shared__ uint64_t ss2[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    lo = warp_min(lo); hi = warp_max(hi); s2 = warp_sum_u64(s2);
+    if (lane == 0) { slo[w] = lo; shi[w] = hi; ss2[w] = s2; }
+    __syncthreads();
+    if (w == 0) {
+        lo = lane < nw ? slo[lane] : INT64_MAX;
+        hi = lane < nw ? shi[lane] : INT64_MIN;
+        s2 = lane < nw ? ss2[lane] : 0;
+        lo = warp_min(lo); hi = warp_max(hi); s2 = warp_sum_u64(s2);
+    }
+}
+
+// Shared state of the fused K1 / K15 kernel.
+struct K1Args {
+    const void *off;
+    int64_t n_rows, n_cols, nnz, iters;
+    int mode;
+    int64_t *out4;          // kModeStats
+    kp_outcome *out;        // kModeFeatures / kModeSeer
+    const void *sel, *known, *gath;
+    RedWorkspace *ws;
+};
+
+template <typename O, bool kVec>
+__global__ void __launch_bounds__(kRedThreads) k_row_stats(K1Args a) {
+    __shared__ SmemTree tree;
+    __shared__ int s_path;
+    __shared__ bool s_last;
+    const O *off = reinterpret_cast<const O *>(a.off);
+
+    if (a.mode == kModeSeer) {
+        // Selector on the known schema (rows, cols, nnz, iterations).
+        load_tree(tree, a.sel);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double xk[4] = {(double)a.n_rows, (double)a.n_cols, (double)a.nnz, (double)a.iters};
+            s_path = predict_smem(tree, xk);
+        }
+        __syncthreads();
+        if (s_path == KP_USE_KNOWN) {
+            // Known path never reads the matrix (SPEC.md:388 purity): CTA 0 answers.
+            if (blockIdx.x != 0) return;
+            __syncthreads();
+            load_tree(tree, a.known);
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                double xk[4] = {(double)a.n_rows, (double)a.n_cols, (double)a.nnz, (double)a.iters};
+                kp_outcome o = {};
+                o.kernel = predict_smem(tree, xk);
+                o.path = KP_USE_KNOWN;
+                o.status = KP_OK;
+                *a.out = o;
+            }
+            return;
+        }
+    }
+
+    int64_t lo = INT64_MAX, hi = INT64_MIN;
+    uint64_t s2 = 0;
+    stats_accum<O, kVec>(off, a.n_rows, lo, hi, s2);
+    block_reduce(lo, hi, s2);
+    if (threadIdx.x == 0) {
+        a.ws->part[blockIdx.x] = Partial{lo, hi, s2, 0};
+        __threadfence();
+        unsigned t = atomicAdd(&a.ws->ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // Last CTA: fold partials in fixed order.
+    lo = INT64_MAX; hi = INT64_MIN; s2 = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+        const Partial *p = &a.ws->part[i];
+        const int64_t plo = __ldcg(&p->lo), phi = __ldcg(&p->hi);
+        lo = plo < lo ? plo : lo;
+        hi = phi > hi ? phi : hi;
+        s2 += (uint64_t)__ldcg((const unsigned long long *)&p->s2);
+    }
+    __syncthreads();
+    block_reduce(lo, hi, s2);
+    if (a.mode == kModeSeer) {
+        __syncthreads();
+        load_tree(tree, a.gath);
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        a.ws->ticket = 0;  // reusable without memset
+        const int64_t n = a.n_rows;
+        if (n <= 0) { lo = hi = 0; s2 = 0; }
+        const int64_t s1 = n > 0 ? (int64_t)((uint64_t)ldo(off + n) - (uint64_t)ldo(off)) : 0;
+        if (a.mode == kModeStats) {
+            a.out4[0] = lo; a.out4[1] = hi; a.out4[2] = s1; a.out4[3] = (int64_t)s2;
+        } else {
+            kp_outcome o = {};
+            epilogue(lo, hi, s1, (int64_t)s2, n, a.n_cols, &o);
+            o.kernel = -1;
+            o.path = KP_USE_GATHERED;
+            if (a.mode == kModeSeer) {
+                double xg[8] = {(double)a.n_rows, (double)a.n_cols, (double)a.nnz, (double)a.iters,
+                                o.max_d, o.min_d, o.mean_d, o.var_d};
+                o.kernel = predict_smem(tree, xg);
+            }
+            *a.out = o;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ K2
+// Small waves (<= 4096 rows): a group of G lanes owns whole waves, lanes stride the
+// wave's rows; large waves: one CTA per wave.  Per-thread running sums of wave maxima
+// -> partials -> last CTA.  units = (len + div - 1) / div in C semantics (_core.pyx:46).
+template <typename O, int G>
+__global__ void __launch_bounds__(kRedThreads) k_wave_small(const O *__restrict__ off, int64_t n_rows,
+                                                            int64_t div, int64_t wave, int64_t *out,
+                                                            RedWorkspace *ws) {
+    __shared__ bool s_last;
+    const int lane = threadIdx.x & 31;
+    const int gl = lane % G;
+    constexpr int kGpw = 32 / G;  // groups (waves) per warp
+    const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t n_waves = (n_rows + wave - 1) / wave;
+    uint64_t sum = 0;
+    // warp-uniform outer loop: the full-mask shuffle below is executed by all lanes
+    for (int64_t wb = gwarp * kGpw; wb < n_waves; wb += nwarps * kGpw) {
+        const int64_t w = wb + lane / G;
+        int64_t m = 0;
+        if (w < n_waves) {
+            const int64_t r0 = w * wave;
+            int64_t r1 = r0 + wave;
+            if (r1 > n_rows) r1 = n_rows;
+            for (int64_t r = r0 + gl; r < r1; r += G) {
+                int64_t u = (ldo(off + r + 1) - ldo(off + r) + div - 1) / div;
+                m = u > m ? u : m;
+            }
+        }
+#pragma unroll
+        for (int o = G / 2; o; o >>= 1) {
+            int64_t t = __shfl_xor_sync(0xffffffffu, m, o);
+            m = t > m ? t : m;
+        }
+        if (gl == 0 && w < n_waves) sum += (uint64_t)m;
+    }
+    sum = warp_sum_u64(sum);
+    __shared__ uint64_t sw[32];
+    if (lane == 0) sw[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t t = 0;
+        for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += sw[i];
+        ws->part[blockIdx.x] = Partial{0, 0, t, 0};
+        __threadfence();
+        s_last = atomicAdd(&ws->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    if (threadIdx.x == 0) {
+        uint64_t t = 0;
+        for (int i = 0; i < (int)gridDim.x; ++i) t += ws->part[i].s2;
+        *out = (int64_t)t;
+        ws->ticket = 0;
+    }
+}
+
+template <typename O>
+__global__ void __launch_bounds__(1024) k_wave_large(const O *__restrict__ off, int64_t n_rows,
+                                                     int64_t div, int64_t wave, int64_t *out,
+                                                     RedWorkspace *ws) {
+    __shared__ bool s_last;
+    __shared__ int64_t sm[32];
+    const int lane = threadIdx.x & 31;
+    const int64_t n_waves = (n_rows + wave - 1) / wave;
+    uint64_t sum = 0;
+    for (int64_t w = blockIdx.x; w < n_waves; w += gridDim.x) {
+        const int64_t r0 = w * wave;
+        int64_t r1 = r0 + wave;
+        if (r1 > n_rows) r1 = n_rows;
+        int64_t m = 0;
+        for (int64_t r = r0 + threadIdx.x; r < r1; r += blockDim.x) {
+            int64_t u = (ldo(off + r + 1) - ldo(off + r) + div - 1) / div;
+            m = u > m ? u : m;
+        }
+        m = warp_max(m);
+        if (lane == 0) sm[threadIdx.x >> 5] = m;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int64_t mm = 0;
+            for (int i = 0; i < (int)(blockDim.x >> 5); ++i) mm = sm[i] > mm ? sm[i] : mm;
+            sum += (uint64_t)mm;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        ws->part[blockIdx.x] = Partial{0, 0, sum, 0};
+        __threadfence();
+        s_last = atomicAdd(&ws->ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    uint64_t t = 0;
+    for (int i = 0; i < (int)gridDim.x; ++i) t += ws->part[i].s2;
+    *out = (int64_t)t;
+    ws->ticket = 0;
+}
+
+// ------------------------------------------------------------------ batch predict
+__global__ void k_tree_predict(const void *tree, const double *__restrict__ x, int64_t n, int32_t nf,
+                               int32_t *__restrict__ out) {
+    __shared__ SmemTree t;
+    load_tree(t, tree);
+    __syncthreads();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double xv[16];
+        for (int f = 0; f < nf && f < 16; ++f) xv[f] = x[i * nf + f];
+        out[i] = predict_smem(t, xv);
+    }
+}
+
+// ------------------------------------------------------------------ launch helpers
+int grid_for(int64_t n_rows, int per_thread) {
+    int64_t want = (n_rows + (int64_t)kRedThreads * per_thread - 1) / ((int64_t)kRedThreads * per_thread);
+    int cap = num_sms() * 8;
+    if (cap > kMaxRedBlocks) cap = kMaxRedBlocks;
+    if (want < 1) want = 1;
+    return (int)(want < cap ? want : cap);
+}
+
+int launch_k1(K1Args a, int32_t off_type, cudaStream_t s) {
+    const bool aligned = ((uintptr_t)a.off & 15) == 0;
+    if (off_type == KP_I32) {
+        int g = grid_for(a.n_rows, 4);
+        if (aligned) k_row_stats<int32_t, true><<<g, kRedThreads, 0, s>>>(a);
+        else k_row_stats<int32_t, false><<<g, kRedThreads, 0, s>>>(a);
+    } else if (off_type == KP_I64) {
+        int g = grid_for(a.n_rows, 2);
+        if (aligned) k_row_stats<int64_t, true><<<g, kRedThreads, 0, s>>>(a);
+        else k_row_stats<int64_t, false><<<g, kRedThreads, 0, s>>>(a);
+    } else {
+        return KP_EINVAL;
+    }
+    KP_LAUNCHED();
+    return KP_OK;
+}
+
+template <typename O>
+int launch_wave(const O *off, int64_t n_rows, int64_t div, int64_t wave, int64_t *out, RedWorkspace *ws,
+                cudaStream_t s) {
+    const int64_t n_waves = (n_rows + wave - 1) / wave;
+    if (wave <= 4096) {
+        int G = 1;
+        while (G < wave && G < 32) G <<= 1;
+        const int64_t groups_per_block = kRedThreads / G;
+        int64_t want = (n_waves + groups_per_block - 1) / groups_per_block;
+        int cap = num_sms() * 8 < kMaxRedBlocks ? num_sms() * 8 : kMaxRedBlocks;
+        int g = (int)(want < cap ? (want < 1 ? 1 : want) : cap);
+        switch (G) {
+            case 1: k_wave_small<O, 1><<<g, kRedThreads, 0, s>>>(off, n_rows, div, wave, out, ws); break;
+            case 2: k_wave_small<O, 2><<<g, kRedThreads, 0, s>>>(off, n_rows, div, wave, out, ws); break;
+            case 4: k_wave_small<O, 4><<<g, kRedThreads, 0, s>>>(off, n_rows, div, wave, out, ws); break;
+            case 8: k_wave_small<O, 8><<<g, kRedThreads, 0, s>>>(off, n_rows, div, wave, out, ws); break;
+            case 16: k_wave_small<O, 16><<<g, kRedThreads, 0, s>>>(off, n_rows, div, wave, out, ws); break;
+            default: k_wave_small<O, 32><<<g, kRedThreads, 0, s>>>(off, n_rows, div, wave, out, ws); break;
+        }
+    } else {
+        int cap = num_sms() * 2 < kMaxRedBlocks ? num_sms() * 2 : kMaxRedBlocks;
+        int g = (int)(n_waves < cap ? n_waves : cap);
+        k_wave_large<O><<<g, 1024, 0, s>>>(off, n_rows, div, wave, out, ws);
+    }
+    KP_LAUNCHED();
+    return KP_OK;
+}
+
+}  // namespace
+}  // namespace kp
+
+using namespace kp;
+
+extern "C" {
+
+size_t kp_reduce_workspace_bytes(void) { return sizeof(RedWorkspace); }
+
+int kp_length_stats(const void *d_off, int32_t off_type, int64_t n_off, int64_t *d_out4, void *d_ws,
+                    void *stream) {
+    if (!d_out4 || !d_ws || n_off < 0 || (n_off > 0 && !d_off)) return KP_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = n_off - 1;
+    if (n <= 0) {  // _core.pyx:21-22 / _pure.py:14-15
+        KP_CUDA_TRY(cudaMemsetAsync(d_out4, 0, 4 * sizeof(int64_t), s));
+        return KP_OK;
+    }
+    K1Args a = {};
+    a.off = d_off; a.n_rows = n; a.mode = kModeStats; a.out4 = d_out4; a.ws = (RedWorkspace *)d_ws;
+    return launch_k1(a, off_type, s);
+}
+
+int kp_gather_features(const void *d_off, int32_t off_type, int64_t n_rows, int64_t n_cols,
+                       kp_outcome *d_out, void *d_ws, void *stream) {
+    if (n_rows <= 0 || n_cols <= 0 || !d_off || !d_out || !d_ws) return KP_EINVAL;
+    K1Args a = {};
+    a.off = d_off; a.n_rows = n_rows; a.n_cols = n_cols; a.mode = kModeFeatures; a.out = d_out;
+    a.ws = (RedWorkspace *)d_ws;
+    return launch_k1(a, off_type, (cudaStream_t)stream);
+}
+
+int kp_seer_select(const void *d_off, int32_t off_type, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                   int64_t iterations, const void *d_selector, const void *d_known, const void *d_gathered,
+                   kp_outcome *d_out, void *d_ws, void *stream) {
+    if (n_rows <= 0 || n_cols <= 0 || !d_off || !d_out || !d_ws || !d_selector || !d_known || !d_gathered)
+        return KP_EINVAL;
+    K1Args a = {};
+    a.off = d_off; a.n_rows = n_rows; a.n_cols = n_cols; a.nnz = nnz; a.iters = iterations;
+    a.mode = kModeSeer; a.out = d_out; a.sel = d_selector; a.known = d_known; a.gath = d_gathered;
+    a.ws = (RedWorkspace *)d_ws;
+    return launch_k1(a, off_type, (cudaStream_t)stream);
+}
+
+int kp_wave_ceil_max_sum(const void *d_off, int32_t off_type, int64_t n_off, int64_t divisor,
+                         int64_t wave_rows, int64_t *d_out1, void *d_ws, void *stream) {
+    if (divisor <= 0 || wave_rows <= 0 || !d_out1 || !d_ws || n_off < 0) return KP_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t n = n_off - 1;
+    if (n <= 0) {
+        KP_CUDA_TRY(cudaMemsetAsync(d_out1, 0, sizeof(int64_t), s));
+        return KP_OK;
+    }
+    RedWorkspace *ws = (RedWorkspace *)d_ws;
+    if (off_type == KP_I32) return launch_wave((const int32_t *)d_off, n, divisor, wave_rows, d_out1, ws, s);
+    if (off_type == KP_I64) return launch_wave((const int64_t *)d_off, n, divisor, wave_rows, d_out1, ws, s);
+    return KP_EINVAL;
+}
+
+int kp_tree_predict(const void *d_tree, const double *d_x, int64_t n, int32_t n_feat, int32_t *d_out,
+                    void *stream) {
+    if (!d_tree || n < 0 || n_feat <= 0 || n_feat > 16) return KP_EINVAL;
+    if (n == 0) return KP_OK;
+    int64_t want = (n + 255) / 256;
+    int g = (int)(want < num_sms() * 8 ? want : num_sms() * 8);
+    k_tree_predict<<<g, 256, 0, (cudaStream_t)stream>>>(d_tree, d_x, n, n_feat, d_out);
+    KP_LAUNCHED();
+    return KP_OK;
+}
+
+uint64_t kp_launch_count(void) { return (uint64_t)kp::g_launches; }
+const char *kp_version(void) { return "kpb200 0.1.0 sm_100a"; }
+
+}  // extern "C"

@@ -1,0 +1,1158 @@
+// kp_spmv.cu -- the SpMV kernel family Seer selects between (Table III
+// order :311-318) and the preprocessing the cost model charges (
+// PAPER.md:280).  sm_100a, CUDA cores + LSU / TMA-bulk; no tensor cores (SpMV is
+// ~0.2 flop/B, far below the ridge).
+//
+//   id kernel          schedule                                         prep
+//   0  Adaptive-CSR    row blocks: short rows staged in smem (stream),   K13 (flags+scan)
+//                      long rows split into CTA pieces (vector-L)
+//   1  CSR,BM          one CTA per row, block reduction                 -
+//   2  CSR,MP          merge-path CTA tiles (Merrill & Garland), smem    K10 partition
+//   3  CSR,WM          G lanes per row (G = 2..32 from nnz/rows), shfl   -
+//   4  CSR,WO          merge-path tiles, in-kernel 32-ary diagonal search -
+//   5  CSR,TM          thread per row; each CTA's nnz window staged into K-
+//                      smem by 1-D TMA bulk copies (double buffered)
+//   6  COO,WM          warp owns 256 nnz, blocked loads, segmented scan  K11 row ids
+//   7  ELL,TM          column-major ELL, thread per row (+CSR tail)      K12 (+K1 width)
+//
+// Determinism: no floating-point atomics anywhere.  Rows split across work units are
+// finished by k_carry_fixup, which sums the carries of a run of units in a fixed
+// (lane-strided + shuffle-tree) order, so y is bit-identical run to run.
+#include "kp_internal.cuh"
+
+namespace kp {
+int launch_k1_stats_into(const void *off, int32_t off_type, int64_t n_rows, int64_t *out4, void *ws,
+                         cudaStream_t s);
+}
+
+namespace kp {
+namespace {
+
+constexpr int kAlign = 256;
+__host__ __device__ constexpr size_t align_up(size_t v, size_t a = kAlign) { return (v + a - 1) / a * a; }
+
+// ---------------------------------------------------------------- prepared layout
+struct PrepHeader {
+    int64_t kernel;
+    int64_t n_units;   // device-written for adaptive
+    int64_t stats[4];  // ELL: (lo, hi, s1, s2) of row lengths (K1)
+    int64_t cap;       // ELL reserved width
+    int64_t pad[9];
+};
+static_assert(sizeof(PrepHeader) <= kAlign, "header");
+constexpr size_t kRedWsBytes = 40960;  // >= kp_reduce_workspace_bytes()
+
+// ---------------------------------------------------------------- tunables
+constexpr int kTile = 256;      // threads per CTA for the tile kernels
+constexpr int kIPT = 8;         // merge items / nnz per thread
+constexpr int kMergeTile = kTile * kIPT;  // 2048 merge items per CTA tile
+constexpr int kCooChunk = 32 * kIPT;      // 256 nnz per warp
+constexpr int kTmRows = 256;              // CSR,TM rows per CTA tile
+constexpr int kTmCap = 4096;              // CSR,TM staged nnz per stage
+constexpr int kAdBlockNnz = 2048;         // adaptive: nnz window of a short row block
+constexpr int kAdLongT = 1024;            // adaptive: rows longer than this are "long"
+constexpr int kAdCap = kAdBlockNnz + kAdLongT;
+constexpr int kAdRows = 256;              // adaptive: max rows per short block
+constexpr int64_t kAdLongChunk = 8192;    // adaptive: nnz per long-row piece
+
+template <typename V>
+__device__ __forceinline__ V fma_acc(V acc, V a, V b) { return fma(a, b, acc); }
+
+// ================================================================= CSR,WM (K4)
+template <typename V, typename O, int G>
+__global__ void __launch_bounds__(256) k_csr_wm(const O *__restrict__ off, const int32_t *__restrict__ col,
+                                                const V *__restrict__ val, const V *__restrict__ x,
+                                                V *__restrict__ y, int64_t n_rows) {
+    const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) / G;
+    if (row >= n_rows) return;  // whole groups exit together (G divides 32)
+    const int gl = threadIdx.x % G;
+    const int64_t s = ldo(off + row), e = ldo(off + row + 1);
+    V sum = 0;
+    int64_t j = s + gl;
+    for (; j + 3 * G < e; j += 4 * G) {  // 4 independent gathers in flight per lane
+        const int32_t c0 = ld_stream(col + j), c1 = ld_stream(col + j + G), c2 = ld_stream(col + j + 2 * G),
+                      c3 = ld_stream(col + j + 3 * G);
+        const V v0 = ld_stream(val + j), v1 = ld_stream(val + j + G), v2 = ld_stream(val + j + 2 * G),
+                v3 = ld_stream(val + j + 3 * G);
+        sum = fma_acc(sum, v0, ld_x(x + c0));
+        sum = fma_acc(sum, v1, ld_x(x + c1));
+        sum = fma_acc(sum, v2, ld_x(x + c2));
+        sum = fma_acc(sum, v3, ld_x(x + c3));
+    }
+    for (; j < e; j += G) sum = fma_acc(sum, ld_stream(val + j), ld_x(x + ld_stream(col + j)));
+    if constexpr (G > 1) {
+        const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) sum += __shfl_xor_sync(mask, sum, o);
+    }
+    if (gl == 0) y[row] = sum;
+}
+
+// ================================================================= CSR,BM (K5)
+template <typename V>
+__device__ __forceinline__ V block_sum(V v, V *sred) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    v = group_sum<32>(v);
+    if (lane == 0) sred[w] = v;
+    __syncthreads();
+    V t = 0;
+    if (w == 0) {
+        t = lane < (int)(blockDim.x >> 5) ? sred[lane] : V(0);
+        t = group_sum<32>(t);
+    }
+    return t;  // valid in thread 0
+}
+
+template <typename V, typename O>
+__global__ void __launch_bounds__(128) k_csr_bm(const O *__restrict__ off, const int32_t *__restrict__ col,
+                                                const V *__restrict__ val, const V *__restrict__ x,
+                                                V *__restrict__ y, int64_t n_rows) {
+    __shared__ V sred[32];
+    for (int64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
+        const int64_t s = ldo(off + row), e = ldo(off + row + 1);
+        V sum = 0;
+        int64_t j = s + threadIdx.x;
+        for (; j + 128 < e; j += 256) {
+            const int32_t c0 = ld_stream(col + j), c1 = ld_stream(col + j + 128);
+            const V v0 = ld_stream(val + j), v1 = ld_stream(val + j + 128);
+            sum = fma_acc(sum, v0, ld_x(x + c0));
+            sum = fma_acc(sum, v1, ld_x(x + c1));
+        }
+        if (j < e) sum = fma_acc(sum, ld_stream(val + j), ld_x(x + ld_stream(col + j)));
+        V t = block_sum(sum, sred);
+        if (threadIdx.x == 0) y[row] = t;
+        __syncthreads();
+    }
+}
+
+// ================================================================= CSR,TM (K3)
+// Thread per row.  A persistent CTA walks row tiles of 256 rows; the tile's nnz
+// window [off[r0], off[r0+256]) is pulled into shared memory by two 1-D TMA bulk
+// copies (cols, vals) completing on an mbarrier, double buffered so tile i+1 lands
+// while tile i is reduced.  Tiles whose window exceeds the stage fall back to
+// direct (per-thread) global walks.
+template <typename V>
+struct TmStage {
+    int32_t col[kTmCap];
+    V val[kTmCap];
+};
+
+template <typename V, typename O, bool kTma>
+__global__ void __launch_bounds__(kTmRows) k_csr_tm(const O *__restrict__ off, const int32_t *__restrict__ col,
+                                                    const V *__restrict__ val, const V *__restrict__ x,
+                                                    V *__restrict__ y, int64_t n_rows) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    TmStage<V> *stage = reinterpret_cast<TmStage<V> *>(smem_raw);
+    __shared__ __align__(8) uint64_t bar[2];
+    __shared__ int64_t s_base[2];  // element index staged at stage[k].col[0]; -1 = direct
+    const int64_t n_tiles = (n_rows + kTmRows - 1) / kTmRows;
+    const int tid = threadIdx.x;
+
+    // Issue (thread 0 only) the staging of tile t into stage k.
+    auto issue = [&](int64_t t, int k) {
+        const int64_t r0 = t * kTmRows;
+        int64_t r1 = r0 + kTmRows;
+        if (r1 > n_rows) r1 = n_rows;
+        const int64_t s = ldo(off + r0), e = ldo(off + r1);
+        const int64_t a = s & ~(int64_t)3;   // 16-byte aligned start (4 elements)
+        const int64_t ea = e & ~(int64_t)3;  // aligned end; tail [ea, e) by hand
+        if (!kTma || e - a > kTmCap || ea <= a) {
+            if (kTma && e - a <= kTmCap && e > s) {
+                // tiny window: copy by hand
+                for (int64_t j = a; j < e; ++j) {
+                    stage[k].col[j - a] = __ldg(col + j);
+                    stage[k].val[j - a] = __ldg(val + j);
+                }
+                s_base[k] = a;
+            } else {
+                s_base[k] = (e > s && e - a <= kTmCap) ? a : -1;
+                if (!kTma) s_base[k] = -1;
+            }
+            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar[k])) : "memory");
+            return;
+        }
+        for (int64_t j = ea; j < e; ++j) {  // < 4 tail elements
+            stage[k].col[j - a] = __ldg(col + j);
+            stage[k].val[j - a] = __ldg(val + j);
+        }
+        s_base[k] = a;
+        const uint32_t n = (uint32_t)(ea - a);
+        mbar_arrive_expect_tx(&bar[k], n * (uint32_t)(sizeof(int32_t) + sizeof(V)));
+        bulk_g2s(stage[k].col, col + a, n * (uint32_t)sizeof(int32_t), &bar[k]);
+        bulk_g2s(stage[k].val, val + a, n * (uint32_t)sizeof(V), &bar[k]);
+    };
+
+    if (tid == 0) {
+        mbar_init(&bar[0], 1);
+        mbar_init(&bar[1], 1);
+        fence_barrier_init();
+    }
+    __syncthreads();
+    int64_t t = blockIdx.x;
+    if (tid == 0 && t < n_tiles) issue(t, 0);
+    for (int i = 0; t < n_tiles; ++i, t += gridDim.x) {
+        const int k = i & 1;
+        const int64_t tn = t + gridDim.x;
+        if (tid == 0 && tn < n_tiles) {
+            fence_proxy_async();
+            issue(tn, k ^ 1);
+        }
+        const int64_t row = t * kTmRows + tid;
+        int64_t s = 0, e = 0;
+        if (row < n_rows) { s = ldo(off + row); e = ldo(off + row + 1); }
+        mbar_wait(&bar[k], (uint32_t)((i >> 1) & 1));
+        const int64_t base = s_base[k];
+        V sum = 0;
+        if (row < n_rows) {
+            if (base >= 0) {
+                const int32_t *sc = stage[k].col - base;
+                const V *sv = stage[k].val - base;
+                for (int64_t j = s; j < e; ++j) sum = fma_acc(sum, sv[j], ld_x(x + sc[j]));
+            } else {
+                for (int64_t j = s; j < e; ++j) sum = fma_acc(sum, __ldg(val + j), ld_x(x + __ldg(col + j)));
+            }
+            y[row] = sum;
+        }
+        __syncthreads();  // stage k fully consumed before it is refilled at i+1
+    }
+}
+
+// ================================================================= ELL,TM (K9 + K12)
+template <typename V, typename O>
+__global__ void __launch_bounds__(256) k_ell_tm(const PrepHeader *__restrict__ hdr, const int32_t *__restrict__ ecol,
+                                                const V *__restrict__ evalv, const O *__restrict__ off,
+                                                const int32_t *__restrict__ col, const V *__restrict__ val,
+                                                const V *__restrict__ x, V *__restrict__ y, int64_t n_rows) {
+    const int64_t row = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (row >= n_rows) return;
+    const int64_t wmax = __ldg(&hdr->stats[1]);
+    const int64_t cap = __ldg(&hdr->cap);
+    const int64_t W = wmax < cap ? wmax : cap;
+    V sum = 0;
+    int64_t k = 0;
+    const int32_t *pc = ecol + row;
+    const V *pv = evalv + row;
+    for (; k + 3 < W; k += 4) {
+        const int32_t c0 = ld_stream(pc + (k + 0) * n_rows), c1 = ld_stream(pc + (k + 1) * n_rows),
+                      c2 = ld_stream(pc + (k + 2) * n_rows), c3 = ld_stream(pc + (k + 3) * n_rows);
+        const V v0 = ld_stream(pv + (k + 0) * n_rows), v1 = ld_stream(pv + (k + 1) * n_rows),
+                v2 = ld_stream(pv + (k + 2) * n_rows), v3 = ld_stream(pv + (k + 3) * n_rows);
+        sum = fma_acc(sum, v0, ld_x(x + c0));
+        sum = fma_acc(sum, v1, ld_x(x + c1));
+        sum = fma_acc(sum, v2, ld_x(x + c2));
+        sum = fma_acc(sum, v3, ld_x(x + c3));
+    }
+    for (; k < W; ++k) sum = fma_acc(sum, ld_stream(pv + k * n_rows), ld_x(x + ld_stream(pc + k * n_rows)));
+    if (wmax > cap) {  // hybrid tail: rows longer than the reserved width continue in CSR
+        const int64_t s = ldo(off + row), e = ldo(off + row + 1);
+        for (int64_t j = s + W; j < e; ++j) sum = fma_acc(sum, __ldg(val + j), ld_x(x + __ldg(col + j)));
+    }
+    y[row] = sum;
+}
+
+// K12: CSR -> column-major ELL of width min(max_len, cap); padding = (col 0, val 0).
+template <typename V, typename O>
+__global__ void __launch_bounds__(256) k_prep_ell(const PrepHeader *__restrict__ hdr, const O *__restrict__ off,
+                                                  const int32_t *__restrict__ col, const V *__restrict__ val,
+                                                  int32_t *__restrict__ ecol, V *__restrict__ evalv, int64_t n_rows) {
+    const int64_t row = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (row >= n_rows) return;
+    const int64_t wmax = __ldg(&hdr->stats[1]);
+    const int64_t cap = __ldg(&hdr->cap);
+    const int64_t W = wmax < cap ? wmax : cap;
+    const int64_t s = ldo(off + row), e = ldo(off + row + 1);
+    for (int64_t k = 0; k < W; ++k) {
+        const int64_t j = s + k;
+        const bool in = j < e;
+        ecol[k * n_rows + row] = in ? __ldg(col + j) : 0;
+        evalv[k * n_rows + row] = in ? __ldg(val + j) : V(0);
+    }
+}
+
+// ================================================================= carries / fix-up
+// A unit u (COO chunk, merge tile, adaptive long piece) that leaves row rho unfinished
+// records carry_row[u] = rho, carry_val[u] = its partial (carry_row = -1: none).  The
+// unit that finishes rho wrote y[rho] = its own partial.  Fix-up: each warp takes 32
+// units; for every run start (carry_row[u] >= 0, != carry_row[u-1]) the whole warp
+// sums the run's carries (lane-strided, shuffle tree: fixed order) into y[rho].
+template <typename V>
+__global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__ crow, const V *__restrict__ cval,
+                                                     const int64_t *__restrict__ n_units_dev, int64_t n_units_host,
+                                                     V *__restrict__ y) {
+    const int64_t n_units = n_units_dev ? *n_units_dev : n_units_host;
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
+    if (wbase >= n_units) return;
+    const int64_t u = wbase + lane;
+    int32_t r = -1;
+    bool start = false;
+    if (u < n_units) {
+        r = crow[u];
+        start = r >= 0 && (u == 0 || crow[u - 1] != r);
+    }
+    unsigned starts = __ballot_sync(0xffffffffu, start);
+    while (starts) {
+        const int src = __ffs(starts) - 1;
+        starts &= starts - 1;
+        const int32_t rho = __shfl_sync(0xffffffffu, r, src);
+        const int64_t u0 = wbase + src;
+        V acc = 0;
+        for (int64_t b = u0;; b += 32) {
+            const int64_t q = b + lane;
+            const bool in = q < n_units && crow[q] == rho;
+            if (in) acc += cval[q];
+            const unsigned m = __ballot_sync(0xffffffffu, in);
+            if (m != 0xffffffffu) break;  // run ended inside this batch (runs are contiguous)
+        }
+        acc = group_sum<32>(acc);
+        if (lane == 0) y[rho] += acc;
+    }
+}
+
+// ================================================================= block-level segmented scan
+// Inclusive scan over threads of (flag, value) with op (fa,va)o(fb,vb) = (fa|fb, fb ? vb : va+vb).
+template <typename V>
+struct SegPair {
+    int f;
+    V v;
+};
+template <typename V>
+__device__ __forceinline__ SegPair<V> seg_op(SegPair<V> a, SegPair<V> b) {
+    return SegPair<V>{a.f | b.f, b.f ? b.v : a.v + b.v};
+}
+// Returns the EXCLUSIVE prefix for this thread (identity: f=0, v=0) and the block total.
+template <typename V>
+__device__ __forceinline__ SegPair<V> block_seg_exscan(SegPair<V> p, SegPair<V> &total, SegPair<V> *swarp) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    SegPair<V> inc = p;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        SegPair<V> t{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
+        if (lane >= o) inc = seg_op(t, inc);
+    }
+    if (lane == 31) swarp[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        SegPair<V> wv = lane < nw ? swarp[lane] : SegPair<V>{0, V(0)};
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            SegPair<V> t{__shfl_up_sync(0xffffffffu, wv.f, o), __shfl_up_sync(0xffffffffu, wv.v, o)};
+            if (lane >= o) wv = seg_op(t, wv);
+        }
+        if (lane < nw) swarp[lane] = wv;  // inclusive warp prefixes
+    }
+    __syncthreads();
+    SegPair<V> ex{__shfl_up_sync(0xffffffffu, inc.f, 1), __shfl_up_sync(0xffffffffu, inc.v, 1)};
+    if (lane == 0) ex = SegPair<V>{0, V(0)};
+    if (w > 0) ex = seg_op(swarp[w - 1], ex);
+    total = swarp[nw - 1];
+    return ex;
+}
+
+// ================================================================= merge-path tiles (K6 MP, K7 WO)
+// Merge of A = row ends off[1..R] with B = nnz indices 0..Z-1 (Merrill & Garland).
+// Diagonal d -> (i rows consumed, d - i nnz consumed).
+template <typename O>
+__device__ __forceinline__ int64_t merge_search_global(const O *off, int64_t n_rows, int64_t nnz, int64_t d) {
+    int64_t lo = d - nnz > 0 ? d - nnz : 0;
+    int64_t hi = d < n_rows ? d : n_rows;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ldo(off + mid + 1) <= d - mid - 1) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// Warp-cooperative 32-ary version (5 rounds of 32 parallel probes for 2^25 items).
+template <typename O>
+__device__ __forceinline__ int64_t merge_search_warp(const O *off, int64_t n_rows, int64_t nnz, int64_t d) {
+    const int lane = threadIdx.x & 31;
+    int64_t lo = d - nnz > 0 ? d - nnz : 0;
+    int64_t hi = d < n_rows ? d : n_rows;
+    while (hi - lo > 32) {
+        const int64_t step = (hi - lo + 32) / 33;  // probes at lo + step*(lane+1) - 1
+        int64_t p = lo + step * (lane + 1) - 1;
+        if (p >= hi) p = hi - 1;
+        const bool go_right = ldo(off + p + 1) <= d - p - 1;  // predicate monotone in p
+        const unsigned m = __ballot_sync(0xffffffffu, go_right);
+        const int cnt = __popc(m);  // lanes 0..cnt-1 true (monotone)
+        int64_t nlo = cnt == 0 ? lo : (lo + step * cnt - 1) + 1;
+        int64_t nhi = cnt == 32 ? hi : lo + step * (cnt + 1) - 1;
+        if (nhi > hi) nhi = hi;
+        if (nlo > nhi) nlo = nhi;
+        lo = nlo;
+        hi = nhi;
+    }
+    // final <= 32 candidates: one probe per lane
+    const int64_t p = lo + lane;
+    const bool gr = p < hi && ldo(off + p + 1) <= d - p - 1;
+    return lo + __popc(__ballot_sync(0xffffffffu, gr));
+}
+
+template <typename V, typename O>
+struct MergeSmem {
+    int64_t row_end[kMergeTile + 1];
+    V prod[kMergeTile];
+    SegPair<V> swarp[32];
+    int64_t coord[4];
+};
+
+// kPrep: tile coordinates from the K10 partition (CSR,MP); else searched in-kernel (CSR,WO).
+template <typename V, typename O, bool kPrep>
+__global__ void __launch_bounds__(kTile) k_csr_merge(const O *__restrict__ off, const int32_t *__restrict__ col,
+                                                     const V *__restrict__ val, const V *__restrict__ x,
+                                                     V *__restrict__ y, int64_t n_rows, int64_t nnz,
+                                                     const int64_t *__restrict__ part, int32_t *__restrict__ crow,
+                                                     V *__restrict__ cval) {
+    __shared__ MergeSmem<V, O> sm;
+    const int64_t tile = blockIdx.x;
+    const int64_t total = n_rows + nnz;
+    const int64_t d0 = tile * kMergeTile;
+    const int64_t d1 = d0 + kMergeTile < total ? d0 + kMergeTile : total;
+    if (kPrep) {
+        if (threadIdx.x < 2) sm.coord[threadIdx.x] = part[tile + threadIdx.x];
+    } else {
+        const int w = threadIdx.x >> 5;
+        if (w < 2) {
+            const int64_t d = w == 0 ? d0 : d1;
+            const int64_t i = merge_search_warp(off, n_rows, nnz, d);
+            if ((threadIdx.x & 31) == 0) sm.coord[w] = i;
+        }
+    }
+    __syncthreads();
+    const int64_t r0 = sm.coord[0], r1 = sm.coord[1];
+    const int64_t j0 = d0 - r0, j1 = d1 - r1;
+    const int nr = (int)(r1 - r0);  // row ends consumed in this tile
+    const int nz = (int)(j1 - j0);
+    // stage row ends (rows r0 .. r0+nr, the last one = row in progress) and products
+    const int nre = (r1 < n_rows) ? nr + 1 : nr;
+    for (int k = threadIdx.x; k < nre; k += kTile) sm.row_end[k] = ldo(off + r0 + 1 + k);
+    for (int k = threadIdx.x; k < nz; k += kTile) {
+        const int64_t j = j0 + k;
+        sm.prod[k] = ld_stream(val + j) * ld_x(x + ld_stream(col + j));
+    }
+    __syncthreads();
+    // thread-local merge of kIPT items starting at local diagonal t*kIPT
+    const int dt = threadIdx.x * kIPT;
+    int i, jj;
+    {
+        int lo = dt - nz > 0 ? dt - nz : 0;
+        int hi = dt < nr ? dt : nr;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (sm.row_end[mid] <= j0 + (dt - mid - 1)) lo = mid + 1;
+            else hi = mid;
+        }
+        i = lo;
+        jj = dt - lo;
+    }
+    V acc = 0;
+    int first_row = -1;
+    V first_val = 0;
+    const int dend = dt + kIPT < nr + nz ? dt + kIPT : nr + nz;
+    for (int d = dt; d < dend; ++d) {
+        if (i < nr && sm.row_end[i] <= j0 + jj) {  // row r0+i ends here
+            if (first_row < 0) { first_row = i; first_val = acc; }
+            else y[r0 + i] = acc;
+            acc = 0;
+            ++i;
+        } else {
+            acc += sm.prod[jj];
+            ++jj;
+        }
+    }
+    SegPair<V> tot;
+    SegPair<V> ex = block_seg_exscan(SegPair<V>{first_row >= 0 ? 1 : 0, acc}, tot, sm.swarp);
+    if (first_row >= 0) y[r0 + first_row] = first_val + ex.v;
+    if (threadIdx.x == kTile - 1) {
+        // carry-out: the row in progress at the tile end (tot = its partial in this tile)
+        const bool has = r1 < n_rows && nz > 0;
+        crow[tile] = has ? (int32_t)r1 : -1;
+        cval[tile] = has ? tot.v : V(0);
+    }
+}
+
+// K10: merge-path partition, one thread per tile boundary.
+template <typename O>
+__global__ void k_prep_mp(const O *__restrict__ off, int64_t n_rows, int64_t nnz, int64_t n_tiles,
+                          int64_t *__restrict__ part) {
+    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > n_tiles) return;
+    const int64_t total = n_rows + nnz;
+    const int64_t d = p * kMergeTile < total ? p * kMergeTile : total;
+    part[p] = merge_search_global(off, n_rows, nnz, d);
+}
+
+// ================================================================= COO,WM (K8 + K11)
+// Each warp owns 256 consecutive nnz; lane l the 8 at [base + 8l, base + 8l + 8)
+// (blocked; 32-byte vector loads).  Warp segmented scan by row id; a row finished in
+// the chunk is written, the row left open at the chunk end becomes the carry.
+// Empty rows (gaps between consecutive row ids) are zero-filled by the element
+// that follows the gap, so y needs no memset.
+template <typename V>
+__global__ void __launch_bounds__(256) k_coo_wm(const int32_t *__restrict__ rid, const int32_t *__restrict__ col,
+                                                const V *__restrict__ val, const V *__restrict__ x,
+                                                V *__restrict__ y, int64_t n_rows, int64_t nnz,
+                                                int32_t *__restrict__ crow, V *__restrict__ cval) {
+    const int lane = threadIdx.x & 31;
+    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int64_t base = chunk * kCooChunk;
+    if (base >= nnz) return;
+    const int64_t j0 = base + lane * kIPT;
+    int32_t r[kIPT];
+    V p[kIPT];
+    const bool full = base + kCooChunk <= nnz;
+    if (full) {
+        const int4 *rp = reinterpret_cast<const int4 *>(rid + j0);
+        const int4 *cp = reinterpret_cast<const int4 *>(col + j0);
+        int4 ra = ld_stream4(rp), rb = ld_stream4(rp + 1);
+        int4 ca = ld_stream4(cp), cb = ld_stream4(cp + 1);
+        r[0] = ra.x; r[1] = ra.y; r[2] = ra.z; r[3] = ra.w; r[4] = rb.x; r[5] = rb.y; r[6] = rb.z; r[7] = rb.w;
+        const int32_t c[kIPT] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+#pragma unroll
+        for (int k = 0; k < kIPT; ++k) p[k] = ld_stream(val + j0 + k) * ld_x(x + c[k]);
+    } else {
+#pragma unroll
+        for (int k = 0; k < kIPT; ++k) {
+            const int64_t j = j0 + k;
+            if (j < nnz) {
+                r[k] = ld_stream(rid + j);
+                p[k] = ld_stream(val + j) * ld_x(x + ld_stream(col + j));
+            } else {
+                r[k] = INT32_MAX;  // sentinel past the end: never written
+                p[k] = 0;
+            }
+        }
+    }
+    // previous element's row (for heads and gap fill)
+    int32_t prev = __shfl_up_sync(0xffffffffu, r[kIPT - 1], 1);
+    if (lane == 0) prev = base > 0 ? __ldg(rid + base - 1) : -1;
+    // next element's row (for row ends)
+    int32_t next = __shfl_down_sync(0xffffffffu, r[0], 1);
+    if (lane == 31) next = (base + kCooChunk < nnz) ? __ldg(rid + base + kCooChunk) : INT32_MAX;
+    // thread-local segmented inclusive scan; elements before the lane's first head
+    // continue the previous lane's segment (carry_in from the warp scan below)
+    V acc[kIPT];
+    int first_head_k = kIPT;
+    {
+        int32_t pr = prev;
+#pragma unroll
+        for (int k = 0; k < kIPT; ++k) {
+            const bool head = r[k] != pr;
+            if (head && first_head_k == kIPT) first_head_k = k;
+            acc[k] = (head || k == 0) ? p[k] : acc[k - 1] + p[k];
+            pr = r[k];
+        }
+    }
+    // warp exclusive segmented scan of (has_head, last-segment sum)
+    SegPair<V> inc{first_head_k < kIPT ? 1 : 0, acc[kIPT - 1]};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        SegPair<V> t{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
+        if (lane >= o) inc = seg_op(t, inc);
+    }
+    SegPair<V> ex{__shfl_up_sync(0xffffffffu, inc.f, 1), __shfl_up_sync(0xffffffffu, inc.v, 1)};
+    if (lane == 0) ex = SegPair<V>{0, V(0)};
+    const V carry_in = ex.v;  // applies to elements before this lane's first head
+    // gap fill + row ends
+    int32_t pr = prev;
+#pragma unroll
+    for (int k = 0; k < kIPT; ++k) {
+        const int32_t rk = r[k];
+        if (rk != INT32_MAX) {
+            // rows strictly between pr and rk are empty
+            for (int64_t g = (int64_t)pr + 1; g < rk; ++g) y[g] = V(0);
+            const int32_t nx = (k + 1 < kIPT) ? r[k + 1] : next;
+            const V v = (k < first_head_k) ? acc[k] + carry_in : acc[k];
+            // row ends here (rows continued from earlier chunks get their carries in the fix-up)
+            if (nx != rk) y[rk] = v;
+            // trailing empty rows after the very last nnz
+            if (j0 + k == nnz - 1)
+                for (int64_t g = (int64_t)rk + 1; g < n_rows; ++g) y[g] = V(0);
+            pr = rk;
+        }
+    }
+    // carry: the row open at the chunk end continues into the next chunk
+    if (lane == 31) {
+        const int32_t rl = r[kIPT - 1];
+        const bool open = (base + kCooChunk < nnz) && next == rl;
+        crow[chunk] = open ? rl : -1;
+        cval[chunk] = open ? ((kIPT - 1 < first_head_k) ? acc[kIPT - 1] + carry_in : acc[kIPT - 1]) : V(0);
+    }
+}
+
+// K11: CSR -> COO row ids.  Thread per 8 nnz: binary search of the first row, then walk.
+template <typename O>
+__global__ void __launch_bounds__(256) k_prep_coo(const O *__restrict__ off, int64_t n_rows, int64_t nnz,
+                                                  int32_t *__restrict__ rid) {
+    const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kIPT;
+    if (j0 >= nnz) return;
+    // row = upper_bound(off, j0) - 1, over off[0..n_rows]
+    int64_t lo = 0, hi = n_rows;  // answer in [0, n_rows-1]
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (ldo(off + mid) <= j0) lo = mid;
+        else hi = mid - 1;
+    }
+    int64_t r = lo;
+    int64_t rend = ldo(off + r + 1);
+    for (int k = 0; k < kIPT; ++k) {
+        const int64_t j = j0 + k;
+        if (j >= nnz) break;
+        while (j >= rend) { ++r; rend = ldo(off + r + 1); }
+        rid[j] = (int32_t)r;
+    }
+}
+
+// ================================================================= Adaptive-CSR (K13)
+// Units: a "short block" of consecutive rows (each <= kAdLongT nnz) whose starts fall in
+// one kAdBlockNnz window and one kAdRows row window, or one kAdLongChunk piece of a
+// long row.  unit_row[u] = first row; unit_piece[u] = -1 (short) or piece index.
+// The short block's last row is unit_row[u+1] (or n_rows).
+template <typename O>
+__device__ __forceinline__ int64_t ad_units_of_row(const O *off, int64_t r, int64_t n_rows) {
+    const int64_t len = ldo(off + r + 1) - ldo(off + r);
+    if (len > kAdLongT) return (len + kAdLongChunk - 1) / kAdLongChunk;
+    if (r == 0) return 1;
+    const int64_t plen = ldo(off + r) - ldo(off + r - 1);
+    if (plen > kAdLongT) return 1;
+    if (r % kAdRows == 0) return 1;
+    if (ldo(off + r) / kAdBlockNnz != ldo(off + r - 1) / kAdBlockNnz) return 1;
+    return 0;
+}
+
+constexpr int kScanItems = 256 * 16;  // rows per scan block
+
+template <typename O>
+__global__ void __launch_bounds__(256) k_ad_count(const O *__restrict__ off, int64_t n_rows,
+                                                  int64_t *__restrict__ bsum) {
+    __shared__ int64_t sw[8];
+    const int64_t r0 = (int64_t)blockIdx.x * kScanItems;
+    int64_t c = 0;
+    for (int k = threadIdx.x; k < kScanItems; k += 256) {
+        const int64_t r = r0 + k;
+        if (r < n_rows) c += ad_units_of_row(off, r, n_rows);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0) sw[threadIdx.x >> 5] = c;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int64_t t = 0;
+        for (int i = 0; i < 8; ++i) t += sw[i];
+        bsum[blockIdx.x] = t;
+    }
+}
+
+// single CTA: exclusive scan of block sums in place, total -> *total
+__global__ void __launch_bounds__(1024) k_scan_bsum(int64_t *__restrict__ bsum, int64_t nb, int64_t *__restrict__ total) {
+    __shared__ int64_t sw[32];
+    __shared__ int64_t s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    for (int64_t b0 = 0; b0 < nb; b0 += 1024) {
+        const int64_t i = b0 + threadIdx.x;
+        const int64_t v = i < nb ? bsum[i] : 0;
+        int64_t inc = v;
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += t;
+        }
+        if (lane == 31) sw[w] = inc;
+        __syncthreads();
+        if (w == 0) {
+            int64_t wv = sw[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                int64_t t = __shfl_up_sync(0xffffffffu, wv, o);
+                if (lane >= o) wv += t;
+            }
+            sw[lane] = wv;
+        }
+        __syncthreads();
+        const int64_t excl = s_carry + (w > 0 ? sw[w - 1] : 0) + inc - v;
+        if (i < nb) bsum[i] = excl;
+        __syncthreads();
+        if (threadIdx.x == 1023) s_carry = excl + v;
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *total = s_carry;
+}
+
+template <typename O>
+__global__ void __launch_bounds__(256) k_ad_write(const O *__restrict__ off, int64_t n_rows,
+                                                  const int64_t *__restrict__ bsum, int32_t *__restrict__ urow,
+                                                  int32_t *__restrict__ upiece) {
+    // each thread owns 16 consecutive rows of the block (blocked), scans locally
+    __shared__ int64_t sw[8];
+    constexpr int kPer = kScanItems / 256;
+    const int64_t r0 = (int64_t)blockIdx.x * kScanItems + threadIdx.x * kPer;
+    int64_t cnt[kPer];
+    int64_t tsum = 0;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int64_t r = r0 + k;
+        cnt[k] = r < n_rows ? ad_units_of_row(off, r, n_rows) : 0;
+        tsum += cnt[k];
+    }
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    int64_t inc = tsum;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) sw[w] = inc;
+    __syncthreads();
+    int64_t wpre = 0;
+    for (int i = 0; i < w; ++i) wpre += sw[i];
+    int64_t u = bsum[blockIdx.x] + wpre + inc - tsum;
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+        const int64_t r = r0 + k;
+        if (cnt[k] == 0) continue;
+        const int64_t len = ldo(off + r + 1) - ldo(off + r);
+        if (len > kAdLongT) {
+            for (int64_t q = 0; q < cnt[k]; ++q) { urow[u + q] = (int32_t)r; upiece[u + q] = (int32_t)q; }
+        } else {
+            urow[u] = (int32_t)r;
+            upiece[u] = -1;
+        }
+        u += cnt[k];
+    }
+}
+
+template <typename V, typename O>
+struct AdSmem {
+    V prod[kAdCap];
+    int64_t roff[kAdRows + 1];
+    V sred[32];
+};
+
+template <typename V, typename O>
+__global__ void __launch_bounds__(256) k_adaptive(const O *__restrict__ off, const int32_t *__restrict__ col,
+                                                  const V *__restrict__ val, const V *__restrict__ x,
+                                                  V *__restrict__ y, int64_t n_rows,
+                                                  const int32_t *__restrict__ urow, const int32_t *__restrict__ upiece,
+                                                  const int64_t *__restrict__ n_units_dev, int32_t *__restrict__ crow,
+                                                  V *__restrict__ cval) {
+    __shared__ AdSmem<V, O> sm;
+    const int64_t U = *n_units_dev;
+    for (int64_t u = blockIdx.x; u < U; u += gridDim.x) {
+        const int64_t ra = urow[u];
+        const int32_t pc = upiece[u];
+        if (pc >= 0) {
+            // vector-L piece of a long row
+            const int64_t rs = ldo(off + ra), re = ldo(off + ra + 1);
+            const int64_t s = rs + (int64_t)pc * kAdLongChunk;
+            const int64_t e = s + kAdLongChunk < re ? s + kAdLongChunk : re;
+            V sum = 0;
+            int64_t j = s + threadIdx.x;
+            for (; j + 3 * 256 < e; j += 4 * 256) {
+                const int32_t c0 = ld_stream(col + j), c1 = ld_stream(col + j + 256), c2 = ld_stream(col + j + 512),
+                              c3 = ld_stream(col + j + 768);
+                const V v0 = ld_stream(val + j), v1 = ld_stream(val + j + 256), v2 = ld_stream(val + j + 512),
+                        v3 = ld_stream(val + j + 768);
+                sum = fma_acc(sum, v0, ld_x(x + c0));
+                sum = fma_acc(sum, v1, ld_x(x + c1));
+                sum = fma_acc(sum, v2, ld_x(x + c2));
+                sum = fma_acc(sum, v3, ld_x(x + c3));
+            }
+            for (; j < e; j += 256) sum = fma_acc(sum, ld_stream(val + j), ld_x(x + ld_stream(col + j)));
+            const V t = block_sum(sum, sm.sred);
+            if (threadIdx.x == 0) {
+                const int64_t npieces = (re - rs + kAdLongChunk - 1) / kAdLongChunk;
+                if (npieces == 1) {
+                    y[ra] = t;
+                    crow[u] = -1;
+                } else if (pc == npieces - 1) {
+                    y[ra] = t;  // finishing piece writes; earlier pieces are carries
+                    crow[u] = -1;
+                } else {
+                    crow[u] = (int32_t)ra;
+                    cval[u] = t;
+                }
+            }
+        } else {
+            const int64_t rb = (u + 1 < U) ? (int64_t)urow[u + 1] : n_rows;
+            const int nrows = (int)(rb - ra);
+            const int64_t s = ldo(off + ra);
+            for (int k = threadIdx.x; k <= nrows; k += 256) sm.roff[k] = ldo(off + ra + k) - s;
+            const int nz = (int)(ldo(off + rb) - s);
+            for (int k = threadIdx.x; k < nz; k += 256) {
+                const int64_t j = s + k;
+                sm.prod[k] = ld_stream(val + j) * ld_x(x + ld_stream(col + j));
+            }
+            if (threadIdx.x == 0) crow[u] = -1;
+            __syncthreads();
+            // G lanes per row, G = min(32, pow2floor(256 / nrows))
+            int G = 1;
+            while (G < 32 && G * 2 * nrows <= 256) G <<= 1;
+            const int grp = threadIdx.x / G, gl = threadIdx.x % G;
+            V sum = 0;
+            if (grp < nrows) {
+                const int a = (int)sm.roff[grp], b = (int)sm.roff[grp + 1];
+                for (int k = a + gl; k < b; k += G) sum += sm.prod[k];
+            }
+            // reduce inside groups (G is CTA-uniform; groups never straddle warps)
+            for (int o = 1; o < G; o <<= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+            if (grp < nrows && gl == 0) y[ra + grp] = sum;
+        }
+        __syncthreads();
+    }
+}
+
+// ================================================================= shard partition (K14)
+template <typename O>
+__global__ void k_shard_partition(const O *__restrict__ off, int64_t n_rows, int32_t parts, int64_t *__restrict__ cuts) {
+    const int p = blockIdx.x * blockDim.x + threadIdx.x;
+    if (p > parts) return;
+    const int64_t nnz = ldo(off + n_rows);
+    if (p == parts) { cuts[p] = n_rows; return; }
+    const int64_t target = (int64_t)((__int128)p * nnz / parts);
+    int64_t lo = 0, hi = n_rows;  // lower_bound(off[0..n_rows], target)
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ldo(off + mid) < target) lo = mid + 1;
+        else hi = mid;
+    }
+    cuts[p] = lo;
+}
+
+// ================================================================= host helpers
+int wm_group(const kp_csr *A) {
+    const double mean = A->n_rows > 0 ? (double)A->nnz / (double)A->n_rows : 0.0;
+    if (mean <= 2) return 2;
+    if (mean <= 4) return 4;
+    if (mean <= 8) return 8;
+    if (mean <= 16) return 16;
+    return 32;
+}
+
+int64_t merge_tiles(const kp_csr *A) { return (A->n_rows + A->nnz + kMergeTile - 1) / kMergeTile; }
+int64_t coo_chunks(const kp_csr *A) { return (A->nnz + kCooChunk - 1) / kCooChunk; }
+int64_t ad_units_max(const kp_csr *A) {
+    return A->n_rows + A->nnz / kAdLongChunk + 2;
+}
+int64_t ad_scan_blocks(const kp_csr *A) { return (A->n_rows + kScanItems - 1) / kScanItems; }
+
+bool valid_csr(const kp_csr *A) {
+    if (!A || A->n_rows < 0 || A->n_cols < 0 || A->nnz < 0) return false;
+    if (A->off_type != KP_I32 && A->off_type != KP_I64) return false;
+    if (A->val_type != KP_F32 && A->val_type != KP_F64) return false;
+    if (A->n_rows >= INT32_MAX || A->n_cols > INT32_MAX) return false;
+    if (A->off_type == KP_I32 && A->nnz >= INT32_MAX) return false;
+    if (!A->row_offsets) return false;
+    if (A->nnz > 0 && (!A->col_indices || !A->values)) return false;
+    return true;
+}
+
+size_t val_bytes(const kp_csr *A) { return A->val_type == KP_F32 ? 4 : 8; }
+
+struct Layout {
+    size_t hdr = 0, red = 0, a = 0, b = 0, c = 0, total = 0;
+};
+
+Layout prep_layout(int32_t kernel, const kp_csr *A, int64_t cap) {
+    Layout L;
+    size_t o = align_up(sizeof(PrepHeader));
+    switch (kernel) {
+        case KP_ELL_TM: {
+            L.red = o; o += align_up(kRedWsBytes);
+            L.a = o; o += align_up((size_t)cap * A->n_rows * sizeof(int32_t));
+            L.b = o; o += align_up((size_t)cap * A->n_rows * val_bytes(A));
+            break;
+        }
+        case KP_COO_WM: L.a = o; o += align_up((size_t)A->nnz * sizeof(int32_t) + 64); break;
+        case KP_CSR_MP: L.a = o; o += align_up((size_t)(merge_tiles(A) + 1) * sizeof(int64_t)); break;
+        case KP_ADAPTIVE_CSR: {
+            const int64_t U = ad_units_max(A);
+            L.a = o; o += align_up((size_t)U * sizeof(int32_t));
+            L.b = o; o += align_up((size_t)U * sizeof(int32_t));
+            L.c = o; o += align_up((size_t)(ad_scan_blocks(A) + 1) * sizeof(int64_t));
+            break;
+        }
+        default: break;
+    }
+    L.total = o;
+    return L;
+}
+
+int64_t spmv_units(int32_t kernel, const kp_csr *A) {
+    switch (kernel) {
+        case KP_CSR_MP:
+        case KP_CSR_WO: return merge_tiles(A);
+        case KP_COO_WM: return coo_chunks(A);
+        case KP_ADAPTIVE_CSR: return ad_units_max(A);
+        default: return 0;
+    }
+}
+
+template <typename V, typename O>
+int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, const Layout &L, kp_prepared *P,
+              cudaStream_t s) {
+    PrepHeader *hdr = reinterpret_cast<PrepHeader *>(buf);
+    const O *off = reinterpret_cast<const O *>(A->row_offsets);
+    const V *val = reinterpret_cast<const V *>(A->values);
+    switch (kernel) {
+        case KP_ELL_TM: {
+            PrepHeader h = {};
+            h.kernel = kernel;
+            h.cap = cap;
+            KP_CUDA_TRY(cudaMemcpyAsync(hdr, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+            KP_CUDA_TRY(cudaMemsetAsync(buf + L.red, 0, kRedWsBytes, s));
+            int rc = launch_k1_stats_into(A->row_offsets, A->off_type, A->n_rows, hdr->stats, buf + L.red, s);
+            if (rc) return rc;
+            const int64_t g = (A->n_rows + 255) / 256;
+            if (g > 0) {
+                k_prep_ell<V, O><<<(unsigned)g, 256, 0, s>>>(hdr, off, A->col_indices, val,
+                                                              reinterpret_cast<int32_t *>(buf + L.a),
+                                                              reinterpret_cast<V *>(buf + L.b), A->n_rows);
+                KP_LAUNCHED();
+            }
+            P->n_units = 0;
+            P->ell_cap = cap;
+            break;
+        }
+        case KP_COO_WM: {
+            const int64_t threads = (A->nnz + kIPT - 1) / kIPT;
+            const int64_t g = (threads + 255) / 256;
+            if (g > 0) {
+                k_prep_coo<O><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, reinterpret_cast<int32_t *>(buf + L.a));
+                KP_LAUNCHED();
+            }
+            P->n_units = coo_chunks(A);
+            break;
+        }
+        case KP_CSR_MP: {
+            const int64_t nt = merge_tiles(A);
+            const int64_t g = (nt + 1 + 255) / 256;
+            k_prep_mp<O><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, nt, reinterpret_cast<int64_t *>(buf + L.a));
+            KP_LAUNCHED();
+            P->n_units = nt;
+            break;
+        }
+        case KP_ADAPTIVE_CSR: {
+            const int64_t nb = ad_scan_blocks(A);
+            int64_t *bsum = reinterpret_cast<int64_t *>(buf + L.c);
+            if (nb > 0) {
+                k_ad_count<O><<<(unsigned)nb, 256, 0, s>>>(off, A->n_rows, bsum);
+                KP_LAUNCHED();
+            }
+            k_scan_bsum<<<1, 1024, 0, s>>>(bsum, nb, &hdr->n_units);
+            KP_LAUNCHED();
+            if (nb > 0) {
+                k_ad_write<O><<<(unsigned)nb, 256, 0, s>>>(off, A->n_rows, bsum, reinterpret_cast<int32_t *>(buf + L.a),
+                                                            reinterpret_cast<int32_t *>(buf + L.b));
+                KP_LAUNCHED();
+            }
+            P->n_units = ad_units_max(A);
+            break;
+        }
+        default: P->n_units = 0; break;
+    }
+    return KP_OK;
+}
+
+template <typename V, typename O>
+int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V *y, unsigned char *ws,
+           cudaStream_t s) {
+    const O *off = reinterpret_cast<const O *>(A->row_offsets);
+    const int32_t *col = A->col_indices;
+    const V *val = reinterpret_cast<const V *>(A->values);
+    const int64_t R = A->n_rows, Z = A->nnz;
+    const int sms = num_sms();
+    // carries live in the workspace: [int32 rows | V vals]
+    const int64_t nu = spmv_units(kernel, A);
+    int32_t *crow = reinterpret_cast<int32_t *>(ws);
+    V *cval = reinterpret_cast<V *>(ws + align_up((size_t)nu * sizeof(int32_t) + 16));
+    switch (kernel) {
+        case KP_CSR_WM: {
+            const int G = P && P->group ? P->group : wm_group(A);
+            const int64_t g = (R * G + 255) / 256;
+            switch (G) {
+                case 2: k_csr_wm<V, O, 2><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R); break;
+                case 4: k_csr_wm<V, O, 4><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R); break;
+                case 8: k_csr_wm<V, O, 8><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R); break;
+                case 16: k_csr_wm<V, O, 16><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R); break;
+                default: k_csr_wm<V, O, 32><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R); break;
+            }
+            KP_LAUNCHED();
+            return KP_OK;
+        }
+        case KP_CSR_BM: {
+            const int64_t g = R < (int64_t)sms * 512 ? R : (int64_t)sms * 512;
+            k_csr_bm<V, O><<<(unsigned)g, 128, 0, s>>>(off, col, val, x, y, R);
+            KP_LAUNCHED();
+            return KP_OK;
+        }
+        case KP_CSR_TM: {
+            const size_t smem = 2 * sizeof(TmStage<V>);
+            const bool aligned = (((uintptr_t)col | (uintptr_t)val) & 15) == 0;
+            const int64_t tiles = (R + kTmRows - 1) / kTmRows;
+            const int per_sm = sizeof(V) == 4 ? 3 : 2;
+            const int64_t g = tiles < (int64_t)sms * per_sm ? tiles : (int64_t)sms * per_sm;
+            if (aligned) {
+                static bool done = false;  // one static per <V, O> instantiation of spmv_t
+                if (!done) {
+                    KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                    done = true;
+                }
+                k_csr_tm<V, O, true><<<(unsigned)g, kTmRows, smem, s>>>(off, col, val, x, y, R);
+            } else {
+                k_csr_tm<V, O, false><<<(unsigned)g, kTmRows, 0, s>>>(off, col, val, x, y, R);
+            }
+            KP_LAUNCHED();
+            return KP_OK;
+        }
+        case KP_ELL_TM: {
+            if (!P || !P->buf) return KP_EINVAL;
+            const Layout L = prep_layout(KP_ELL_TM, A, P->ell_cap);
+            unsigned char *b = reinterpret_cast<unsigned char *>(P->buf);
+            const int64_t g = (R + 255) / 256;
+            k_ell_tm<V, O><<<(unsigned)g, 256, 0, s>>>(reinterpret_cast<const PrepHeader *>(b),
+                                                       reinterpret_cast<const int32_t *>(b + L.a),
+                                                       reinterpret_cast<const V *>(b + L.b), off, col, val, x, y, R);
+            KP_LAUNCHED();
+            return KP_OK;
+        }
+        case KP_COO_WM: {
+            if (!P || !P->buf) return KP_EINVAL;
+            const Layout L = prep_layout(KP_COO_WM, A, 0);
+            const int64_t chunks = coo_chunks(A);
+            const int64_t g = (chunks * 32 + 255) / 256;
+            k_coo_wm<V><<<(unsigned)g, 256, 0, s>>>(reinterpret_cast<const int32_t *>((unsigned char *)P->buf + L.a), col,
+                                                    val, x, y, R, Z, crow, cval);
+            KP_LAUNCHED();
+            k_carry_fixup<V><<<(unsigned)((chunks * 32 + 255) / 256), 256, 0, s>>>(crow, cval, nullptr, chunks, y);
+            KP_LAUNCHED();
+            return KP_OK;
+        }
+        case KP_CSR_MP:
+        case KP_CSR_WO: {
+            const int64_t nt = merge_tiles(A);
+            if (kernel == KP_CSR_MP) {
+                if (!P || !P->buf) return KP_EINVAL;
+                const Layout L = prep_layout(KP_CSR_MP, A, 0);
+                k_csr_merge<V, O, true><<<(unsigned)nt, kTile, 0, s>>>(
+                    off, col, val, x, y, R, Z, reinterpret_cast<const int64_t *>((unsigned char *)P->buf + L.a), crow, cval);
+            } else {
+                k_csr_merge<V, O, false><<<(unsigned)nt, kTile, 0, s>>>(off, col, val, x, y, R, Z, nullptr, crow, cval);
+            }
+            KP_LAUNCHED();
+            k_carry_fixup<V><<<(unsigned)((nt * 32 + 255) / 256), 256, 0, s>>>(crow, cval, nullptr, nt, y);
+            KP_LAUNCHED();
+            return KP_OK;
+        }
+        case KP_ADAPTIVE_CSR: {
+            if (!P || !P->buf) return KP_EINVAL;
+            const Layout L = prep_layout(KP_ADAPTIVE_CSR, A, 0);
+            unsigned char *b = reinterpret_cast<unsigned char *>(P->buf);
+            const int64_t *U = &reinterpret_cast<const PrepHeader *>(b)->n_units;
+            const int per_sm = sizeof(V) == 4 ? 8 : 6;
+            k_adaptive<V, O><<<(unsigned)(sms * per_sm), 256, 0, s>>>(
+                off, col, val, x, y, R, reinterpret_cast<const int32_t *>(b + L.a),
+                reinterpret_cast<const int32_t *>(b + L.b), U, crow, cval);
+            KP_LAUNCHED();
+            const int64_t umax = ad_units_max(A);
+            k_carry_fixup<V><<<(unsigned)((umax * 32 + 255) / 256), 256, 0, s>>>(crow, cval, U, 0, y);
+            KP_LAUNCHED();
+            return KP_OK;
+        }
+        default: return KP_EINVAL;
+    }
+}
+
+}  // namespace
+
+// K1 stats into a caller pointer (used by the ELL prep); defined here to keep the
+// reduction kernels private to kp_reduce.cu via its public C entry.
+}  // namespace kp
+
+using namespace kp;
+
+extern "C" int kp_length_stats(const void *, int32_t, int64_t, int64_t *, void *, void *);
+
+int kp::launch_k1_stats_into(const void *off, int32_t off_type, int64_t n_rows, int64_t *out4, void *ws,
+                             cudaStream_t s) {
+    return kp_length_stats(off, off_type, n_rows + 1, out4, ws, s);
+}
+
+extern "C" {
+
+int kp_prepare_bytes(int32_t kernel, const kp_csr *A, int64_t ell_cap, size_t *bytes) {
+    if (!valid_csr(A) || !bytes || kernel < 0 || kernel >= KP_NUM_KERNELS) return KP_EINVAL;
+    if (kernel == KP_ELL_TM && ell_cap < 1) return KP_EINVAL;
+    *bytes = prep_layout(kernel, A, kernel == KP_ELL_TM ? ell_cap : 0).total;
+    return KP_OK;
+}
+
+int kp_prepare(int32_t kernel, const kp_csr *A, int64_t ell_cap, void *d_buf, size_t bytes, kp_prepared *out,
+               void *stream) {
+    if (!valid_csr(A) || !out || kernel < 0 || kernel >= KP_NUM_KERNELS) return KP_EINVAL;
+    if (kernel == KP_ELL_TM && ell_cap < 1) return KP_EINVAL;
+    const Layout L = prep_layout(kernel, A, kernel == KP_ELL_TM ? ell_cap : 0);
+    if (bytes < L.total || !d_buf) return KP_ENOMEM;
+    if (((uintptr_t)d_buf & (kAlign - 1)) != 0) return KP_EINVAL;
+    out->kernel = kernel;
+    out->group = wm_group(A);
+    out->n_units = 0;
+    out->ell_cap = kernel == KP_ELL_TM ? ell_cap : 0;
+    out->buf = d_buf;
+    out->bytes = bytes;
+    cudaStream_t s = (cudaStream_t)stream;
+    unsigned char *b = reinterpret_cast<unsigned char *>(d_buf);
+    if (A->val_type == KP_F32) {
+        return A->off_type == KP_I32 ? prepare_t<float, int32_t>(kernel, A, ell_cap, b, L, out, s)
+                                     : prepare_t<float, int64_t>(kernel, A, ell_cap, b, L, out, s);
+    }
+    return A->off_type == KP_I32 ? prepare_t<double, int32_t>(kernel, A, ell_cap, b, L, out, s)
+                                 : prepare_t<double, int64_t>(kernel, A, ell_cap, b, L, out, s);
+}
+
+int kp_spmv_workspace_bytes(int32_t kernel, const kp_csr *A, size_t *bytes) {
+    if (!valid_csr(A) || !bytes || kernel < 0 || kernel >= KP_NUM_KERNELS) return KP_EINVAL;
+    const int64_t nu = spmv_units(kernel, A);
+    *bytes = nu ? align_up((size_t)nu * sizeof(int32_t) + 16) + align_up((size_t)nu * val_bytes(A)) : 0;
+    return KP_OK;
+}
+
+int kp_spmv(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x, void *d_y, void *d_ws,
+            size_t ws_bytes, void *stream) {
+    if (!valid_csr(A) || kernel < 0 || kernel >= KP_NUM_KERNELS || !d_y || (A->n_cols > 0 && !d_x)) return KP_EINVAL;
+    size_t need = 0;
+    kp_spmv_workspace_bytes(kernel, A, &need);
+    if (ws_bytes < need || (need && !d_ws)) return KP_ENOMEM;
+    if (P && P->buf && P->kernel != kernel) return KP_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (A->n_rows == 0) return KP_OK;
+    if (A->nnz == 0) {
+        KP_CUDA_TRY(cudaMemsetAsync(d_y, 0, (size_t)A->n_rows * val_bytes(A), s));
+        return KP_OK;
+    }
+    unsigned char *ws = reinterpret_cast<unsigned char *>(d_ws);
+    if (A->val_type == KP_F32) {
+        return A->off_type == KP_I32
+                   ? spmv_t<float, int32_t>(kernel, A, P, (const float *)d_x, (float *)d_y, ws, s)
+                   : spmv_t<float, int64_t>(kernel, A, P, (const float *)d_x, (float *)d_y, ws, s);
+    }
+    return A->off_type == KP_I32 ? spmv_t<double, int32_t>(kernel, A, P, (const double *)d_x, (double *)d_y, ws, s)
+                                 : spmv_t<double, int64_t>(kernel, A, P, (const double *)d_x, (double *)d_y, ws, s);
+}
+
+int kp_shard_partition(const void *d_off, int32_t off_type, int64_t n_rows, int32_t parts, int64_t *d_cuts,
+                       void *stream) {
+    if (!d_off || !d_cuts || parts < 1 || n_rows < 0) return KP_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    const unsigned g = (unsigned)((parts + 1 + 255) / 256);
+    if (off_type == KP_I32) k_shard_partition<int32_t><<<g, 256, 0, s>>>((const int32_t *)d_off, n_rows, parts, d_cuts);
+    else if (off_type == KP_I64) k_shard_partition<int64_t><<<g, 256, 0, s>>>((const int64_t *)d_off, n_rows, parts, d_cuts);
+    else return KP_EINVAL;
+    KP_LAUNCHED();
+    return KP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,148 @@
+"""Device-resident CSR and the per-device scratch the C-ABI needs.
+
+``DeviceCSR`` is the HBM layout every kernel reads:
+row_offsets int32 (nnz < 2^31) or int64, col_indices int32, values fp32 / fp64,
+each a separate 256-byte-aligned torch allocation (so 16-byte vector loads and the
+1-D TMA bulk copies of CSR,TM are always legal).  torch only allocates; all compute
+goes through libkpb200.so.
+
+Prepared formats (ELL, COO row ids, merge-path partition, adaptive row blocks) are
+cached on the matrix per kernel: the amortisation lever of PAPER.md:280.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+
+_I32_MAX = 2**31 - 1
+_red_ws: dict = {}
+
+
+def reduce_workspace(device=None):
+    """Zeroed K1/K2 scratch for `device` (the kernels leave it zeroed)."""
+    torch = _lib.require_cuda()
+    dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+    ws = _red_ws.get(dev)
+    if ws is None:
+        n = int(_lib.load().kp_reduce_workspace_bytes())
+        ws = torch.zeros(n, dtype=torch.uint8, device=dev)
+        _red_ws[dev] = ws
+    return ws
+
+
+def _torch_dtype(dtype):
+    import torch
+    if dtype in (np.float32, "float32", "f32", torch.float32):
+        return torch.float32
+    if dtype in (np.float64, "float64", "f64", torch.float64):
+        return torch.float64
+    raise ValueError(f"unsupported value dtype {dtype!r} (fp32 or fp64)")
+
+
+class DeviceCSR:
+    """A CSR matrix resident in HBM.  Construct from torch CUDA tensors, or use
+    ``DeviceCSR.from_host`` for a reference ``SparseMatrixCSR`` / numpy arrays."""
+
+    def __init__(self, n_rows: int, n_cols: int, row_offsets, col_indices, values):
+        torch = _lib.require_cuda()
+        if row_offsets.dtype not in (torch.int32, torch.int64):
+            raise ValueError("row_offsets must be int32 or int64")
+        if col_indices.dtype != torch.int32:
+            raise ValueError("col_indices must be int32 on the device")
+        if values.dtype not in (torch.float32, torch.float64):
+            raise ValueError("values must be fp32 or fp64")
+        if not (row_offsets.is_cuda and col_indices.is_cuda and values.is_cuda):
+            raise ValueError("DeviceCSR tensors must live on a CUDA device")
+        if row_offsets.numel() != n_rows + 1:
+            raise ValueError("row_offsets length must be n_rows + 1")
+        if n_rows > _I32_MAX - 1 or n_cols > _I32_MAX:
+            raise ValueError("device layout supports < 2^31 rows / columns")
+        self.n_rows, self.n_cols = int(n_rows), int(n_cols)
+        self.row_offsets = row_offsets.contiguous()
+        self.col_indices = col_indices.contiguous()
+        self.values = values.contiguous()
+        self.nnz = int(col_indices.numel())
+        if values.numel() != self.nnz:
+            raise ValueError("values and col_indices lengths differ")
+        if self.row_offsets.dtype == torch.int32 and self.nnz > _I32_MAX - 1:
+            raise ValueError("int32 offsets need nnz < 2^31")
+        self.device = self.row_offsets.device
+        self.off_type = _lib.KP_I32 if self.row_offsets.dtype == torch.int32 else _lib.KP_I64
+        self.val_type = _lib.KP_F32 if self.values.dtype == torch.float32 else _lib.KP_F64
+        self._struct = _lib.kp_csr(self.n_rows, self.n_cols, self.nnz, self.off_type, self.val_type,
+                                   self.row_offsets.data_ptr(), self.col_indices.data_ptr(),
+                                   self.values.data_ptr())
+        self._prepared: dict = {}
+
+    # ------------------------------------------------------------------ constructors
+    @classmethod
+    def from_host(cls, m=None, *, n_rows=None, n_cols=None, row_offsets=None, col_indices=None,
+                  values=None, dtype=np.float32, index: str = "auto", device=None, non_blocking=False):
+        """Upload a reference-layout matrix (int64 / float64 host arrays).  Offsets are
+        narrowed to int32 when nnz < 2^31 (index='auto'), columns always to int32,
+        values to ``dtype``."""
+        torch = _lib.require_cuda()
+        if m is not None:
+            n_rows, n_cols = m.n_rows, m.n_cols
+            row_offsets, col_indices, values = m.row_offsets, m.col_indices, m.values
+        off = np.asarray(row_offsets)
+        nnz = int(off[-1]) if off.size else 0
+        use32 = index == "int32" or (index == "auto" and nnz < _I32_MAX)
+        off_np = np.ascontiguousarray(off, dtype=np.int32 if use32 else np.int64)
+        col_np = np.ascontiguousarray(col_indices, dtype=np.int32)
+        tdt = _torch_dtype(dtype)
+        val_np = np.ascontiguousarray(values, dtype=np.float32 if tdt == torch.float32 else np.float64)
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        t = lambda a: torch.from_numpy(a).to(dev, non_blocking=non_blocking)  # noqa: E731
+        return cls(int(n_rows), int(n_cols), t(off_np), t(col_np), t(val_np))
+
+    # ------------------------------------------------------------------ views
+    @property
+    def struct(self) -> _lib.kp_csr:
+        return self._struct
+
+    @property
+    def dtype(self):
+        return self.values.dtype
+
+    def known(self):
+        from .sparse import KnownFeatures
+        return KnownFeatures(self.n_rows, self.n_cols, self.nnz)
+
+    def to_host(self):
+        """(row_offsets, col_indices, values) as numpy (test / oracle use)."""
+        return (self.row_offsets.cpu().numpy(), self.col_indices.cpu().numpy(), self.values.cpu().numpy())
+
+    def byte_model(self, kernel: int, ell_width: int | None = None) -> int:
+        """Compulsory bytes of one SpMV: x counted once, y written once."""
+        sv = self.values.element_size()
+        so = self.row_offsets.element_size()
+        R, C, Z = self.n_rows, self.n_cols, self.nnz
+        if kernel == 6:   # COO,WM: row ids + cols + vals
+            return Z * (4 + 4 + sv) + C * sv + R * sv
+        if kernel == 7 and ell_width is not None:  # ELL,TM: padded slots
+            return R * ell_width * (4 + sv) + C * sv + R * sv
+        return Z * (4 + sv) + (R + 1) * so + C * sv + R * sv
+
+    def __repr__(self):
+        return (f"DeviceCSR({self.n_rows}x{self.n_cols}, nnz={self.nnz}, "
+                f"off={self.row_offsets.dtype}, val={self.values.dtype}, {self.device})")
+
+
+def as_device(m, dtype=None) -> DeviceCSR:
+    """DeviceCSR passthrough, or upload a host SparseMatrixCSR."""
+    if isinstance(m, DeviceCSR):
+        return m
+    return DeviceCSR.from_host(m, dtype=dtype or np.float32)
+
+
+def ptr(t) -> int:
+    return int(t.data_ptr())
+
+
+def cptr(obj) -> ctypes.c_void_p:
+    return ctypes.c_void_p(ptr(obj))

@@ -1,0 +1,123 @@
+"""The SpMV kernel family Seer selects between, and its preprocessing.
+
+Vocabulary order is PAPER.md Table III (:311-318) and never changes: tree class
+indices and the lowest-index tie-break of ``fastest_kernel`` depend
+on it.  Every call runs the sm_100a kernels in libkpb200.so (csrc/kp_spmv.cu);
+there is no CPU path.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+
+from . import _lib
+from .device import DeviceCSR, as_device
+
+KERNELS = ("Adaptive-CSR", "CSR,BM", "CSR,MP", "CSR,WM", "CSR,WO", "CSR,TM", "COO,WM", "ELL,TM")
+ADAPTIVE_CSR, CSR_BM, CSR_MP, CSR_WM, CSR_WO, CSR_TM, COO_WM, ELL_TM = range(8)
+# kernels whose one-time preprocessing is charged to the first iteration
+NEEDS_PREP = frozenset({ADAPTIVE_CSR, CSR_MP, COO_WM, ELL_TM})
+# SPEC.md:190 file-name convention: csr_tm.csv <-> "CSR,TM"
+FILE_NAMES = {k: KERNELS[k].lower().replace(",", "_").replace("-", "_") for k in range(8)}
+
+
+def kernel_index(k) -> int:
+    if isinstance(k, str):
+        return KERNELS.index(k)
+    k = int(k)
+    if not 0 <= k < len(KERNELS):
+        raise ValueError(f"kernel index {k} out of range")
+    return k
+
+
+class Prepared:
+    """A kernel's preprocessed format living in one device buffer."""
+
+    def __init__(self, kernel: int, buf, struct: _lib.kp_prepared, ell_cap: int = 0):
+        self.kernel = kernel
+        self.buf = buf
+        self.struct = struct
+        self.ell_cap = ell_cap
+
+    @property
+    def nbytes(self) -> int:
+        return 0 if self.buf is None else int(self.buf.numel())
+
+
+def default_ell_cap(A: DeviceCSR, budget_bytes: int | None = None) -> int:
+    """Reserved ELL width: 2x the mean row length + 8, capped by a memory budget.
+    Rows longer than the actual width spill to the CSR tail, so any cap is correct."""
+    torch = _lib.require_cuda()
+    if A.n_rows == 0:
+        return 1
+    mean = A.nnz / A.n_rows
+    cap = int(math.ceil(2 * mean)) + 8
+    if budget_bytes is None:
+        free, _ = torch.cuda.mem_get_info(A.device)
+        budget_bytes = free // 4
+    per_col = A.n_rows * (4 + A.values.element_size())
+    return max(1, min(cap, budget_bytes // max(per_col, 1)))
+
+
+def prepare(A, kernel, *, ell_cap: int | None = None, stream=None, cache: bool = True) -> Prepared:
+    """Run the kernel's preprocessing (K10-K13) on the device; cached on ``A``."""
+    torch = _lib.require_cuda()
+    A = as_device(A)
+    k = kernel_index(kernel)
+    if cache and k in A._prepared:
+        return A._prepared[k]
+    L = _lib.load()
+    cap = 0
+    if k == ELL_TM:
+        cap = int(ell_cap) if ell_cap else default_ell_cap(A)
+    nbytes = ctypes.c_size_t(0)
+    _lib.check(L.kp_prepare_bytes(k, ctypes.byref(A.struct), cap, ctypes.byref(nbytes)), "kp_prepare_bytes")
+    buf = torch.empty(max(int(nbytes.value), 256), dtype=torch.uint8, device=A.device)
+    st = _lib.kp_prepared()
+    _lib.check(L.kp_prepare(k, ctypes.byref(A.struct), cap, buf.data_ptr(), buf.numel(), ctypes.byref(st),
+                            _lib.stream_handle(stream)), "kp_prepare")
+    P = Prepared(k, buf, st, cap)
+    if cache:
+        A._prepared[k] = P
+    return P
+
+
+_ws_cache: dict = {}
+
+
+def spmv_workspace(A: DeviceCSR, kernel: int):
+    torch = _lib.require_cuda()
+    nbytes = ctypes.c_size_t(0)
+    _lib.check(_lib.load().kp_spmv_workspace_bytes(kernel, ctypes.byref(A.struct), ctypes.byref(nbytes)),
+               "kp_spmv_workspace_bytes")
+    n = int(nbytes.value)
+    if n == 0:
+        return None
+    key = (A.device, kernel)  # one per device and kernel; grows to the largest matrix
+    ws = _ws_cache.get(key)
+    if ws is None or ws.numel() < n:
+        ws = torch.empty(n, dtype=torch.uint8, device=A.device)
+        _ws_cache[key] = ws
+    return ws
+
+
+def spmv(A, x, kernel, *, y=None, prepared: Prepared | None = None, stream=None):
+    """y = A.x with the chosen kernel (index or label).  Preprocesses on first use."""
+    torch = _lib.require_cuda()
+    A = as_device(A)
+    k = kernel_index(kernel)
+    if x.dtype != A.values.dtype or not x.is_cuda or x.numel() != A.n_cols:
+        raise ValueError("x must be a CUDA tensor of n_cols elements with the matrix value dtype")
+    x = x.contiguous()
+    if y is None:
+        y = torch.empty(A.n_rows, dtype=A.values.dtype, device=A.device)
+    if k in NEEDS_PREP and prepared is None:
+        prepared = prepare(A, k, stream=stream)
+    ws = spmv_workspace(A, k)
+    P = ctypes.byref(prepared.struct) if prepared is not None else None
+    rc = _lib.load().kp_spmv(k, ctypes.byref(A.struct), P, x.data_ptr(), y.data_ptr(),
+                             0 if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
+                             _lib.stream_handle(stream))
+    _lib.check(rc, f"kp_spmv[{KERNELS[k]}]")
+    return y

@@ -1,0 +1,296 @@
+"""Seer runtime: the three-tree model and device-side inference.
+
+* ``SeerModel`` -- known tree over (rows, cols, nnz, iterations), gathered tree over
+  that + (max, min, mean, var) row density, selector tree over the known schema with
+  classes {USE_KNOWN, USE_GATHERED}, plus the kernel vocabulary.
+  Versioned JSON bundle.
+* ``infer`` -- on a matrix, ONE fused kernel (``kp_seer_select``):
+  every CTA evaluates the selector; USE_KNOWN answers from CTA 0 without touching
+  the matrix (SPEC.md:388 purity); USE_GATHERED runs the feature pass and the last
+  CTA evaluates the gathered tree on the bit-exact features.  The charged overhead
+  is the measured collection time on the gathered path and 0 on the known path.
+* ``train_seer`` / ``selector_label`` -- offline, host-side.
+* ``SeerRunner.run`` -- select -> preprocess (cached) -> k SpMV iterations on the
+  device: the end-to-end cost T_seer of SURVEY 8d.
+"""
+
+from __future__ import annotations
+
+import json
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .dataset import fastest_kernel, total_cost
+from .dtree import DecisionTree, leaf_tree, train_tree
+from .kernels import KERNELS, NEEDS_PREP, prepare, spmv
+
+SEER_FORMAT = "kernelpick-b200-seer/1"
+KNOWN_SCHEMA = ("rows", "cols", "nnz", "iterations")
+GATHERED_SCHEMA = KNOWN_SCHEMA + ("max_density", "min_density", "mean_density", "var_density")
+USE_KNOWN, USE_GATHERED = 0, 1
+
+
+@dataclass(frozen=True)
+class InferenceOutcome:
+    chosen_kernel: int
+    path: int                    # USE_KNOWN / USE_GATHERED
+    charged_overhead: float      # seconds; 0 on the known path
+    predicted_total: float = float("nan")  # diagnostic only
+    inference_time: float = 0.0  # the selection launch itself ("negligible but accounted")
+    features: tuple | None = None
+
+
+def known_vector(rows, cols, nnz, k) -> tuple:
+    return (float(rows), float(cols), float(nnz), float(k))
+
+
+class SeerModel:
+    def __init__(self, known_tree: DecisionTree, gathered_tree: DecisionTree, selector_tree: DecisionTree,
+                 kernels=KERNELS, meta: dict | None = None):
+        self.known_tree, self.gathered_tree, self.selector_tree = known_tree, gathered_tree, selector_tree
+        self.kernels = tuple(kernels)
+        self.meta = dict(meta or {})
+        if known_tree.n_classes != len(self.kernels) or gathered_tree.n_classes != len(self.kernels):
+            raise ValueError("known/gathered trees must classify over the kernel vocabulary")
+        if selector_tree.n_classes != 2:
+            raise ValueError("selector tree must have 2 classes")
+        if known_tree.n_features != 4 or selector_tree.n_features != 4 or gathered_tree.n_features != 8:
+            raise ValueError("tree feature schemas must be known(4) / gathered(8) / selector(4)")
+        self._dev: dict = {}
+
+    # ------------------------------------------------------------------ bundle
+    def to_json(self) -> str:
+        return json.dumps({"format": SEER_FORMAT, "kernels": list(self.kernels), "meta": self.meta,
+                           "known": self.known_tree.to_dict(), "gathered": self.gathered_tree.to_dict(),
+                           "selector": self.selector_tree.to_dict()}, sort_keys=True, indent=1)
+
+    @classmethod
+    def from_json(cls, text: str) -> "SeerModel":
+        from .errors import SchemaError
+        d = json.loads(text)
+        if not isinstance(d, dict) or d.get("format") != SEER_FORMAT:
+            raise SchemaError("unsupported Seer bundle format")
+        return cls(DecisionTree.from_dict(d["known"]), DecisionTree.from_dict(d["gathered"]),
+                   DecisionTree.from_dict(d["selector"]), d["kernels"], d.get("meta"))
+
+    @classmethod
+    def load(cls, path: str) -> "SeerModel":
+        with open(path) as f:
+            return cls.from_json(f.read())
+
+    def save(self, path: str) -> None:
+        with open(path, "w") as f:
+            f.write(self.to_json())
+
+    def device_trees(self, device):
+        """Packed (selector, known, gathered) trees resident on ``device``."""
+        torch = _lib.require_cuda()
+        key = str(device)
+        if key not in self._dev:
+            def up(t):
+                raw = np.frombuffer(t.pack(), dtype=np.uint8).copy()
+                return torch.from_numpy(raw).to(device)
+            self._dev[key] = (up(self.selector_tree), up(self.known_tree), up(self.gathered_tree))
+        return self._dev[key]
+
+    # ------------------------------------------------------------------ host predict
+    def predict_host(self, rows, cols, nnz, k, gathered=None) -> tuple[int, int]:
+        """Host evaluation of the same trees (precomputed-features path / tests)."""
+        kv = known_vector(rows, cols, nnz, k)
+        path = self.selector_tree.predict(kv)
+        if path == USE_KNOWN:
+            return self.known_tree.predict(kv), USE_KNOWN
+        if gathered is None:
+            raise ValueError("selector demands gathered features but none were supplied")
+        return self.gathered_tree.predict(kv + tuple(gathered)), USE_GATHERED
+
+
+# ---------------------------------------------------------------------- inference
+def select_async(model: SeerModel, A, k: int, out=None, stream=None):
+    """Enqueue kp_seer_select for DeviceCSR ``A``; returns the 96-byte device outcome."""
+    torch = _lib.require_cuda()
+    from .device import reduce_workspace
+    sel, kn, ga = model.device_trees(A.device)
+    if out is None:
+        out = torch.empty(_lib.OUTCOME_BYTES, dtype=torch.uint8, device=A.device)
+    rc = _lib.load().kp_seer_select(A.row_offsets.data_ptr(), A.off_type, A.n_rows, A.n_cols, A.nnz, int(k),
+                                    sel.data_ptr(), kn.data_ptr(), ga.data_ptr(), out.data_ptr(),
+                                    reduce_workspace(A.device).data_ptr(), _lib.stream_handle(stream))
+    _lib.check(rc, "kp_seer_select")
+    return out
+
+
+def infer(model: SeerModel, m=None, k: int = 1, clock=None, features=None) -> InferenceOutcome:
+    """SPEC.md:376-384.  ``m``: DeviceCSR or host SparseMatrixCSR (uploaded);
+    ``features``: precomputed GatheredFeatures (host evaluation, overhead passed through)."""
+    from .features import decode_outcome
+    if m is None:
+        if features is None:
+            raise ValueError("infer needs a matrix or precomputed features")
+        raise ValueError("precomputed-feature inference needs the known features: use infer_features")
+    from .device import as_device
+    A = as_device(m)
+    clock = clock or time.perf_counter
+    t0 = clock()
+    buf = select_async(model, A, k)
+    o = decode_outcome(buf)
+    dt = clock() - t0
+    if o.status == _lib.KP_ERANGE:
+        raise OverflowError("feature epilogue outside the exactly representable range")
+    gathered = o.path == USE_GATHERED
+    feats = (o.max_d, o.min_d, o.mean_d, o.var_d) if gathered else None
+    return InferenceOutcome(int(o.kernel), int(o.path), dt if gathered else 0.0, float("nan"), dt, feats)
+
+
+def infer_features(model: SeerModel, known, k: int, gathered=None) -> InferenceOutcome:
+    """Precomputed-features form of infer: ``known`` = (rows, cols, nnz);
+    ``gathered`` = GatheredFeatures (its collection_time is the charged overhead)."""
+    kv = known_vector(*known, k)
+    path = model.selector_tree.predict(kv)
+    if path == USE_KNOWN:
+        return InferenceOutcome(model.known_tree.predict(kv), USE_KNOWN, 0.0)
+    if gathered is None:
+        raise ValueError("selector demands gathered features but neither matrix nor features were supplied")
+    return InferenceOutcome(model.gathered_tree.predict(kv + tuple(gathered.as_vector())), USE_GATHERED,
+                            float(gathered.collection_time), features=tuple(gathered.as_vector()))
+
+
+class SeerRunner:
+    """End-to-end Seer on one device matrix: select -> preprocess -> k SpMVs.
+
+    The only host synchronisation is the 96-byte read of the selection outcome
+    (the chosen kernel decides which kernel to launch next)."""
+
+    def __init__(self, model: SeerModel):
+        self.model = model
+
+    def run(self, A, x, k: int = 1, y=None, stream=None, chain: bool = False):
+        """Returns (y, outcome).  chain=False: y = A.x repeated k times (SPEC cost
+        model k*runtime); chain=True: power iteration x <- A.x (square A)."""
+        torch = _lib.require_cuda()
+        from .features import decode_outcome
+        buf = select_async(self.model, A, k, stream=stream)
+        o = decode_outcome(buf)
+        kern = int(o.kernel)
+        P = prepare(A, kern, stream=stream) if kern in NEEDS_PREP else None
+        if y is None:
+            y = torch.empty(A.n_rows, dtype=A.values.dtype, device=A.device)
+        if chain:
+            if A.n_rows != A.n_cols:
+                raise ValueError("chain=True needs a square matrix")
+            src, dst = x, y
+            for _ in range(k):
+                spmv(A, src, kern, y=dst, prepared=P, stream=stream)
+                src, dst = dst, (x if dst is y else y)
+            y = src
+        else:
+            for _ in range(k):
+                spmv(A, x, kern, y=y, prepared=P, stream=stream)
+        return y, o
+
+
+# ---------------------------------------------------------------------- training
+def selector_label(row, known_pred: int, gathered_pred: int, k: int) -> int:
+    """USE_GATHERED iff cost(gathered_pred) + collection < cost(known_pred);
+    ties -> USE_KNOWN."""
+    cg = row.cost(gathered_pred, k) + row.collection_time
+    ck = row.cost(known_pred, k)
+    return USE_GATHERED if cg < ck else USE_KNOWN
+
+
+def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int = 1,
+               kernels=KERNELS, meta: dict | None = None) -> SeerModel:
+    """labels = fastest_kernel per (matrix, k); known tree on the known
+    schema, gathered tree on the full schema, selector on labels from the two
+    sub-models' own predictions on the training rows."""
+    nk = len(kernels)
+    Xk, Xg, y, ex = [], [], [], []
+    for r in rows:
+        if r.gathered is None:
+            raise ValueError(f"row {r.name!r} has no gathered features")
+        for k in iterations:
+            try:
+                lab = fastest_kernel(r.timings(), k)
+            except Exception:
+                continue
+            kv = known_vector(*r.known, k)
+            Xk.append(kv)
+            Xg.append(kv + tuple(r.gathered))
+            y.append(lab)
+            ex.append((r, k))
+    if not y:
+        raise ValueError("no labelled examples")
+    kt = train_tree(Xk, y, max_depth, min_samples_leaf, nk, KNOWN_SCHEMA)
+    gt = train_tree(Xg, y, max_depth, min_samples_leaf, nk, GATHERED_SCHEMA)
+    ys = [selector_label(r, kt.predict(xk), gt.predict(xg), k) for (r, k), xk, xg in zip(ex, Xk, Xg)]
+    st = train_tree(Xk, ys, max_depth, min_samples_leaf, 2, KNOWN_SCHEMA)
+    return SeerModel(kt, gt, st, kernels, meta)
+
+
+def realized_cost(model: SeerModel, row, k: int) -> tuple[float, int, int]:
+    """(cost incl. charged collection, kernel, path) of the selector on a dataset row."""
+    kv = known_vector(*row.known, k)
+    path = model.selector_tree.predict(kv)
+    if path == USE_KNOWN:
+        kern = model.known_tree.predict(kv)
+        return row.cost(kern, k), kern, path
+    kern = model.gathered_tree.predict(kv + tuple(row.gathered))
+    return row.cost(kern, k) + row.collection_time, kern, path
+
+
+def geomean_speedup(rows, model: SeerModel, k: int) -> dict:
+    """geomean over fixed kernels K of total(K) / total(selector),
+    totals summed over ``rows``; also the best-fixed-kernel aggregate ratio."""
+    sel = sum(realized_cost(model, r, k)[0] for r in rows)
+    nk = len(model.kernels)
+    fixed = []
+    for K in range(nk):
+        tot = 0.0
+        for r in rows:
+            c = r.cost(K, k)
+            if not np.isfinite(c):  # SPEC.md:495 fallback: worst present kernel
+                c = max(r.cost(j, k) for j in range(nk) if np.isfinite(r.cost(j, k)))
+            tot += c
+        fixed.append(tot)
+    ratios = [f / sel for f in fixed]
+    return {"selector_total": sel, "fixed_totals": fixed,
+            "geomean_vs_fixed": float(np.exp(np.mean(np.log(ratios)))),
+            "vs_best_fixed": min(fixed) / sel,
+            "oracle_total": sum(min(r.cost(j, k) for j in range(nk)) for r in rows)}
+
+
+def bootstrap_model() -> SeerModel:
+    """A rule-derived placeholder used only until a B200-measured bundle exists
+    (models/seer_b200.json).  Selector always gathers; gathered tree splits on
+    mean/max density like the paper's Table III intuition."""
+    rng = np.random.default_rng(0)
+    X, y = [], []
+    for _ in range(4000):
+        rows = float(10 ** rng.uniform(3, 7.5))
+        mean = float(10 ** rng.uniform(0, 2.5))
+        cols = rows
+        mx = mean * float(10 ** rng.uniform(0, 4))
+        nnz = rows * mean
+        k = float(rng.choice([1, 10, 100]))
+        var = (mx - mean) ** 2 / 50
+        if mx > 64 * mean:
+            lab = 2 if k < 10 else 0          # skewed: MP / adaptive
+        elif mean >= 24 and mx <= 2 * mean:
+            lab = 7 if k >= 10 else 3         # regular: ELL when amortised
+        elif mean > 12:
+            lab = 3
+        else:
+            lab = 5
+        X.append((rows, cols, nnz, k, mx / cols, 0.0, mean / cols, var / cols / cols))
+        y.append(lab)
+    gt = train_tree(X, y, 5, 1, 8, GATHERED_SCHEMA)
+    kt = train_tree([x[:4] for x in X], y, 5, 1, 8, KNOWN_SCHEMA)
+    st = leaf_tree(USE_GATHERED, 2, 4, KNOWN_SCHEMA)
+    return SeerModel(kt, gt, st, KERNELS, {"source": "bootstrap rules (not B200-measured)"})
+
+
+def total_cost_of(row, kernel, k):
+    return total_cost(row.runtime[kernel], row.preprocess[kernel], k)

@@ -1,0 +1,97 @@
+"""Every SpMV kernel vs the fp64-accumulating CPU oracle, normwise tolerance
+|y - y_ref|_i <= tol * sum_j |a_ij x_j| with tol = 1e-5 (fp32) / 1e-12 (fp64)."""
+import numpy as np
+import pytest
+import torch
+
+from paper_2403_17017_b200 import gen, kernels
+from paper_2403_17017_b200.device import DeviceCSR
+
+pytestmark = pytest.mark.gpu
+TOL = {torch.float32: 1e-5, torch.float64: 1e-12}
+
+
+def _edge_matrices():
+    ms = []
+    # all rows empty but one; empty leading/trailing rows; single row; single column
+    def mk(name, R, C, rows, cols):
+        return gen.from_coo(name, R, C, torch.tensor(rows, dtype=torch.int64), torch.tensor(cols, dtype=torch.int64), 9)
+    ms.append(mk("one_entry", 1000, 1000, [500], [3]))
+    ms.append(mk("single_row", 1, 5000, [0] * 3000, list(range(0, 6000, 2))[:3000]))
+    ms.append(mk("single_col", 3000, 1, list(range(3000)), [0] * 3000))
+    ms.append(mk("empty_ends", 5000, 100, [2000, 2000, 2001, 2999], [1, 5, 7, 99]))
+    # row lengths straddling tile / chunk / long-row thresholds
+    lens = [0, 1, 255, 256, 257, 1023, 1024, 1025, 2047, 2048, 2049, 8191, 8192, 8193, 20000, 0, 3, 0]
+    rows = np.repeat(np.arange(len(lens)), lens)
+    cols = np.concatenate([np.arange(l) for l in lens])
+    ms.append(mk("thresholds", len(lens), 20001, rows.tolist(), cols.tolist()))
+    ms.append(gen.powerlaw_rows(30000, 12.0, 1.3, seed=4))
+    ms.append(gen.constant_rows(50000, 3, seed=2))
+    ms.append(gen.banded(40000, 27))
+    return ms
+
+
+MATS = None
+
+
+def mats():
+    global MATS
+    if MATS is None:
+        MATS = [gen.config(c, small=True) for c in ("C1", "C2", "C3", "C4", "C5")] + _edge_matrices()
+    return MATS
+
+
+def _check(m, A, kern, y, orc):
+    off, col, val = A.to_host()
+    x = XS[(m.name, A.values.dtype)]
+    yref, absy = orc.spmv_csr(off, col, val, x.cpu().numpy())
+    ok, ratio = orc.spmv_check(y.cpu().numpy(), yref, absy, TOL[A.values.dtype])
+    assert ok, f"{m.name} {kernels.KERNELS[kern]} {A.values.dtype} {A.row_offsets.dtype}: ratio {ratio}"
+
+
+XS = {}
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("index", ["int32", "int64"])
+@pytest.mark.parametrize("kern", range(8))
+def test_kernel_parity(kern, dtype, index, orc):
+    for m in mats():
+        A = m.to_device_csr(dtype, index=index)
+        key = (m.name, dtype)
+        if key not in XS:
+            g = torch.Generator().manual_seed(3)
+            XS[key] = (torch.rand(m.n_cols, generator=g, dtype=torch.float64) * 2 - 1).to(dtype).cuda()
+        x = XS[key]
+        y = torch.full((A.n_rows,), float("nan"), dtype=dtype, device="cuda")
+        kernels.spmv(A, x, kern, y=y)
+        torch.cuda.synchronize()
+        _check(m, A, kern, y, orc)
+        # determinism: bit-identical on a re-run (no float atomics)
+        y2 = kernels.spmv(A, x, kern)
+        assert torch.equal(y, y2)
+
+
+def test_ell_hybrid_tail_small_cap(orc):
+    m = gen.config("C4", small=True)
+    A = m.to_device_csr(torch.float32)
+    P = kernels.prepare(A, kernels.ELL_TM, ell_cap=4, cache=False)
+    x = (torch.rand(A.n_cols, dtype=torch.float64) * 2 - 1).float().cuda()
+    XS[(m.name + "_ell", torch.float32)] = x
+    y = kernels.spmv(A, x, kernels.ELL_TM, prepared=P)
+    off, col, val = A.to_host()
+    yref, absy = orc.spmv_csr(off, col, val, x.cpu().numpy())
+    assert orc.spmv_check(y.cpu().numpy(), yref, absy, 1e-5)[0]
+
+
+def test_c2_full_size_every_kernel_agrees(orc):
+    """Full-size C2 (R-MAT s20): every kernel vs the oracle (sampled-free full check)."""
+    m = gen.config("C2", device="cuda")
+    A = m.to_device_csr(torch.float32)
+    x = (torch.rand(A.n_cols, device="cuda", dtype=torch.float64) * 2 - 1).float()
+    off, col, val = A.to_host()
+    yref, absy = orc.spmv_csr(off, col, val, x.cpu().numpy())
+    for k in range(8):
+        y = kernels.spmv(A, x, k)
+        ok, r = orc.spmv_check(y.cpu().numpy(), yref, absy, 1e-5)
+        assert ok, (kernels.KERNELS[k], r)
