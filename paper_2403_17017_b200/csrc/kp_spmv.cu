@@ -48,7 +48,6 @@ constexpr int kIPT = 8;         // merge items / nnz per thread
 constexpr int kMergeTile = kTile * kIPT;  // 2048 merge items per CTA tile
 constexpr int kCooChunk = 32 * kIPT;      // 256 nnz per warp
 constexpr int kTmRows = 256;              // CSR,TM rows per CTA tile
-constexpr int kTmCap = 4096;              // CSR,TM staged nnz per stage
 constexpr int kAdBlockNnz = 2048;         // adaptive: nnz window of a short row block
 constexpr int kAdLongT = 1024;            // adaptive: rows longer than this are "long"
 constexpr int kAdCap = kAdBlockNnz + kAdLongT;
@@ -59,27 +58,36 @@ template <typename V>
 __device__ __forceinline__ V fma_acc(V acc, V a, V b) { return fma(a, b, acc); }
 
 // ================================================================= CSR,WM (K4)
+// Predicated batch of U strided elements: all U (col, val) loads are issued before the
+// first x gather, so a lane keeps 2U + U requests in flight instead of one chain.
+template <int U, int S, typename V>
+__device__ __forceinline__ V batch_dot(const int32_t *__restrict__ col, const V *__restrict__ val,
+                                       const V *__restrict__ x, int64_t j, int64_t e, V sum) {
+    int32_t c[U];
+    V v[U];
+#pragma unroll
+    for (int i = 0; i < U; ++i) {
+        const int64_t q = j + (int64_t)i * S;
+        c[i] = q < e ? ld_stream(col + q) : 0;
+        v[i] = q < e ? ld_stream(val + q) : V(0);
+    }
+#pragma unroll
+    for (int i = 0; i < U; ++i)
+        if (j + (int64_t)i * S < e) sum = fma_acc(sum, v[i], ld_x(x + c[i]));
+    return sum;
+}
+
 template <typename V, typename O, int G>
 __global__ void __launch_bounds__(256) k_csr_wm(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                 const V *__restrict__ val, const V *__restrict__ x,
                                                 V *__restrict__ y, int64_t n_rows) {
+    constexpr int U = 4;
     const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) / G;
     if (row >= n_rows) return;  // whole groups exit together (G divides 32)
     const int gl = threadIdx.x % G;
     const int64_t s = ldo(off + row), e = ldo(off + row + 1);
     V sum = 0;
-    int64_t j = s + gl;
-    for (; j + 3 * G < e; j += 4 * G) {  // 4 independent gathers in flight per lane
-        const int32_t c0 = ld_stream(col + j), c1 = ld_stream(col + j + G), c2 = ld_stream(col + j + 2 * G),
-                      c3 = ld_stream(col + j + 3 * G);
-        const V v0 = ld_stream(val + j), v1 = ld_stream(val + j + G), v2 = ld_stream(val + j + 2 * G),
-                v3 = ld_stream(val + j + 3 * G);
-        sum = fma_acc(sum, v0, ld_x(x + c0));
-        sum = fma_acc(sum, v1, ld_x(x + c1));
-        sum = fma_acc(sum, v2, ld_x(x + c2));
-        sum = fma_acc(sum, v3, ld_x(x + c3));
-    }
-    for (; j < e; j += G) sum = fma_acc(sum, ld_stream(val + j), ld_x(x + ld_stream(col + j)));
+    for (int64_t j = s + gl; j < e; j += (int64_t)U * G) sum = batch_dot<U, G>(col, val, x, j, e, sum);
     if constexpr (G > 1) {
         const unsigned mask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((threadIdx.x & 31) & ~(G - 1)));
 #pragma unroll
@@ -111,14 +119,7 @@ __global__ void __launch_bounds__(128) k_csr_bm(const O *__restrict__ off, const
     for (int64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
         const int64_t s = ldo(off + row), e = ldo(off + row + 1);
         V sum = 0;
-        int64_t j = s + threadIdx.x;
-        for (; j + 128 < e; j += 256) {
-            const int32_t c0 = ld_stream(col + j), c1 = ld_stream(col + j + 128);
-            const V v0 = ld_stream(val + j), v1 = ld_stream(val + j + 128);
-            sum = fma_acc(sum, v0, ld_x(x + c0));
-            sum = fma_acc(sum, v1, ld_x(x + c1));
-        }
-        if (j < e) sum = fma_acc(sum, ld_stream(val + j), ld_x(x + ld_stream(col + j)));
+        for (int64_t j = s + threadIdx.x; j < e; j += 4 * 128) sum = batch_dot<4, 128>(col, val, x, j, e, sum);
         V t = block_sum(sum, sred);
         if (threadIdx.x == 0) y[row] = t;
         __syncthreads();
@@ -126,48 +127,52 @@ __global__ void __launch_bounds__(128) k_csr_bm(const O *__restrict__ off, const
 }
 
 // ================================================================= CSR,TM (K3)
-// Thread per row.  A persistent CTA walks row tiles of 256 rows; the tile's nnz
-// window [off[r0], off[r0+256]) is pulled into shared memory by two 1-D TMA bulk
-// copies (cols, vals) completing on an mbarrier, double buffered so tile i+1 lands
-// while tile i is reduced.  Tiles whose window exceeds the stage fall back to
-// direct (per-thread) global walks.
+// Thread per row.  A persistent CTA walks row tiles of 256*RPT rows (RPT rows per
+// thread, chosen on the host from the KNOWN mean row length so a tile's nnz window
+// fills ~3/4 of a stage).  The window [off[r0], off[r0 + 256*RPT]) of cols and vals is
+// pulled into shared memory by two 1-D TMA bulk copies (SASS UBLKCP) completing on an
+// mbarrier; 3 stages per CTA (tile i+2 lands while tile i is reduced).  Windows larger
+// than a stage fall back to direct per-thread global walks.
+constexpr int kTmStages = 3;
+template <typename V>
+struct TmCfg {
+    static constexpr int kCap = sizeof(V) == 4 ? 4096 : 2048;  // elements per stage
+};
 template <typename V>
 struct TmStage {
-    int32_t col[kTmCap];
-    V val[kTmCap];
+    int32_t col[TmCfg<V>::kCap];
+    V val[TmCfg<V>::kCap];
 };
 
 template <typename V, typename O, bool kTma>
 __global__ void __launch_bounds__(kTmRows) k_csr_tm(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                     const V *__restrict__ val, const V *__restrict__ x,
-                                                    V *__restrict__ y, int64_t n_rows) {
+                                                    V *__restrict__ y, int64_t n_rows, int rpt) {
+    constexpr int kCap = TmCfg<V>::kCap;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     TmStage<V> *stage = reinterpret_cast<TmStage<V> *>(smem_raw);
-    __shared__ __align__(8) uint64_t bar[2];
-    __shared__ int64_t s_base[2];  // element index staged at stage[k].col[0]; -1 = direct
-    const int64_t n_tiles = (n_rows + kTmRows - 1) / kTmRows;
+    __shared__ __align__(8) uint64_t bar[kTmStages];
+    __shared__ int64_t s_base[kTmStages];  // element index staged at stage[k].col[0]; -1 = direct
+    const int64_t tile_rows = (int64_t)kTmRows * rpt;
+    const int64_t n_tiles = (n_rows + tile_rows - 1) / tile_rows;
     const int tid = threadIdx.x;
 
-    // Issue (thread 0 only) the staging of tile t into stage k.
+    // thread 0 only: stage tile t into slot k (or mark it direct) and arm bar[k]
     auto issue = [&](int64_t t, int k) {
-        const int64_t r0 = t * kTmRows;
-        int64_t r1 = r0 + kTmRows;
+        const int64_t r0 = t * tile_rows;
+        int64_t r1 = r0 + tile_rows;
         if (r1 > n_rows) r1 = n_rows;
         const int64_t s = ldo(off + r0), e = ldo(off + r1);
         const int64_t a = s & ~(int64_t)3;   // 16-byte aligned start (4 elements)
         const int64_t ea = e & ~(int64_t)3;  // aligned end; tail [ea, e) by hand
-        if (!kTma || e - a > kTmCap || ea <= a) {
-            if (kTma && e - a <= kTmCap && e > s) {
-                // tiny window: copy by hand
+        const bool fits = kTma && e > s && e - a <= kCap;
+        if (!fits || ea <= a) {
+            if (fits)  // tiny window: copy by hand
                 for (int64_t j = a; j < e; ++j) {
                     stage[k].col[j - a] = __ldg(col + j);
                     stage[k].val[j - a] = __ldg(val + j);
                 }
-                s_base[k] = a;
-            } else {
-                s_base[k] = (e > s && e - a <= kTmCap) ? a : -1;
-                if (!kTma) s_base[k] = -1;
-            }
+            s_base[k] = fits ? a : -1;
             asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar[k])) : "memory");
             return;
         }
@@ -183,37 +188,61 @@ __global__ void __launch_bounds__(kTmRows) k_csr_tm(const O *__restrict__ off, c
     };
 
     if (tid == 0) {
-        mbar_init(&bar[0], 1);
-        mbar_init(&bar[1], 1);
+        for (int k = 0; k < kTmStages; ++k) mbar_init(&bar[k], 1);
         fence_barrier_init();
     }
     __syncthreads();
+    if (tid == 0)
+        for (int k = 0; k < kTmStages - 1; ++k) {
+            const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
+            if (t < n_tiles) issue(t, k);
+        }
     int64_t t = blockIdx.x;
-    if (tid == 0 && t < n_tiles) issue(t, 0);
     for (int i = 0; t < n_tiles; ++i, t += gridDim.x) {
-        const int k = i & 1;
-        const int64_t tn = t + gridDim.x;
+        const int k = i % kTmStages;
+        const int64_t tn = t + (int64_t)(kTmStages - 1) * gridDim.x;
         if (tid == 0 && tn < n_tiles) {
             fence_proxy_async();
-            issue(tn, k ^ 1);
+            issue(tn, (i + kTmStages - 1) % kTmStages);
         }
-        const int64_t row = t * kTmRows + tid;
-        int64_t s = 0, e = 0;
-        if (row < n_rows) { s = ldo(off + row); e = ldo(off + row + 1); }
-        mbar_wait(&bar[k], (uint32_t)((i >> 1) & 1));
+        // row bounds of this thread's rows (independent loads, overlap the TMA wait)
+        int64_t rs[8], re[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int64_t row = t * tile_rows + tid + (int64_t)q * kTmRows;
+            const bool in = q < rpt && row < n_rows;
+            rs[q] = in ? ldo(off + row) : 0;
+            re[q] = in ? ldo(off + row + 1) : 0;
+        }
+        mbar_wait(&bar[k], (uint32_t)((i / kTmStages) & 1));
         const int64_t base = s_base[k];
-        V sum = 0;
-        if (row < n_rows) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            const int64_t row = t * tile_rows + tid + (int64_t)q * kTmRows;
+            if (q >= rpt || row >= n_rows) break;
+            const int64_t s = rs[q], e = re[q];
+            V sum = 0;
             if (base >= 0) {
                 const int32_t *sc = stage[k].col - base;
                 const V *sv = stage[k].val - base;
-                for (int64_t j = s; j < e; ++j) sum = fma_acc(sum, sv[j], ld_x(x + sc[j]));
+                for (int64_t j = s; j < e; j += 4) {  // 4 gathers in flight per thread
+                    int32_t c[4];
+                    V v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        c[u] = j + u < e ? sc[j + u] : 0;
+                        v[u] = j + u < e ? sv[j + u] : V(0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (j + u < e) sum = fma_acc(sum, v[u], ld_x(x + c[u]));
+                }
             } else {
-                for (int64_t j = s; j < e; ++j) sum = fma_acc(sum, __ldg(val + j), ld_x(x + __ldg(col + j)));
+                for (int64_t j = s; j < e; j += 4) sum = batch_dot<4, 1>(col, val, x, j, e, sum);
             }
             y[row] = sum;
         }
-        __syncthreads();  // stage k fully consumed before it is refilled at i+1
+        __syncthreads();  // slot k fully consumed before it is refilled
     }
 }
 
@@ -229,28 +258,34 @@ __global__ void __launch_bounds__(256) k_ell_tm(const PrepHeader *__restrict__ h
     const int64_t cap = __ldg(&hdr->cap);
     const int64_t W = wmax < cap ? wmax : cap;
     V sum = 0;
-    int64_t k = 0;
-    const int32_t *pc = ecol + row;
-    const V *pv = evalv + row;
-    for (; k + 3 < W; k += 4) {
-        const int32_t c0 = ld_stream(pc + (k + 0) * n_rows), c1 = ld_stream(pc + (k + 1) * n_rows),
-                      c2 = ld_stream(pc + (k + 2) * n_rows), c3 = ld_stream(pc + (k + 3) * n_rows);
-        const V v0 = ld_stream(pv + (k + 0) * n_rows), v1 = ld_stream(pv + (k + 1) * n_rows),
-                v2 = ld_stream(pv + (k + 2) * n_rows), v3 = ld_stream(pv + (k + 3) * n_rows);
-        sum = fma_acc(sum, v0, ld_x(x + c0));
-        sum = fma_acc(sum, v1, ld_x(x + c1));
-        sum = fma_acc(sum, v2, ld_x(x + c2));
-        sum = fma_acc(sum, v3, ld_x(x + c3));
+    // warp-sliced column-major layout: the 32 rows of a warp own a contiguous [W][32]
+    // slab, so slot k of this row is at slab + 32*k -> each warp streams one contiguous
+    // region (DRAM-page / TLB friendly, unlike a global n_rows stride); 8 slots
+    // (16 loads) in flight per thread before the x gathers.
+    const int64_t slab = (row >> 5) * 32 * W + (row & 31);
+    const int32_t *pc = ecol + slab;
+    const V *pv = evalv + slab;
+    for (int64_t k = 0; k < W; k += 8) {
+        int32_t c[8];
+        V v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            c[i] = k + i < W ? ld_stream(pc + (k + i) * 32) : 0;
+            v[i] = k + i < W ? ld_stream(pv + (k + i) * 32) : V(0);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+            if (k + i < W) sum = fma_acc(sum, v[i], ld_x(x + c[i]));
     }
-    for (; k < W; ++k) sum = fma_acc(sum, ld_stream(pv + k * n_rows), ld_x(x + ld_stream(pc + k * n_rows)));
     if (wmax > cap) {  // hybrid tail: rows longer than the reserved width continue in CSR
         const int64_t s = ldo(off + row), e = ldo(off + row + 1);
-        for (int64_t j = s + W; j < e; ++j) sum = fma_acc(sum, __ldg(val + j), ld_x(x + __ldg(col + j)));
+        for (int64_t j = s + W; j < e; j += 4) sum = batch_dot<4, 1>(col, val, x, j, e, sum);
     }
     y[row] = sum;
 }
 
-// K12: CSR -> column-major ELL of width min(max_len, cap); padding = (col 0, val 0).
+// K12: CSR -> warp-sliced column-major ELL of width W = min(max_len, cap): slot (row, k)
+// at (row/32)*32*W + 32*k + row%32; padding = (col 0, val 0).
 template <typename V, typename O>
 __global__ void __launch_bounds__(256) k_prep_ell(const PrepHeader *__restrict__ hdr, const O *__restrict__ off,
                                                   const int32_t *__restrict__ col, const V *__restrict__ val,
@@ -264,8 +299,9 @@ __global__ void __launch_bounds__(256) k_prep_ell(const PrepHeader *__restrict__
     for (int64_t k = 0; k < W; ++k) {
         const int64_t j = s + k;
         const bool in = j < e;
-        ecol[k * n_rows + row] = in ? __ldg(col + j) : 0;
-        evalv[k * n_rows + row] = in ? __ldg(val + j) : V(0);
+        const int64_t slot = (row >> 5) * 32 * W + k * 32 + (row & 31);
+        ecol[slot] = in ? __ldg(col + j) : 0;
+        evalv[slot] = in ? __ldg(val + j) : V(0);
     }
 }
 
@@ -510,8 +546,15 @@ __global__ void __launch_bounds__(256) k_coo_wm(const int32_t *__restrict__ rid,
         int4 ca = ld_stream4(cp), cb = ld_stream4(cp + 1);
         r[0] = ra.x; r[1] = ra.y; r[2] = ra.z; r[3] = ra.w; r[4] = rb.x; r[5] = rb.y; r[6] = rb.z; r[7] = rb.w;
         const int32_t c[kIPT] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
+        V vv[kIPT];
+        const int4 *vp = reinterpret_cast<const int4 *>(val + j0);  // 8 values = 2 (fp32) / 4 (fp64) x 16 B
 #pragma unroll
-        for (int k = 0; k < kIPT; ++k) p[k] = ld_stream(val + j0 + k) * ld_x(x + c[k]);
+        for (int q = 0; q < (int)(kIPT * sizeof(V) / 16); ++q) {
+            const int4 w = ld_stream4(vp + q);
+            memcpy(&vv[q * 16 / sizeof(V)], &w, 16);
+        }
+#pragma unroll
+        for (int k = 0; k < kIPT; ++k) p[k] = vv[k] * ld_x(x + c[k]);
     } else {
 #pragma unroll
         for (int k = 0; k < kIPT; ++k) {
@@ -782,9 +825,20 @@ __global__ void __launch_bounds__(256) k_adaptive(const O *__restrict__ off, con
             const int64_t s = ldo(off + ra);
             for (int k = threadIdx.x; k <= nrows; k += 256) sm.roff[k] = ldo(off + ra + k) - s;
             const int nz = (int)(ldo(off + rb) - s);
-            for (int k = threadIdx.x; k < nz; k += 256) {
-                const int64_t j = s + k;
-                sm.prod[k] = ld_stream(val + j) * ld_x(x + ld_stream(col + j));
+            for (int b = 0; b < nz; b += 256 * 6) {  // 6 independent (col, val) pairs per thread
+                int32_t c[6];
+                V v[6];
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const int k = b + threadIdx.x + i * 256;
+                    c[i] = k < nz ? ld_stream(col + s + k) : 0;
+                    v[i] = k < nz ? ld_stream(val + s + k) : V(0);
+                }
+#pragma unroll
+                for (int i = 0; i < 6; ++i) {
+                    const int k = b + threadIdx.x + i * 256;
+                    if (k < nz) sm.prod[k] = v[i] * ld_x(x + c[i]);
+                }
             }
             if (threadIdx.x == 0) crow[u] = -1;
             __syncthreads();
@@ -824,12 +878,20 @@ __global__ void k_shard_partition(const O *__restrict__ off, int64_t n_rows, int
 
 // ================================================================= host helpers
 int wm_group(const kp_csr *A) {
+    // G lanes per row so that each lane issues ~U = 4 independent (col, val) pairs per
+    // row (batch_dot): G = clamp(pow2 >= mean / 4, 2, 32), from the KNOWN mean nnz/rows.
     const double mean = A->n_rows > 0 ? (double)A->nnz / (double)A->n_rows : 0.0;
-    if (mean <= 2) return 2;
-    if (mean <= 4) return 4;
-    if (mean <= 8) return 8;
-    if (mean <= 16) return 16;
-    return 32;
+    int G = 2;
+    while (G < 32 && G * 4 < mean) G <<= 1;
+    return G;
+}
+
+// CSR,TM rows per thread: tile window ~3/4 of a stage at the KNOWN mean row length.
+int tm_rows_per_thread(const kp_csr *A, int cap) {
+    const double mean = A->n_rows > 0 ? (double)A->nnz / (double)A->n_rows : 1.0;
+    int rpt = 1;
+    while (rpt < 8 && 2.0 * rpt * kTmRows * (mean > 1 ? mean : 1.0) <= 0.75 * cap) rpt <<= 1;
+    return rpt;
 }
 
 int64_t merge_tiles(const kp_csr *A) { return (A->n_rows + A->nnz + kMergeTile - 1) / kMergeTile; }
@@ -862,8 +924,9 @@ Layout prep_layout(int32_t kernel, const kp_csr *A, int64_t cap) {
     switch (kernel) {
         case KP_ELL_TM: {
             L.red = o; o += align_up(kRedWsBytes);
-            L.a = o; o += align_up((size_t)cap * A->n_rows * sizeof(int32_t));
-            L.b = o; o += align_up((size_t)cap * A->n_rows * val_bytes(A));
+            const size_t rpad = (size_t)((A->n_rows + 31) / 32 * 32);
+            L.a = o; o += align_up((size_t)cap * rpad * sizeof(int32_t));
+            L.b = o; o += align_up((size_t)cap * rpad * val_bytes(A));
             break;
         }
         case KP_COO_WM: L.a = o; o += align_up((size_t)A->nnz * sizeof(int32_t) + 64); break;
@@ -990,10 +1053,11 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
             return KP_OK;
         }
         case KP_CSR_TM: {
-            const size_t smem = 2 * sizeof(TmStage<V>);
+            const size_t smem = kTmStages * sizeof(TmStage<V>);
             const bool aligned = (((uintptr_t)col | (uintptr_t)val) & 15) == 0;
-            const int64_t tiles = (R + kTmRows - 1) / kTmRows;
-            const int per_sm = sizeof(V) == 4 ? 3 : 2;
+            const int rpt = tm_rows_per_thread(A, TmCfg<V>::kCap);
+            const int64_t tiles = (R + (int64_t)kTmRows * rpt - 1) / ((int64_t)kTmRows * rpt);
+            const int per_sm = (int)((227 * 1024) / (smem + 1024));
             const int64_t g = tiles < (int64_t)sms * per_sm ? tiles : (int64_t)sms * per_sm;
             if (aligned) {
                 static bool done = false;  // one static per <V, O> instantiation of spmv_t
@@ -1001,9 +1065,9 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
                     KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
                     done = true;
                 }
-                k_csr_tm<V, O, true><<<(unsigned)g, kTmRows, smem, s>>>(off, col, val, x, y, R);
+                k_csr_tm<V, O, true><<<(unsigned)g, kTmRows, smem, s>>>(off, col, val, x, y, R, rpt);
             } else {
-                k_csr_tm<V, O, false><<<(unsigned)g, kTmRows, 0, s>>>(off, col, val, x, y, R);
+                k_csr_tm<V, O, false><<<(unsigned)g, kTmRows, 0, s>>>(off, col, val, x, y, R, rpt);
             }
             KP_LAUNCHED();
             return KP_OK;
