@@ -45,7 +45,6 @@ constexpr size_t kRedWsBytes = 40960;  // >= kp_reduce_workspace_bytes()
 // ---------------------------------------------------------------- tunables
 constexpr int kTile = 256;      // threads per CTA for the tile kernels
 constexpr int kIPT = 8;         // merge items / nnz per thread
-constexpr int kMergeTile = kTile * kIPT;  // 2048 merge items per CTA tile
 constexpr int kCooChunk = 32 * kIPT;      // 256 nnz per warp
 constexpr int kTmRows = 256;              // CSR,TM rows per CTA tile
 constexpr int kAdBlockNnz = 2048;         // adaptive: nnz window of a short row block
@@ -127,104 +126,118 @@ __global__ void __launch_bounds__(128) k_csr_bm(const O *__restrict__ off, const
 }
 
 // ================================================================= CSR,TM (K3)
-// Thread per row.  A persistent CTA walks row tiles of 256*RPT rows (RPT rows per
-// thread, chosen on the host from the KNOWN mean row length so a tile's nnz window
-// fills ~3/4 of a stage).  The window [off[r0], off[r0 + 256*RPT]) of cols and vals is
-// pulled into shared memory by two 1-D TMA bulk copies (SASS UBLKCP) completing on an
-// mbarrier; 3 stages per CTA (tile i+2 lands while tile i is reduced).  Windows larger
-// than a stage fall back to direct per-thread global walks.
+// Thread per row, warp-specialised TMA pipeline.  A persistent CTA = 8 consumer warps
+// (256 threads, RPT rows each per tile) + 1 producer warp.  Per tile of 256*RPT rows
+// the producer pulls the row-offset window [r0, r1] and the nnz window
+// [off[r0], off[r1]) of cols and vals into one of 3 shared-memory stages with 1-D TMA
+// bulk copies (SASS UBLKCP) completing on the stage's `full` mbarrier; consumer warps
+// release a stage through its `empty` mbarrier, so no CTA-wide barrier sits in the
+// loop.  RPT is chosen on the host from the KNOWN mean row length (window ~3/4 of a
+// stage).  Windows larger than a stage fall back to direct per-thread global walks.
 constexpr int kTmStages = 3;
-template <typename V>
+constexpr int kTmMaxRpt = 4;
+template <typename V, typename O>
 struct TmCfg {
-    static constexpr int kCap = sizeof(V) == 4 ? 4096 : 2048;  // elements per stage
-};
-template <typename V>
-struct TmStage {
-    int32_t col[TmCfg<V>::kCap];
-    V val[TmCfg<V>::kCap];
+    static constexpr int kCap = sizeof(V) == 4 ? 4096 : 2048;                    // nnz per stage
+    static constexpr int kOffs = kTmRows * kTmMaxRpt + 8;                          // offsets per stage
+    static constexpr size_t kOffBytes = (kOffs * sizeof(O) + 127) / 128 * 128;
+    static constexpr size_t kColBytes = (size_t)kCap * 4;
+    static constexpr size_t kStageBytes = kOffBytes + kColBytes + (size_t)kCap * sizeof(V);
 };
 
 template <typename V, typename O, bool kTma>
-__global__ void __launch_bounds__(kTmRows) k_csr_tm(const O *__restrict__ off, const int32_t *__restrict__ col,
-                                                    const V *__restrict__ val, const V *__restrict__ x,
-                                                    V *__restrict__ y, int64_t n_rows, int rpt) {
-    constexpr int kCap = TmCfg<V>::kCap;
+__global__ void __launch_bounds__(kTmRows + 32) k_csr_tm(const O *__restrict__ off, const int32_t *__restrict__ col,
+                                                         const V *__restrict__ val, const V *__restrict__ x,
+                                                         V *__restrict__ y, int64_t n_rows, int rpt) {
+    using Cfg = TmCfg<V, O>;
+    constexpr int kCap = Cfg::kCap;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    TmStage<V> *stage = reinterpret_cast<TmStage<V> *>(smem_raw);
-    __shared__ __align__(8) uint64_t bar[kTmStages];
-    __shared__ int64_t s_base[kTmStages];  // element index staged at stage[k].col[0]; -1 = direct
+    __shared__ __align__(8) uint64_t full[kTmStages], empty[kTmStages];
+    __shared__ int64_t s_base[kTmStages];  // element index staged at col slot 0; -1 = direct
     const int64_t tile_rows = (int64_t)kTmRows * rpt;
     const int64_t n_tiles = (n_rows + tile_rows - 1) / tile_rows;
-    const int tid = threadIdx.x;
-
-    // thread 0 only: stage tile t into slot k (or mark it direct) and arm bar[k]
-    auto issue = [&](int64_t t, int k) {
-        const int64_t r0 = t * tile_rows;
-        int64_t r1 = r0 + tile_rows;
-        if (r1 > n_rows) r1 = n_rows;
-        const int64_t s = ldo(off + r0), e = ldo(off + r1);
-        const int64_t a = s & ~(int64_t)3;   // 16-byte aligned start (4 elements)
-        const int64_t ea = e & ~(int64_t)3;  // aligned end; tail [ea, e) by hand
-        const bool fits = kTma && e > s && e - a <= kCap;
-        if (!fits || ea <= a) {
-            if (fits)  // tiny window: copy by hand
-                for (int64_t j = a; j < e; ++j) {
-                    stage[k].col[j - a] = __ldg(col + j);
-                    stage[k].val[j - a] = __ldg(val + j);
-                }
-            s_base[k] = fits ? a : -1;
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&bar[k])) : "memory");
-            return;
-        }
-        for (int64_t j = ea; j < e; ++j) {  // < 4 tail elements
-            stage[k].col[j - a] = __ldg(col + j);
-            stage[k].val[j - a] = __ldg(val + j);
-        }
-        s_base[k] = a;
-        const uint32_t n = (uint32_t)(ea - a);
-        mbar_arrive_expect_tx(&bar[k], n * (uint32_t)(sizeof(int32_t) + sizeof(V)));
-        bulk_g2s(stage[k].col, col + a, n * (uint32_t)sizeof(int32_t), &bar[k]);
-        bulk_g2s(stage[k].val, val + a, n * (uint32_t)sizeof(V), &bar[k]);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    auto st_off = [&](int k) { return reinterpret_cast<O *>(smem_raw + k * Cfg::kStageBytes); };
+    auto st_col = [&](int k) { return reinterpret_cast<int32_t *>(smem_raw + k * Cfg::kStageBytes + Cfg::kOffBytes); };
+    auto st_val = [&](int k) {
+        return reinterpret_cast<V *>(smem_raw + k * Cfg::kStageBytes + Cfg::kOffBytes + Cfg::kColBytes);
     };
-
     if (tid == 0) {
-        for (int k = 0; k < kTmStages; ++k) mbar_init(&bar[k], 1);
+        for (int k = 0; k < kTmStages; ++k) {
+            mbar_init(&full[k], 1);
+            mbar_init(&empty[k], kTmRows / 32);
+        }
         fence_barrier_init();
     }
     __syncthreads();
-    if (tid == 0)
-        for (int k = 0; k < kTmStages - 1; ++k) {
-            const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
-            if (t < n_tiles) issue(t, k);
+
+    if (warp == kTmRows / 32) {  // ------------------------------------------- producer
+        if (lane != 0) return;
+        const int64_t nnz = ldo(off + n_rows);
+        auto bounds = [&](int64_t t, int64_t &s, int64_t &e) {
+            const int64_t r0 = t * tile_rows;
+            s = ldo(off + r0);
+            e = ldo(off + (r0 + tile_rows < n_rows ? r0 + tile_rows : n_rows));
+        };
+        int64_t sn = 0, en = 0;
+        if ((int64_t)blockIdx.x < n_tiles) bounds(blockIdx.x, sn, en);
+        int i = 0;
+        for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
+            const int k = i % kTmStages;
+            const int64_t s = sn, e = en;
+            if (t + gridDim.x < n_tiles) bounds(t + gridDim.x, sn, en);  // prefetch next tile's window
+            if (i >= kTmStages) mbar_wait(&empty[k], (uint32_t)(((i / kTmStages) - 1) & 1));
+            const int64_t r0 = t * tile_rows;
+            const int64_t r1 = r0 + tile_rows < n_rows ? r0 + tile_rows : n_rows;
+            // offsets window [r0, r1], rounded up to 16 B while in bounds (n_rows + 1 entries)
+            const int64_t n1 = r1 - r0 + 1;
+            constexpr int kOV = 16 / (int)sizeof(O);
+            int64_t nb = kTma ? (n1 + kOV - 1) / kOV * kOV : 0;
+            if (r0 + nb > n_rows + 1) nb = kTma ? n1 / kOV * kOV : 0;
+            O *so = st_off(k);
+            for (int64_t q = nb; q < n1; ++q) so[q] = off[r0 + q];
+            // nnz window [a, e) with a 16-byte aligned, end rounded up while in bounds
+            const int64_t a = s & ~(int64_t)3;
+            const bool fits = kTma && e > s && ((e + 3) & ~(int64_t)3) - a <= kCap;
+            int32_t *sc = st_col(k);
+            V *sv = st_val(k);
+            int64_t eb = (e + 3) & ~(int64_t)3;
+            if (eb > nnz) eb = e & ~(int64_t)3;  // last window of the matrix: hand-copy the tail
+            if (!fits || eb < a) eb = a;
+            if (fits)
+                for (int64_t j = eb; j < e; ++j) {
+                    sc[j - a] = __ldg(col + j);
+                    sv[j - a] = __ldg(val + j);
+                }
+            s_base[k] = fits ? a : -1;
+            const uint32_t n = (uint32_t)(eb - a);
+            const uint32_t tx = (uint32_t)(nb * sizeof(O)) + n * (uint32_t)(sizeof(int32_t) + sizeof(V));
+            mbar_arrive_expect_tx(&full[k], tx);
+            if (nb) bulk_g2s(so, off + r0, (uint32_t)(nb * sizeof(O)), &full[k]);
+            if (n) {
+                bulk_g2s(sc, col + a, n * (uint32_t)sizeof(int32_t), &full[k]);
+                bulk_g2s(sv, val + a, n * (uint32_t)sizeof(V), &full[k]);
+            }
         }
-    int64_t t = blockIdx.x;
-    for (int i = 0; t < n_tiles; ++i, t += gridDim.x) {
+        return;
+    }
+    // ------------------------------------------------------------------ consumers
+    int i = 0;
+    for (int64_t t = blockIdx.x; t < n_tiles; t += gridDim.x, ++i) {
         const int k = i % kTmStages;
-        const int64_t tn = t + (int64_t)(kTmStages - 1) * gridDim.x;
-        if (tid == 0 && tn < n_tiles) {
-            fence_proxy_async();
-            issue(tn, (i + kTmStages - 1) % kTmStages);
-        }
-        // row bounds of this thread's rows (independent loads, overlap the TMA wait)
-        int64_t rs[8], re[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int64_t row = t * tile_rows + tid + (int64_t)q * kTmRows;
-            const bool in = q < rpt && row < n_rows;
-            rs[q] = in ? ldo(off + row) : 0;
-            re[q] = in ? ldo(off + row + 1) : 0;
-        }
-        mbar_wait(&bar[k], (uint32_t)((i / kTmStages) & 1));
+        mbar_wait(&full[k], (uint32_t)((i / kTmStages) & 1));
         const int64_t base = s_base[k];
+        const O *so = st_off(k);
+        const int32_t *sc = st_col(k) - base;
+        const V *sv = st_val(k) - base;
+        const int64_t r0 = t * tile_rows;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            const int64_t row = t * tile_rows + tid + (int64_t)q * kTmRows;
-            if (q >= rpt || row >= n_rows) break;
-            const int64_t s = rs[q], e = re[q];
+        for (int q = 0; q < kTmMaxRpt; ++q) {
+            const int rl = tid + q * kTmRows;
+            if (q >= rpt || r0 + rl >= n_rows) break;
+            const int64_t s = (int64_t)so[rl], e = (int64_t)so[rl + 1];
             V sum = 0;
             if (base >= 0) {
-                const int32_t *sc = stage[k].col - base;
-                const V *sv = stage[k].val - base;
                 for (int64_t j = s; j < e; j += 4) {  // 4 gathers in flight per thread
                     int32_t c[4];
                     V v[4];
@@ -240,9 +253,10 @@ __global__ void __launch_bounds__(kTmRows) k_csr_tm(const O *__restrict__ off, c
             } else {
                 for (int64_t j = s; j < e; j += 4) sum = batch_dot<4, 1>(col, val, x, j, e, sum);
             }
-            y[row] = sum;
+            y[r0 + rl] = sum;
         }
-        __syncthreads();  // slot k fully consumed before it is refilled
+        __syncwarp();
+        if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[k])) : "memory");
     }
 }
 
@@ -387,7 +401,12 @@ __device__ __forceinline__ SegPair<V> block_seg_exscan(SegPair<V> p, SegPair<V> 
 
 // ================================================================= merge-path tiles (K6 MP, K7 WO)
 // Merge of A = row ends off[1..R] with B = nnz indices 0..Z-1 (Merrill & Garland).
-// Diagonal d -> (i rows consumed, d - i nnz consumed).
+// Diagonal d -> (i rows consumed, d - i nnz consumed).  Work unit = one WARP tile of
+// 256 merge items: the warp stages its row ends (int32, relative to the tile's first
+// nnz) and products val*x[col] in its own shared-memory slice (batched loads, no
+// CTA barrier), each lane merges 8 items sequentially, a warp segmented scan (shfl)
+// carries partial rows between lanes, and the row left open at the tile end is the
+// unit's carry (finished by k_carry_fixup).
 template <typename O>
 __device__ __forceinline__ int64_t merge_search_global(const O *off, int64_t n_rows, int64_t nnz, int64_t d) {
     int64_t lo = d - nnz > 0 ? d - nnz : 0;
@@ -420,64 +439,96 @@ __device__ __forceinline__ int64_t merge_search_warp(const O *off, int64_t n_row
         lo = nlo;
         hi = nhi;
     }
-    // final <= 32 candidates: one probe per lane
-    const int64_t p = lo + lane;
+    const int64_t p = lo + lane;  // final <= 32 candidates: one probe per lane
     const bool gr = p < hi && ldo(off + p + 1) <= d - p - 1;
     return lo + __popc(__ballot_sync(0xffffffffu, gr));
 }
 
-template <typename V, typename O>
-struct MergeSmem {
-    int64_t row_end[kMergeTile + 1];
-    V prod[kMergeTile];
-    SegPair<V> swarp[32];
-    int64_t coord[4];
+constexpr int kWarpTile = 32 * kIPT;  // 256 merge items per warp unit
+constexpr int kMergeWarps = 8;        // warps per CTA
+
+template <typename V>
+struct MergeWarpSmem {
+    int32_t rend[kWarpTile + 1];  // row ends relative to the tile's first nnz, clamped
+    V prod[kWarpTile];
 };
 
-// kPrep: tile coordinates from the K10 partition (CSR,MP); else searched in-kernel (CSR,WO).
+// kPrep: unit coordinates from the K10 partition (CSR,MP); else searched in-kernel (CSR,WO).
 template <typename V, typename O, bool kPrep>
-__global__ void __launch_bounds__(kTile) k_csr_merge(const O *__restrict__ off, const int32_t *__restrict__ col,
-                                                     const V *__restrict__ val, const V *__restrict__ x,
-                                                     V *__restrict__ y, int64_t n_rows, int64_t nnz,
-                                                     const int64_t *__restrict__ part, int32_t *__restrict__ crow,
-                                                     V *__restrict__ cval) {
-    __shared__ MergeSmem<V, O> sm;
-    const int64_t tile = blockIdx.x;
+__global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
+    const O *__restrict__ off, const int32_t *__restrict__ col, const V *__restrict__ val, const V *__restrict__ x,
+    V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, const int64_t *__restrict__ part,
+    int32_t *__restrict__ crow, V *__restrict__ cval) {
+    __shared__ MergeWarpSmem<V> smw[kMergeWarps];
+    __shared__ int64_t s_coord[kMergeWarps + 1];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t tile0 = (int64_t)blockIdx.x * kMergeWarps;
     const int64_t total = n_rows + nnz;
-    const int64_t d0 = tile * kMergeTile;
-    const int64_t d1 = d0 + kMergeTile < total ? d0 + kMergeTile : total;
     if (kPrep) {
-        if (threadIdx.x < 2) sm.coord[threadIdx.x] = part[tile + threadIdx.x];
+        if (threadIdx.x <= kMergeWarps) {
+            const int64_t t = tile0 + threadIdx.x;
+            s_coord[threadIdx.x] = part[t < n_units ? t : n_units];
+        }
     } else {
-        const int w = threadIdx.x >> 5;
-        if (w < 2) {
-            const int64_t d = w == 0 ? d0 : d1;
-            const int64_t i = merge_search_warp(off, n_rows, nnz, d);
-            if ((threadIdx.x & 31) == 0) sm.coord[w] = i;
+        int64_t d = (tile0 + w) * kWarpTile;
+        int64_t i = merge_search_warp(off, n_rows, nnz, d < total ? d : total);
+        if (lane == 0) s_coord[w] = i;
+        if (w == 0) {
+            d = (tile0 + kMergeWarps) * kWarpTile;
+            i = merge_search_warp(off, n_rows, nnz, d < total ? d : total);
+            if (lane == 0) s_coord[kMergeWarps] = i;
         }
     }
     __syncthreads();
-    const int64_t r0 = sm.coord[0], r1 = sm.coord[1];
+    const int64_t tile = tile0 + w;
+    if (tile >= n_units) return;
+    MergeWarpSmem<V> &sm = smw[w];
+    const int64_t d0 = tile * kWarpTile;
+    const int64_t d1 = d0 + kWarpTile < total ? d0 + kWarpTile : total;
+    const int64_t r0 = s_coord[w], r1 = s_coord[w + 1];
     const int64_t j0 = d0 - r0, j1 = d1 - r1;
-    const int nr = (int)(r1 - r0);  // row ends consumed in this tile
+    const int nr = (int)(r1 - r0);  // row ends consumed in this unit
     const int nz = (int)(j1 - j0);
-    // stage row ends (rows r0 .. r0+nr, the last one = row in progress) and products
-    const int nre = (r1 < n_rows) ? nr + 1 : nr;
-    for (int k = threadIdx.x; k < nre; k += kTile) sm.row_end[k] = ldo(off + r0 + 1 + k);
-    for (int k = threadIdx.x; k < nz; k += kTile) {
-        const int64_t j = j0 + k;
-        sm.prod[k] = ld_stream(val + j) * ld_x(x + ld_stream(col + j));
+    const int nre = (r1 < n_rows) ? nr + 1 : nr;  // + the row in progress at the end
+    {
+        int64_t re[kIPT + 1];
+        int32_t c[kIPT];
+        V v[kIPT];
+#pragma unroll
+        for (int i = 0; i <= kIPT; ++i) {
+            const int k = lane + i * 32;
+            re[i] = k < nre ? ldo(off + r0 + 1 + k) : 0;
+        }
+#pragma unroll
+        for (int i = 0; i < kIPT; ++i) {
+            const int k = lane + i * 32;
+            c[i] = k < nz ? ld_stream(col + j0 + k) : 0;
+            v[i] = k < nz ? ld_stream(val + j0 + k) : V(0);
+        }
+#pragma unroll
+        for (int i = 0; i <= kIPT; ++i) {
+            const int k = lane + i * 32;
+            if (k < nre) {
+                const int64_t rel = re[i] - j0;
+                sm.rend[k] = (int32_t)(rel < kWarpTile + 1 ? rel : kWarpTile + 1);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < kIPT; ++i) {
+            const int k = lane + i * 32;
+            if (k < nz) sm.prod[k] = v[i] * ld_x(x + c[i]);
+        }
     }
-    __syncthreads();
-    // thread-local merge of kIPT items starting at local diagonal t*kIPT
-    const int dt = threadIdx.x * kIPT;
+    __syncwarp();
+    // lane-local merge of kIPT items starting at local diagonal lane*kIPT
+    const int dt = lane * kIPT;
     int i, jj;
     {
         int lo = dt - nz > 0 ? dt - nz : 0;
         int hi = dt < nr ? dt : nr;
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (sm.row_end[mid] <= j0 + (dt - mid - 1)) lo = mid + 1;
+            if (sm.rend[mid] <= dt - mid - 1) lo = mid + 1;
             else hi = mid;
         }
         i = lo;
@@ -488,7 +539,7 @@ __global__ void __launch_bounds__(kTile) k_csr_merge(const O *__restrict__ off, 
     V first_val = 0;
     const int dend = dt + kIPT < nr + nz ? dt + kIPT : nr + nz;
     for (int d = dt; d < dend; ++d) {
-        if (i < nr && sm.row_end[i] <= j0 + jj) {  // row r0+i ends here
+        if (i < nr && sm.rend[i] <= jj) {  // row r0+i ends here
             if (first_row < 0) { first_row = i; first_val = acc; }
             else y[r0 + i] = acc;
             acc = 0;
@@ -498,25 +549,31 @@ __global__ void __launch_bounds__(kTile) k_csr_merge(const O *__restrict__ off, 
             ++jj;
         }
     }
-    SegPair<V> tot;
-    SegPair<V> ex = block_seg_exscan(SegPair<V>{first_row >= 0 ? 1 : 0, acc}, tot, sm.swarp);
-    if (first_row >= 0) y[r0 + first_row] = first_val + ex.v;
-    if (threadIdx.x == kTile - 1) {
-        // carry-out: the row in progress at the tile end (tot = its partial in this tile)
+    // warp segmented scan: carry-in for this lane's first finished row
+    SegPair<V> inc{first_row >= 0 ? 1 : 0, acc};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        SegPair<V> t{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
+        if (lane >= o) inc = seg_op(t, inc);
+    }
+    V ex = __shfl_up_sync(0xffffffffu, inc.v, 1);
+    if (lane == 0) ex = V(0);
+    if (first_row >= 0) y[r0 + first_row] = first_val + ex;
+    if (lane == 31) {  // carry-out: the row in progress at the unit end
         const bool has = r1 < n_rows && nz > 0;
         crow[tile] = has ? (int32_t)r1 : -1;
-        cval[tile] = has ? tot.v : V(0);
+        cval[tile] = has ? inc.v : V(0);
     }
 }
 
-// K10: merge-path partition, one thread per tile boundary.
+// K10: merge-path partition, one thread per unit boundary.
 template <typename O>
 __global__ void k_prep_mp(const O *__restrict__ off, int64_t n_rows, int64_t nnz, int64_t n_tiles,
                           int64_t *__restrict__ part) {
     const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (p > n_tiles) return;
     const int64_t total = n_rows + nnz;
-    const int64_t d = p * kMergeTile < total ? p * kMergeTile : total;
+    const int64_t d = p * kWarpTile < total ? p * kWarpTile : total;
     part[p] = merge_search_global(off, n_rows, nnz, d);
 }
 
@@ -625,26 +682,77 @@ __global__ void __launch_bounds__(256) k_coo_wm(const int32_t *__restrict__ rid,
     }
 }
 
-// K11: CSR -> COO row ids.  Thread per 8 nnz: binary search of the first row, then walk.
+// K11: CSR -> COO row ids.  One CTA per 2048 consecutive nnz: the rows that START
+// inside the window are the contiguous range [ra, rb) (two binary searches), each
+// marks its start position in shared memory (atomicMax picks the last of several rows
+// sharing an offset, i.e. the non-empty one), and a block max-scan seeded with the
+// row containing the window's first element fills every position.  Reads the
+// offsets once and writes each row id once (vectorised), no per-element search.
+constexpr int kCooPrepItems = 256 * kIPT;
+
+template <typename O>
+__device__ __forceinline__ int64_t upper_bound_off(const O *off, int64_t n_rows, int64_t v) {
+    int64_t lo = 0, hi = n_rows + 1;  // first index in off[0..n_rows] with off[i] > v
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) >> 1;
+        if (ldo(off + mid) <= v) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
 template <typename O>
 __global__ void __launch_bounds__(256) k_prep_coo(const O *__restrict__ off, int64_t n_rows, int64_t nnz,
                                                   int32_t *__restrict__ rid) {
-    const int64_t j0 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * kIPT;
-    if (j0 >= nnz) return;
-    // row = upper_bound(off, j0) - 1, over off[0..n_rows]
-    int64_t lo = 0, hi = n_rows;  // answer in [0, n_rows-1]
-    while (lo < hi) {
-        const int64_t mid = (lo + hi + 1) >> 1;
-        if (ldo(off + mid) <= j0) lo = mid;
-        else hi = mid - 1;
+    __shared__ int32_t s_mark[kCooPrepItems];
+    __shared__ int64_t s_r[3];
+    __shared__ int32_t s_wmax[8];
+    const int64_t j0 = (int64_t)blockIdx.x * kCooPrepItems;
+    const int64_t j1 = j0 + kCooPrepItems < nnz ? j0 + kCooPrepItems : nnz;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    if (lane == 0 && w < 3) {
+        const int64_t v = w == 0 ? j0 : (w == 1 ? j0 : j1 - 1);
+        s_r[w] = upper_bound_off(off, n_rows, v);  // rows with off[r] <= v: [0, result)
     }
-    int64_t r = lo;
-    int64_t rend = ldo(off + r + 1);
-    for (int k = 0; k < kIPT; ++k) {
-        const int64_t j = j0 + k;
-        if (j >= nnz) break;
-        while (j >= rend) { ++r; rend = ldo(off + r + 1); }
-        rid[j] = (int32_t)r;
+    for (int k = tid; k < kCooPrepItems; k += 256) s_mark[k] = -1;
+    __syncthreads();
+    const int64_t c0 = s_r[0] - 1;  // row containing j0
+    const int64_t ra = s_r[1], rb = s_r[2];  // rows starting in (j0, j1)
+    for (int64_t r = ra + tid; r < rb; r += 256) atomicMax(&s_mark[(int)(ldo(off + r) - j0)], (int32_t)r);
+    __syncthreads();
+    // blocked max-scan: thread t owns positions 8t .. 8t+7
+    int32_t v[kIPT];
+    int32_t m = -1;
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) {
+        const int32_t q = s_mark[tid * kIPT + i];
+        m = q > m ? q : m;
+        v[i] = m;
+    }
+    int32_t inc = m;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc = t > inc ? t : inc;
+    }
+    if (lane == 31) s_wmax[w] = inc;
+    __syncthreads();
+    int32_t carry = (int32_t)c0;
+    for (int i = 0; i < w; ++i) carry = s_wmax[i] > carry ? s_wmax[i] : carry;
+    int32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
+    if (lane > 0) carry = ex > carry ? ex : carry;
+    int32_t outv[kIPT];
+#pragma unroll
+    for (int i = 0; i < kIPT; ++i) outv[i] = v[i] > carry ? v[i] : carry;
+    const int64_t jb = j0 + tid * kIPT;
+    if (jb + kIPT <= j1) {
+        int4 *dst = reinterpret_cast<int4 *>(rid + jb);
+        dst[0] = make_int4(outv[0], outv[1], outv[2], outv[3]);
+        dst[1] = make_int4(outv[4], outv[5], outv[6], outv[7]);
+    } else {
+#pragma unroll
+        for (int i = 0; i < kIPT; ++i)
+            if (jb + i < j1) rid[jb + i] = outv[i];
     }
 }
 
@@ -890,11 +998,11 @@ int wm_group(const kp_csr *A) {
 int tm_rows_per_thread(const kp_csr *A, int cap) {
     const double mean = A->n_rows > 0 ? (double)A->nnz / (double)A->n_rows : 1.0;
     int rpt = 1;
-    while (rpt < 8 && 2.0 * rpt * kTmRows * (mean > 1 ? mean : 1.0) <= 0.75 * cap) rpt <<= 1;
+    while (rpt < kTmMaxRpt && 2.0 * rpt * kTmRows * (mean > 1 ? mean : 1.0) <= 0.75 * cap) rpt <<= 1;
     return rpt;
 }
 
-int64_t merge_tiles(const kp_csr *A) { return (A->n_rows + A->nnz + kMergeTile - 1) / kMergeTile; }
+int64_t merge_tiles(const kp_csr *A) { return (A->n_rows + A->nnz + kWarpTile - 1) / kWarpTile; }
 int64_t coo_chunks(const kp_csr *A) { return (A->nnz + kCooChunk - 1) / kCooChunk; }
 int64_t ad_units_max(const kp_csr *A) {
     return A->n_rows + A->nnz / kAdLongChunk + 2;
@@ -981,8 +1089,7 @@ int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, 
             break;
         }
         case KP_COO_WM: {
-            const int64_t threads = (A->nnz + kIPT - 1) / kIPT;
-            const int64_t g = (threads + 255) / 256;
+            const int64_t g = (A->nnz + kCooPrepItems - 1) / kCooPrepItems;
             if (g > 0) {
                 k_prep_coo<O><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, reinterpret_cast<int32_t *>(buf + L.a));
                 KP_LAUNCHED();
@@ -1053,22 +1160,21 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
             return KP_OK;
         }
         case KP_CSR_TM: {
-            const size_t smem = kTmStages * sizeof(TmStage<V>);
-            const bool aligned = (((uintptr_t)col | (uintptr_t)val) & 15) == 0;
-            const int rpt = tm_rows_per_thread(A, TmCfg<V>::kCap);
+            using Cfg = TmCfg<V, O>;
+            const size_t smem = kTmStages * Cfg::kStageBytes;
+            const bool aligned = (((uintptr_t)col | (uintptr_t)val | (uintptr_t)off) & 15) == 0;
+            const int rpt = tm_rows_per_thread(A, Cfg::kCap);
             const int64_t tiles = (R + (int64_t)kTmRows * rpt - 1) / ((int64_t)kTmRows * rpt);
             const int per_sm = (int)((227 * 1024) / (smem + 1024));
             const int64_t g = tiles < (int64_t)sms * per_sm ? tiles : (int64_t)sms * per_sm;
-            if (aligned) {
-                static bool done = false;  // one static per <V, O> instantiation of spmv_t
-                if (!done) {
-                    KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                    done = true;
-                }
-                k_csr_tm<V, O, true><<<(unsigned)g, kTmRows, smem, s>>>(off, col, val, x, y, R, rpt);
-            } else {
-                k_csr_tm<V, O, false><<<(unsigned)g, kTmRows, 0, s>>>(off, col, val, x, y, R, rpt);
+            static bool done = false;  // one static per <V, O> instantiation of spmv_t
+            if (!done) {
+                KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+                done = true;
             }
+            if (aligned) k_csr_tm<V, O, true><<<(unsigned)g, kTmRows + 32, smem, s>>>(off, col, val, x, y, R, rpt);
+            else k_csr_tm<V, O, false><<<(unsigned)g, kTmRows + 32, smem, s>>>(off, col, val, x, y, R, rpt);
             KP_LAUNCHED();
             return KP_OK;
         }
@@ -1098,13 +1204,14 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
         case KP_CSR_MP:
         case KP_CSR_WO: {
             const int64_t nt = merge_tiles(A);
+            const unsigned g = (unsigned)((nt + kMergeWarps - 1) / kMergeWarps);
             if (kernel == KP_CSR_MP) {
                 if (!P || !P->buf) return KP_EINVAL;
                 const Layout L = prep_layout(KP_CSR_MP, A, 0);
-                k_csr_merge<V, O, true><<<(unsigned)nt, kTile, 0, s>>>(
-                    off, col, val, x, y, R, Z, reinterpret_cast<const int64_t *>((unsigned char *)P->buf + L.a), crow, cval);
+                k_csr_merge<V, O, true><<<g, kMergeWarps * 32, 0, s>>>(
+                    off, col, val, x, y, R, Z, nt, reinterpret_cast<const int64_t *>((unsigned char *)P->buf + L.a), crow, cval);
             } else {
-                k_csr_merge<V, O, false><<<(unsigned)nt, kTile, 0, s>>>(off, col, val, x, y, R, Z, nullptr, crow, cval);
+                k_csr_merge<V, O, false><<<g, kMergeWarps * 32, 0, s>>>(off, col, val, x, y, R, Z, nt, nullptr, crow, cval);
             }
             KP_LAUNCHED();
             k_carry_fixup<V><<<(unsigned)((nt * 32 + 255) / 256), 256, 0, s>>>(crow, cval, nullptr, nt, y);
