@@ -1,0 +1,148 @@
+"""Row-sharded SpMV across GPUs: nnz-balanced partition, x replicated in a
+rank-padded layout, y local, one in-place all-gather per iteration.
+
+Partition (K14, ``kp_shard_partition``): cut p = lower_bound(row_offsets, p*nnz/P), so each
+rank owns a contiguous row range with ~nnz/P entries.  Unequal row counts R_p would break
+NCCL's equal-count all-gather, so columns are remapped ONCE at partition time into a
+rank-padded x layout:
+
+    col' = owner(col) * R_max + (col - cut[owner(col)])
+
+x then has P*R_max slots; rank p writes its y into slots [p*R_max, p*R_max + R_p), and the
+all-gather ``all_gather_into_tensor(x_pad, x_pad[p*R_max:(p+1)*R_max])`` is in place (send
+buffer = own slice of the receive buffer): no copies, padding slots are never referenced.
+Feature partials are exact integers, so global features (and hence the Seer selection) are
+identical to the single-matrix pass.
+
+The communicator is torch.distributed (NCCL over NVLink on GPUs, gloo on CPU for tests).
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def partition_cuts(row_offsets, parts: int) -> np.ndarray:
+    """Host restatement of K14 (lower_bound of p*nnz/P), int64 cuts[0..parts]."""
+    off = np.asarray(row_offsets, dtype=np.int64)
+    n_rows = off.size - 1
+    nnz = int(off[-1])
+    targets = (np.arange(parts, dtype=object) * nnz // parts).astype(np.int64)
+    cuts = np.searchsorted(off, targets, side="left").astype(np.int64)
+    cuts = np.minimum(cuts, n_rows)
+    return np.concatenate([cuts, [n_rows]])
+
+
+def device_cuts(A, parts: int):
+    """K14 on the device (DeviceCSR) -> int64 CUDA tensor of parts+1 cuts."""
+    import torch
+    from . import _lib
+    _lib.require_cuda()
+    out = torch.empty(parts + 1, dtype=torch.int64, device=A.device)
+    _lib.check(_lib.load().kp_shard_partition(A.row_offsets.data_ptr(), A.off_type, A.n_rows, parts,
+                                              out.data_ptr(), _lib.stream_handle()), "kp_shard_partition")
+    return out
+
+
+def remap_columns(cols, cuts, r_max: int):
+    """col -> owner*R_max + (col - cuts[owner]); works on numpy arrays or torch tensors."""
+    try:
+        import torch
+        if isinstance(cols, torch.Tensor):
+            c = cols.to(torch.int64)
+            cu = cuts.to(c.device)
+            owner = torch.searchsorted(cu, c, right=True) - 1
+            return (owner * r_max + (c - cu[owner])).to(torch.int32)
+    except ImportError:
+        pass
+    c = np.asarray(cols, dtype=np.int64)
+    cu = np.asarray(cuts, dtype=np.int64)
+    owner = np.searchsorted(cu, c, side="right") - 1
+    return (owner * r_max + (c - cu[owner])).astype(np.int32)
+
+
+class ShardPlan:
+    """This rank's slice of a square matrix in the rank-padded layout."""
+
+    def __init__(self, rank: int, world: int, cuts, n_rows: int):
+        self.rank, self.world = rank, world
+        self.cuts = np.asarray(cuts, dtype=np.int64)
+        self.r0, self.r1 = int(self.cuts[rank]), int(self.cuts[rank + 1])
+        self.r_max = int(np.max(np.diff(self.cuts))) if world > 0 else 0
+        self.n_rows = n_rows
+
+    @property
+    def local_rows(self) -> int:
+        return self.r1 - self.r0
+
+    def pad(self, x_full):
+        """Full-length x -> rank-padded x (host or torch)."""
+        import torch
+        if isinstance(x_full, torch.Tensor):
+            out = torch.zeros(self.world * self.r_max, dtype=x_full.dtype, device=x_full.device)
+        else:
+            out = np.zeros(self.world * self.r_max, dtype=np.asarray(x_full).dtype)
+        for p in range(self.world):
+            a, b = int(self.cuts[p]), int(self.cuts[p + 1])
+            out[p * self.r_max: p * self.r_max + (b - a)] = x_full[a:b]
+        return out
+
+    def unpad(self, x_pad):
+        parts = [x_pad[p * self.r_max: p * self.r_max + int(self.cuts[p + 1] - self.cuts[p])]
+                 for p in range(self.world)]
+        import torch
+        return torch.cat(parts) if isinstance(x_pad, torch.Tensor) else np.concatenate(parts)
+
+
+def local_csr(row_offsets, col_indices, values, plan: ShardPlan):
+    """Rows [r0, r1) rebased, columns remapped into the padded layout (host arrays or tensors)."""
+    off = row_offsets[plan.r0: plan.r1 + 1]
+    s = off[0]
+    loff = off - s
+    e = off[-1]
+    lc = remap_columns(col_indices[int(s): int(e)], plan.cuts if not hasattr(col_indices, "device")
+                       else _as_tensor(plan.cuts, col_indices.device), plan.r_max)
+    return loff, lc, values[int(s): int(e)]
+
+
+def _as_tensor(a, device):
+    import torch
+    return torch.as_tensor(np.asarray(a), dtype=torch.int64, device=device)
+
+
+class ShardedSpMV:
+    """Iterative y = A x with x <- y across ranks (power iteration), GPU kernels + NCCL.
+
+    ``run(x_full, k)``: x_pad[p] <- A_p . x_pad ; all_gather -> next x_pad ; k times."""
+
+    def __init__(self, A_full_host, kernel, group=None, dtype=None):
+        import torch
+        import torch.distributed as dist
+        from .device import DeviceCSR
+        self.dist = dist
+        self.group = group
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        off, col, val = A_full_host
+        cuts = partition_cuts(off, world)
+        self.plan = ShardPlan(rank, world, cuts, int(np.asarray(off).size - 1))
+        loff, lc, lv = local_csr(np.asarray(off), np.asarray(col), np.asarray(val), self.plan)
+        dt = dtype or torch.float32
+        self.A = DeviceCSR.from_host(n_rows=self.plan.local_rows, n_cols=world * self.plan.r_max,
+                                     row_offsets=loff, col_indices=lc, values=lv, dtype=dt)
+        self.kernel = kernel
+        self.bufs = [torch.zeros(world * self.plan.r_max, dtype=dt, device=self.A.device) for _ in range(2)]
+
+    def run(self, x_full, k: int):
+        from . import kernels
+        p = self.plan
+        cur = 0
+        self.bufs[cur].copy_(p.pad(x_full.to(self.bufs[0].device)))
+        P = kernels.prepare(self.A, self.kernel) if kernels.kernel_index(self.kernel) in kernels.NEEDS_PREP else None
+        for _ in range(k):
+            nxt = 1 - cur
+            mine = self.bufs[nxt][p.rank * p.r_max: p.rank * p.r_max + p.local_rows]
+            kernels.spmv(self.A, self.bufs[cur], self.kernel, y=mine, prepared=P)
+            self.dist.all_gather_into_tensor(self.bufs[nxt], self.bufs[nxt][p.rank * p.r_max:(p.rank + 1) * p.r_max],
+                                             group=self.group)
+            cur = nxt
+        return p.unpad(self.bufs[cur])

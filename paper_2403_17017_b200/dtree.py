@@ -45,25 +45,34 @@ def _midpoint(a: float, b: float) -> float:
     return a if t >= b else t
 
 
-def best_split(X, y, min_samples_leaf: int = 1, n_classes: int | None = None):
+def best_split(X, y, min_samples_leaf: int = 1, n_classes: int | None = None, sample_weight=None):
     """(feature, threshold, weighted impurity) minimising the children's weighted
-    Gini, or None when no split reduces impurity."""
+    Gini, or None when no split reduces impurity.
+
+    ``sample_weight`` (extension, default None = SPEC's plain CART): per-sample weights
+    enter the class frequencies and the children's weighting; ``min_samples_leaf``
+    still counts samples."""
     X = np.asarray(X, dtype=np.float64)
     y = np.asarray(y, dtype=np.int64)
     n = y.size
     if n < 2:
         return None
     k = int(n_classes if n_classes is not None else y.max() + 1)
-    parent = gini(y)
-    if parent == 0.0:
+    w = np.ones(n) if sample_weight is None else np.asarray(sample_weight, dtype=np.float64)
+    W = float(w.sum())
+    if W <= 0:
         return None
-    onehot = np.zeros((n, k), dtype=np.int64)
-    onehot[np.arange(n), y] = 1
+    tot = np.bincount(y, weights=w, minlength=k)
+    parent = float(1.0 - np.sum((tot / W) ** 2))
+    if np.count_nonzero(np.bincount(y, minlength=k)) <= 1:
+        return None
+    onehot = np.zeros((n, k), dtype=np.float64)
+    onehot[np.arange(n), y] = w
     best = None  # (impurity, feature, threshold)
     for f in range(X.shape[1]):
         order = np.argsort(X[:, f], kind="stable")
         xs = X[order, f]
-        cl = np.cumsum(onehot[order], axis=0)          # class counts of the left prefix
+        cl = np.cumsum(onehot[order], axis=0)          # weighted class mass of the left prefix
         nl = np.arange(1, n + 1)
         # candidate split after position i (left = 0..i) where xs[i] < xs[i+1]
         pos = np.flatnonzero(xs[:-1] < xs[1:])
@@ -72,14 +81,17 @@ def best_split(X, y, min_samples_leaf: int = 1, n_classes: int | None = None):
         nL = nl[pos]
         nR = n - nL
         ok = (nL >= min_samples_leaf) & (nR >= min_samples_leaf)
-        pos, nL, nR = pos[ok], nL[ok], nR[ok]
+        pos = pos[ok]
         if pos.size == 0:
             continue
         cL = cl[pos]
-        cR = cl[-1] - cL
-        gL = 1.0 - np.sum((cL / nL[:, None]) ** 2, axis=1)
-        gR = 1.0 - np.sum((cR / nR[:, None]) ** 2, axis=1)
-        imp = (nL * gL + nR * gR) / n
+        cR = tot[None, :] - cL
+        wL = cL.sum(1)
+        wR = cR.sum(1)
+        with np.errstate(invalid="ignore", divide="ignore"):
+            gL = np.where(wL > 0, 1.0 - np.sum((cL / wL[:, None]) ** 2, axis=1), 0.0)
+            gR = np.where(wR > 0, 1.0 - np.sum((cR / wR[:, None]) ** 2, axis=1), 0.0)
+        imp = (wL * gL + wR * gR) / W
         i = int(np.argmin(imp))  # first minimum = lowest threshold for this feature
         cand = (float(imp[i]), f, _midpoint(float(xs[pos[i]]), float(xs[pos[i] + 1])))
         if best is None or cand[0] < best[0]:
@@ -89,13 +101,13 @@ def best_split(X, y, min_samples_leaf: int = 1, n_classes: int | None = None):
     # scikit (impurity decrease >= 0 accepted) so both the XOR example and the
     # "splitting never increases impurity" invariant hold; pure nodes and
     # constant features still return None.
-    if best is None or best[0] > parent:
+    if best is None or best[0] > parent + 1e-15:
         return None
     return best[1], best[2], best[0]
 
 
-def _majority(y, n_classes: int) -> int:
-    counts = np.bincount(np.asarray(y, dtype=np.int64), minlength=n_classes)
+def _majority(y, n_classes: int, w=None) -> int:
+    counts = np.bincount(np.asarray(y, dtype=np.int64), weights=w, minlength=n_classes)
     return int(np.argmax(counts))  # argmax returns the lowest index on ties
 
 
@@ -237,8 +249,9 @@ def leaf_tree(cls: int, n_classes: int, n_features: int, feature_names=()) -> De
 
 
 def train_tree(X, y, max_depth: int = 5, min_samples_leaf: int = 1, n_classes: int | None = None,
-               feature_names=()) -> DecisionTree:
-    """Recursive CART with Gini; deterministic for fixed input order."""
+               feature_names=(), sample_weight=None) -> DecisionTree:
+    """Recursive CART with Gini; deterministic for fixed input order.
+    ``sample_weight`` is an extension (None = SPEC's plain CART)."""
     X = np.asarray(X, dtype=np.float64)
     y = np.asarray(y, dtype=np.int64)
     if y.size == 0:
@@ -248,14 +261,16 @@ def train_tree(X, y, max_depth: int = 5, min_samples_leaf: int = 1, n_classes: i
     if max_depth < 0:
         raise ValueError("max_depth must be >= 0")
     k = int(n_classes if n_classes is not None else y.max() + 1)
+    sw = None if sample_weight is None else np.asarray(sample_weight, dtype=np.float64)
     t = DecisionTree(n_classes=k, n_features=X.shape[1], max_depth=max_depth, feature_names=list(feature_names))
 
     def grow(idx: np.ndarray, depth: int) -> int:
         yy = y[idx]
-        node = t._add(-1, 0.0, _majority(yy, k))
+        ww = None if sw is None else sw[idx]
+        node = t._add(-1, 0.0, _majority(yy, k, ww))
         if depth >= max_depth or np.all(yy == yy[0]) or idx.size < 2 * min_samples_leaf:
             return node
-        s = best_split(X[idx], yy, min_samples_leaf, k)
+        s = best_split(X[idx], yy, min_samples_leaf, k, ww)
         if s is None:
             return node
         f, thr, _ = s

@@ -202,12 +202,19 @@ def selector_label(row, known_pred: int, gathered_pred: int, k: int) -> int:
 
 
 def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int = 1,
-               kernels=KERNELS, meta: dict | None = None) -> SeerModel:
+               kernels=KERNELS, meta: dict | None = None, weighting: str = "none") -> SeerModel:
     """labels = fastest_kernel per (matrix, k); known tree on the known
     schema, gathered tree on the full schema, selector on labels from the two
-    sub-models' own predictions on the training rows."""
+    sub-models' own predictions on the training rows.
+
+    weighting="none" is SPEC's plain CART.  weighting="regret" (extension) weights each
+    example by what a wrong decision costs relative to the matrix's best time:
+    kernel trees by log1p(mean relative regret over the other kernels), the selector by
+    |log(realised gathered-path cost / realised known-path cost)| -- measured kernel
+    families have 100-1000x outliers (thread-mapped schedules on 1M-nnz rows) that
+    unweighted CART treats like a 1% miss."""
     nk = len(kernels)
-    Xk, Xg, y, ex = [], [], [], []
+    Xk, Xg, y, ex, wk = [], [], [], [], []
     for r in rows:
         if r.gathered is None:
             raise ValueError(f"row {r.name!r} has no gathered features")
@@ -221,12 +228,27 @@ def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int 
             Xg.append(kv + tuple(r.gathered))
             y.append(lab)
             ex.append((r, k))
+            best = r.cost(lab, k)
+            regrets = [(r.cost(j, k) - best) / best for j in range(nk)
+                       if j != lab and np.isfinite(r.cost(j, k))]
+            wk.append(float(np.log1p(np.mean(regrets))) if regrets else 0.0)
     if not y:
         raise ValueError("no labelled examples")
-    kt = train_tree(Xk, y, max_depth, min_samples_leaf, nk, KNOWN_SCHEMA)
-    gt = train_tree(Xg, y, max_depth, min_samples_leaf, nk, GATHERED_SCHEMA)
-    ys = [selector_label(r, kt.predict(xk), gt.predict(xg), k) for (r, k), xk, xg in zip(ex, Xk, Xg)]
-    st = train_tree(Xk, ys, max_depth, min_samples_leaf, 2, KNOWN_SCHEMA)
+    if weighting not in ("none", "regret"):
+        raise ValueError("weighting must be 'none' or 'regret'")
+    w = None if weighting == "none" else np.asarray(wk) + 1e-3
+    kt = train_tree(Xk, y, max_depth, min_samples_leaf, nk, KNOWN_SCHEMA, w)
+    gt = train_tree(Xg, y, max_depth, min_samples_leaf, nk, GATHERED_SCHEMA, w)
+    ys, wsel = [], []
+    for (r, k), xk, xg in zip(ex, Xk, Xg):
+        kp, gp = kt.predict(xk), gt.predict(xg)
+        ys.append(selector_label(r, kp, gp, k))
+        ck, cg = r.cost(kp, k), r.cost(gp, k) + r.collection_time
+        wsel.append(abs(float(np.log(cg / ck))) if np.isfinite(ck) and np.isfinite(cg) else 10.0)
+    ws = None if weighting == "none" else np.asarray(wsel) + 1e-3
+    st = train_tree(Xk, ys, max_depth, min_samples_leaf, 2, KNOWN_SCHEMA, ws)
+    meta = dict(meta or {})
+    meta.setdefault("weighting", weighting)
     return SeerModel(kt, gt, st, kernels, meta)
 
 

@@ -1,0 +1,222 @@
+"""Measure every kernel on a synthetic B200 corpus -> Seer training data (GPU).
+
+    python tools/collect_corpus.py --out DIR [--quick]
+
+Writes the SPEC.md:246 artifact files into DIR:
+  elapsed.csv     name + one column per kernel: seconds per SpMV iteration (median, L2 flushed)
+  preprocess.csv  name + one column per kernel: seconds of one-time preprocessing (0 if none)
+  metadata.csv    name, max/min/mean/var density, collection_time (device time of the fused
+                  feature pass, kp_gather_features)
+  known.csv       name, rows, cols, nnz
+Times are CUDA-event device times on the launching stream (PAPER.md:331 uses 10 warm-ups +
+mean of 10; we use 2 warm-ups + median of 5, enough for ranking).  A kernel slower than
+--cap-ms on its first run is recorded from that run only.
+"""
+
+from __future__ import annotations
+
+import argparse
+import csv
+import os
+import statistics
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import torch  # noqa: E402
+
+from paper_2403_17017_b200 import features, gen, kernels  # noqa: E402
+
+
+def corpus(quick: bool, extra: int = 400):
+    C = []
+    for R in (10_000, 100_000, 1_000_000, 4_000_000):
+        for per in (2, 8, 32):
+            if R * per <= 64_000_000:
+                C.append(("uniform", dict(n_rows=R, n_cols=R, n_pairs=R * per, seed=R + per)))
+    for R in (100_000, 1_000_000, 8_000_000):
+        for ln in (1, 3, 8, 24, 64):
+            if R * ln <= 128_000_000:
+                C.append(("const", dict(n_rows=R, length=ln, seed=ln)))
+    for R in (100_000, 1_000_000, 8_000_000):
+        for w in (3, 7, 27, 100):
+            if R * w <= 220_000_000:
+                C.append(("band", dict(n_rows=R, width=w)))
+    C += [("band", dict(n_rows=65_536, width=1024)), ("band", dict(n_rows=65_536, width=2048)),
+          ("band", dict(n_rows=8_192, width=8_192))]
+    for n in (20, 50, 100, 159):
+        C.append(("stencil", dict(n=n)))
+    for R in (100_000, 1_000_000, 4_000_000):
+        for mean in (4.0, 16.0, 64.0):
+            for alpha in (1.2, 1.5, 2.5):
+                if R * mean <= 128_000_000:
+                    C.append(("powerlaw", dict(n_rows=R, mean=mean, alpha=alpha, seed=int(mean * 10 + alpha * 100))))
+    for scale in (12, 14, 16, 18, 20, 22):
+        for ef in (4, 16):
+            if (1 << scale) * ef <= 80_000_000:
+                C.append(("rmat", dict(scale=scale, edge_factor=ef, seed=scale * 7 + ef)))
+    for R in (200_000, 2_000_000):
+        for nd in (1, 4, 16):
+            for dl in (10_000, 100_000, 1_000_000):
+                if dl <= R:
+                    C.append(("skewed", dict(n_rows=R, n_dense=nd, dense_len=dl, seed=nd + dl % 97)))
+    # seeded random draws per family (log-uniform sizes) for coverage between the grid points
+    import numpy as np
+    rng = np.random.default_rng(20240317)
+    lu = lambda lo, hi: float(np.exp(rng.uniform(np.log(lo), np.log(hi))))  # noqa: E731
+    for i in range(extra):
+        fam = ["uniform", "const", "band", "powerlaw", "rmat", "skewed", "stencil"][i % 7]
+        sd = 1000 + i
+        if fam == "uniform":
+            R = int(lu(5e3, 6e6)); per = lu(1, 64)
+            if R * per > 1.2e8: per = 1.2e8 / R
+            C.append(("uniform", dict(n_rows=R, n_cols=int(R * lu(0.2, 5)), n_pairs=int(R * per), seed=sd)))
+        elif fam == "const":
+            R = int(lu(5e3, 8e6)); ln = max(1, int(lu(1, 128)))
+            if R * ln > 1.2e8: ln = max(1, int(1.2e8 / R))
+            C.append(("const", dict(n_rows=R, length=ln, seed=sd)))
+        elif fam == "band":
+            R = int(lu(5e3, 8e6)); w = max(1, int(lu(1, 512)))
+            if R * w > 1.5e8: w = max(1, int(1.5e8 / R))
+            C.append(("band", dict(n_rows=R, width=w)))
+        elif fam == "powerlaw":
+            R = int(lu(5e3, 6e6)); mean = lu(2, 128); al = float(rng.uniform(1.1, 3.0))
+            if R * mean > 1.2e8: mean = 1.2e8 / R
+            C.append(("powerlaw", dict(n_rows=R, mean=round(mean, 2), alpha=round(al, 2), seed=sd)))
+        elif fam == "rmat":
+            sc = int(rng.integers(11, 22)); ef = int(rng.choice([2, 4, 8, 16, 32]))
+            if (1 << sc) * ef > 8e7: ef = max(1, int(8e7 / (1 << sc)))
+            C.append(("rmat", dict(scale=sc, edge_factor=ef, seed=sd)))
+        elif fam == "skewed":
+            R = int(lu(5e4, 4e6)); nd = int(rng.integers(1, 32)); dl = int(min(R, lu(1e3, 2e6)))
+            C.append(("skewed", dict(n_rows=R, n_dense=nd, dense_len=dl, seed=sd)))
+        else:
+            C.append(("stencil", dict(n=int(lu(8, 170)))))
+    if quick:
+        C = C[::6]
+    uniq, seen = [], set()  # random draws can repeat a grid point (e.g. a stencil size)
+    for fam, p in C:
+        key = (fam, tuple(sorted(p.items())))
+        if key not in seen:
+            seen.add(key)
+            uniq.append((fam, p))
+    return uniq
+
+
+def build(fam, p, dev):
+    if fam == "uniform":
+        return gen.uniform_random(p["n_rows"], p["n_cols"], p["n_pairs"], p["seed"], device=dev)
+    if fam == "const":
+        return gen.constant_rows(p["n_rows"], p["length"], p["seed"], device=dev)
+    if fam == "band":
+        return gen.banded(p["n_rows"], p["width"], device=dev)
+    if fam == "stencil":
+        return gen.stencil27(p["n"], device=dev)
+    if fam == "powerlaw":
+        return gen.powerlaw_rows(p["n_rows"], p["mean"], p["alpha"], p["seed"], device=dev)
+    if fam == "rmat":
+        return gen.rmat(p["scale"], p["edge_factor"], seed=p["seed"], device=dev)
+    if fam == "skewed":
+        return gen.skewed(p["n_rows"], 8.0, p["n_dense"], p["dense_len"], p["seed"], device=dev)
+    raise ValueError(fam)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--extra", type=int, default=400, help="seeded random draws on top of the grid")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--cap-ms", type=float, default=40.0)
+    a = ap.parse_args()
+    os.makedirs(a.out, exist_ok=True)
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
+    rows_el, rows_pp, rows_md, rows_kn = [], [], [], []
+    t_start = time.time()
+    for fam, p in corpus(a.quick, a.extra):
+        m = build(fam, p, dev)
+        name = fam + "_" + "_".join(f"{k}{v}" for k, v in p.items())
+        A = m.to_device_csr(torch.float32, device=dev)
+        del m
+        x = (torch.rand(A.n_cols, device=dev, dtype=torch.float64) * 2 - 1).float()
+        y = torch.empty(A.n_rows, device=dev, dtype=torch.float32)
+        # gathered features + device collection time
+        for _ in range(2):
+            buf = features.gather_outcome(A)
+        cts = []
+        for _ in range(5):
+            flush.zero_()
+            e0, e1 = ev(), ev()
+            e0.record()
+            buf = features.gather_outcome(A, out=buf)
+            e1.record()
+            e1.synchronize()
+            cts.append(e0.elapsed_time(e1) * 1e-3)
+        o = features.decode_outcome(buf)
+        rows_md.append([name, o.max_d, o.min_d, o.mean_d, o.var_d, statistics.median(cts)])
+        rows_kn.append([name, A.n_rows, A.n_cols, A.nnz])
+        el, pp = [], []
+        for k in range(len(kernels.KERNELS)):
+            try:
+                P, tprep = None, 0.0
+                if k in kernels.NEEDS_PREP:
+                    ts = []
+                    for _ in range(3):
+                        e0, e1 = ev(), ev()
+                        e0.record()
+                        P = kernels.prepare(A, k, cache=False)
+                        e1.record()
+                        e1.synchronize()
+                        ts.append(e0.elapsed_time(e1) * 1e-3)
+                    tprep = min(ts[1:])  # first call may include a cudaMalloc
+                ts = []
+                for r in range(a.reps + 1):
+                    flush.zero_()
+                    e0, e1 = ev(), ev()
+                    e0.record()
+                    kernels.spmv(A, x, k, y=y, prepared=P)
+                    e1.record()
+                    e1.synchronize()
+                    t = e0.elapsed_time(e1) * 1e-3
+                    if r > 0 or t * 1e3 > a.cap_ms:
+                        ts.append(t)
+                    if t * 1e3 > a.cap_ms:
+                        break
+                el.append(statistics.median(ts))
+                pp.append(tprep)
+                del P
+            except Exception as exc:  # record as missing (+inf cost)
+                print(f"  {name} {kernels.KERNELS[k]} failed: {exc}", flush=True)
+                el.append(None)
+                pp.append(None)
+        rows_el.append([name, *el])
+        rows_pp.append([name, *pp])
+        best = min(range(8), key=lambda i: el[i] if el[i] is not None else 1e9)
+        print(f"{name:55s} R={A.n_rows:9d} nnz={A.nnz:11d} best={kernels.KERNELS[best]:13s} "
+              f"{el[best] * 1e6:9.1f} us  coll={statistics.median(cts) * 1e6:6.1f} us  [{time.time() - t_start:5.0f}s]",
+              flush=True)
+        del A, x, y
+        torch.cuda.empty_cache()
+
+    def dump(fn, head, rows):
+        with open(os.path.join(a.out, fn), "w", newline="") as f:
+            w = csv.writer(f, lineterminator="\n")
+            w.writerow(head)
+            for r in rows:
+                w.writerow(["" if v is None else (repr(float(v)) if isinstance(v, float) else v) for v in r])
+
+    labels = list(kernels.KERNELS)
+    dump("elapsed.csv", ["name", *labels], rows_el)
+    dump("preprocess.csv", ["name", *labels], rows_pp)
+    dump("metadata.csv", ["name", "max_density", "min_density", "mean_density", "var_density", "collection_time"],
+         rows_md)
+    dump("known.csv", ["name", "rows", "cols", "nnz"], rows_kn)
+    print(f"wrote {len(rows_el)} matrices to {a.out}")
+
+
+if __name__ == "__main__":
+    main()
