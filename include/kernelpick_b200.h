@@ -164,6 +164,22 @@ KP_API int kp_spmv_workspace_bytes(int32_t kernel, const kp_csr *A, size_t *byte
 KP_API int kp_spmv(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x,
             void *d_y, void *d_ws, size_t ws_bytes, void *stream);
 
+/* ------------------------------------------------------------ Seer plan (one CUDA graph) */
+/* The whole pipeline -- kp_seer_select, then the chosen kernel's kp_prepare and
+ * `iterations` kp_spmv -- as one CUDA graph whose conditional SWITCH node is steered on
+ * the device by the selected kernel index (no host round trip).  The matrix, x, y, trees,
+ * outcome and reduction workspace are bound at creation; d_buf (kp_seer_plan_bytes) holds
+ * every kernel's prepared format and the SpMV workspace.  `stream` must be a created
+ * (non-legacy) stream; creation captures through it. */
+typedef struct kp_seer_plan kp_seer_plan;
+KP_API int kp_seer_plan_bytes(const kp_csr *A, int64_t ell_cap, size_t *bytes);
+KP_API int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap,
+                               const void *d_selector, const void *d_known, const void *d_gathered,
+                               const void *d_x, void *d_y, void *d_buf, size_t bytes, void *d_red_ws,
+                               kp_outcome *d_out, kp_seer_plan **plan, void *stream);
+KP_API int kp_seer_plan_launch(kp_seer_plan *plan, void *stream);
+KP_API int kp_seer_plan_destroy(kp_seer_plan *plan);
+
 /* ------------------------------------------------------------ multi-GPU (K14) */
 /* nnz-balanced row cut: d_cuts[p] = lower_bound(row_offsets, p*nnz/parts), p = 0..parts
  * (d_cuts[parts] = n_rows). */

@@ -24,7 +24,8 @@ KP_USE_KNOWN, KP_USE_GATHERED = 0, 1
 EXPORTS = (
     "kp_reduce_workspace_bytes", "kp_length_stats", "kp_wave_ceil_max_sum", "kp_gather_features",
     "kp_tree_predict", "kp_seer_select", "kp_prepare_bytes", "kp_prepare",
-    "kp_spmv_workspace_bytes", "kp_spmv", "kp_shard_partition", "kp_version", "kp_launch_count",
+    "kp_spmv_workspace_bytes", "kp_spmv", "kp_seer_plan_bytes", "kp_seer_plan_create", "kp_seer_plan_launch",
+    "kp_seer_plan_destroy", "kp_shard_partition", "kp_version", "kp_launch_count",
 )
 
 
@@ -84,6 +85,10 @@ def load(require: bool = True):
         "kp_prepare": (ctypes.c_int, [i32, P(kp_csr), i64, p, sz, P(kp_prepared), p]),
         "kp_spmv_workspace_bytes": (ctypes.c_int, [i32, P(kp_csr), P(sz)]),
         "kp_spmv": (ctypes.c_int, [i32, P(kp_csr), P(kp_prepared), p, p, p, sz, p]),
+        "kp_seer_plan_bytes": (ctypes.c_int, [P(kp_csr), i64, P(sz)]),
+        "kp_seer_plan_create": (ctypes.c_int, [P(kp_csr), i64, i64, p, p, p, p, p, p, sz, p, p, P(p), p]),
+        "kp_seer_plan_launch": (ctypes.c_int, [p, p]),
+        "kp_seer_plan_destroy": (ctypes.c_int, [p]),
         "kp_shard_partition": (ctypes.c_int, [p, i32, i64, i32, p, p]),
         "kp_version": (ctypes.c_char_p, []),
         "kp_launch_count": (ctypes.c_uint64, []),

@@ -23,6 +23,7 @@
 namespace kp {
 int launch_k1_stats_into(const void *off, int32_t off_type, int64_t n_rows, int64_t *out4, void *ws,
                          cudaStream_t s);
+int ensure_kernel_attrs();
 }
 
 namespace kp {
@@ -296,6 +297,13 @@ __global__ void __launch_bounds__(256) k_ell_tm(const PrepHeader *__restrict__ h
         for (int64_t j = s + W; j < e; j += 4) sum = batch_dot<4, 1>(col, val, x, j, e, sum);
     }
     y[row] = sum;
+}
+
+__global__ void k_prep_hdr(PrepHeader *hdr, int64_t kernel, int64_t cap) {
+    PrepHeader h = {};
+    h.kernel = kernel;
+    h.cap = cap;
+    *hdr = h;
 }
 
 // K12: CSR -> warp-sliced column-major ELL of width W = min(max_len, cap): slot (row, k)
@@ -1070,10 +1078,9 @@ int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, 
     const V *val = reinterpret_cast<const V *>(A->values);
     switch (kernel) {
         case KP_ELL_TM: {
-            PrepHeader h = {};
-            h.kernel = kernel;
-            h.cap = cap;
-            KP_CUDA_TRY(cudaMemcpyAsync(hdr, &h, sizeof(h), cudaMemcpyHostToDevice, s));
+            // header written by a kernel (no host-memory copy: plans capture this into a graph)
+            k_prep_hdr<<<1, 1, 0, s>>>(hdr, kernel, cap);
+            KP_LAUNCHED();
             KP_CUDA_TRY(cudaMemsetAsync(buf + L.red, 0, kRedWsBytes, s));
             int rc = launch_k1_stats_into(A->row_offsets, A->off_type, A->n_rows, hdr->stats, buf + L.red, s);
             if (rc) return rc;
@@ -1127,6 +1134,19 @@ int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, 
     return KP_OK;
 }
 
+// Opt-in shared memory for the TMA CSR,TM kernel (once per <V, O>; also called before a
+// plan's graph capture so no attribute call happens inside a capture).
+template <typename V, typename O>
+int tm_attrs() {
+    static bool done = false;
+    if (done) return KP_OK;
+    const int smem = (int)(kTmStages * TmCfg<V, O>::kStageBytes);
+    KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    done = true;
+    return KP_OK;
+}
+
 template <typename V, typename O>
 int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V *y, unsigned char *ws,
            cudaStream_t s) {
@@ -1167,11 +1187,9 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
             const int64_t tiles = (R + (int64_t)kTmRows * rpt - 1) / ((int64_t)kTmRows * rpt);
             const int per_sm = (int)((227 * 1024) / (smem + 1024));
             const int64_t g = tiles < (int64_t)sms * per_sm ? tiles : (int64_t)sms * per_sm;
-            static bool done = false;  // one static per <V, O> instantiation of spmv_t
-            if (!done) {
-                KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-                done = true;
+            {
+                const int rc = tm_attrs<V, O>();
+                if (rc) return rc;
             }
             if (aligned) k_csr_tm<V, O, true><<<(unsigned)g, kTmRows + 32, smem, s>>>(off, col, val, x, y, R, rpt);
             else k_csr_tm<V, O, false><<<(unsigned)g, kTmRows + 32, smem, s>>>(off, col, val, x, y, R, rpt);
@@ -1246,6 +1264,14 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
 using namespace kp;
 
 extern "C" int kp_length_stats(const void *, int32_t, int64_t, int64_t *, void *, void *);
+
+int kp::ensure_kernel_attrs() {
+    int rc = tm_attrs<float, int32_t>();
+    if (!rc) rc = tm_attrs<float, int64_t>();
+    if (!rc) rc = tm_attrs<double, int32_t>();
+    if (!rc) rc = tm_attrs<double, int64_t>();
+    return rc;
+}
 
 int kp::launch_k1_stats_into(const void *off, int32_t off_type, int64_t n_rows, int64_t *out4, void *ws,
                              cudaStream_t s) {

@@ -192,6 +192,64 @@ class SeerRunner:
         return y, o
 
 
+class SeerPlan:
+    """The whole pipeline (select -> chosen kernel's preprocessing -> k SpMVs) as one CUDA
+    graph with device-side dispatch (``kp_seer_plan_*``): no host round trip per run.
+
+    Binds ``A``, ``x`` and ``y`` (their device buffers; contents may change between
+    launches).  ``launch()`` enqueues one graph launch on the current (or given) stream;
+    ``outcome()`` reads the selection the last launch made."""
+
+    def __init__(self, model: SeerModel, A, x, y, k: int = 1, ell_cap: int | None = None):
+        import ctypes
+        torch = _lib.require_cuda()
+        from .device import as_device
+        from .kernels import default_ell_cap
+        self.A = as_device(A)
+        if x.dtype != self.A.values.dtype or y.dtype != self.A.values.dtype:
+            raise ValueError("x / y must have the matrix value dtype")
+        self.x, self.y, self.k = x, y, int(k)
+        L = _lib.load()
+        cap = int(ell_cap) if ell_cap else default_ell_cap(self.A)
+        nbytes = ctypes.c_size_t(0)
+        _lib.check(L.kp_seer_plan_bytes(ctypes.byref(self.A.struct), cap, ctypes.byref(nbytes)), "kp_seer_plan_bytes")
+        dev = self.A.device
+        self.buf = torch.empty(max(int(nbytes.value), 256), dtype=torch.uint8, device=dev)
+        self.out = torch.zeros(_lib.OUTCOME_BYTES, dtype=torch.uint8, device=dev)
+        self.red = torch.zeros(int(L.kp_reduce_workspace_bytes()), dtype=torch.uint8, device=dev)
+        self.trees = model.device_trees(dev)
+        sel, kn, ga = self.trees
+        cap_stream = torch.cuda.Stream(device=dev)  # graph capture needs a created stream
+        torch.cuda.synchronize(dev)
+        handle = ctypes.c_void_p()
+        rc = L.kp_seer_plan_create(ctypes.byref(self.A.struct), self.k, cap, sel.data_ptr(), kn.data_ptr(),
+                                   ga.data_ptr(), x.data_ptr(), y.data_ptr(), self.buf.data_ptr(), self.buf.numel(),
+                                   self.red.data_ptr(), self.out.data_ptr(), ctypes.byref(handle),
+                                   int(cap_stream.cuda_stream))
+        _lib.check(rc, "kp_seer_plan_create")
+        torch.cuda.synchronize(dev)
+        self._handle = handle
+        self._L = L
+
+    def launch(self, stream=None) -> None:
+        _lib.check(self._L.kp_seer_plan_launch(self._handle, _lib.stream_handle(stream)), "kp_seer_plan_launch")
+
+    def outcome(self):
+        from .features import decode_outcome
+        return decode_outcome(self.out)
+
+    def close(self) -> None:
+        if getattr(self, "_handle", None) is not None and self._handle.value:
+            self._L.kp_seer_plan_destroy(self._handle)
+            self._handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 # ---------------------------------------------------------------------- training
 def selector_label(row, known_pred: int, gathered_pred: int, k: int) -> int:
     """SPEC.md:367-375: USE_GATHERED iff cost(gathered_pred) + collection < cost(known_pred);

@@ -65,3 +65,29 @@ def test_runner_end_to_end(orc):
     off, col, val = A.to_host()
     yref, absy = orc.spmv_csr(off, col, val, x.cpu().numpy())
     assert orc.spmv_check(y.cpu().numpy(), yref, absy, 1e-5)[0]
+
+
+@pytest.mark.parametrize("name,k", [("C1", 1), ("C2", 1), ("C3", 3), ("C4", 2)])
+def test_plan_graph_matches_host_dispatch(name, k, orc):
+    """The one-graph pipeline (device-side SWITCH) selects the same kernel as the
+    host-dispatched path and produces bit-identical y."""
+    import os
+    m = gen.config(name, small=name != "C1")
+    A = m.to_device_csr(torch.float64 if name == "C4" else torch.float32)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    model = seer.SeerModel.load(os.path.join(root, "paper_2403_17017_b200", "models", "seer_b200.json"))
+    x = (torch.rand(A.n_cols, device="cuda", dtype=torch.float64) * 2 - 1).to(A.values.dtype)
+    y_plan = torch.full((A.n_rows,), float("nan"), device="cuda", dtype=A.values.dtype)
+    plan = seer.SeerPlan(model, A, x, y_plan, k)
+    for _ in range(3):
+        plan.launch()
+    torch.cuda.synchronize()
+    o = plan.outcome()
+    y_host, o2 = seer.SeerRunner(model).run(A, x, k=k)
+    assert (o.kernel, o.path) == (o2.kernel, o2.path)
+    assert torch.equal(y_plan, y_host)
+    off, col, val = A.to_host()
+    yref, absy = orc.spmv_csr(off, col, val, x.cpu().numpy())
+    tol = 1e-12 if name == "C4" else 1e-5
+    assert orc.spmv_check(y_plan.cpu().numpy(), yref, absy, tol)[0]
+    plan.close()
