@@ -49,27 +49,24 @@ struct RedWorkspace {
 enum Mode : int { kModeStats = 0, kModeFeatures = 1, kModeSeer = 2 };
 
 // ------------------------------------------------------------------ trees in smem
-constexpr int kMaxTreeNodes = 1023;  // depth <= 9 complete tree; SPEC default depth 5 -> 63
+constexpr int kMaxTreeNodes = 255;  // staged in smem (depth <= 7); larger trees are walked in global memory
 
 struct SmemTree {
     int32_t n;
+    const void *src;
     kp_tree_node node[kMaxTreeNodes];
 };
 
 __device__ __forceinline__ void load_tree(SmemTree &t, const void *d_tree) {
     const kp_tree_header *h = reinterpret_cast<const kp_tree_header *>(d_tree);
     const kp_tree_node *src = reinterpret_cast<const kp_tree_node *>(h + 1);
-    int n = h->n_nodes;
-    if (n > kMaxTreeNodes) n = kMaxTreeNodes;
-    if (threadIdx.x == 0) t.n = n;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) t.node[i] = src[i];
-}
-
-// SPEC.md:296-301: root-to-leaf, x[f] <= thr goes left.
-__device__ __forceinline__ int32_t predict_smem(const SmemTree &t, const double *x) {
-    int32_t i = 0;
-    while (t.node[i].feature >= 0) i = (x[t.node[i].feature] <= t.node[i].threshold) ? t.node[i].left : t.node[i].right;
-    return t.node[i].value;
+    const int n = h->n_nodes;
+    if (threadIdx.x == 0) {
+        t.n = n;
+        t.src = d_tree;
+    }
+    if (n <= kMaxTreeNodes)
+        for (int i = threadIdx.x; i < n; i += blockDim.x) t.node[i] = src[i];
 }
 
 __device__ __forceinline__ int32_t predict_global(const void *d_tree, const double *x) {
@@ -81,6 +78,14 @@ __device__ __forceinline__ int32_t predict_global(const void *d_tree, const doub
         if (v.feature < 0) return v.value;
         i = (x[v.feature] <= v.threshold) ? v.left : v.right;
     }
+}
+
+// SPEC.md:296-301: root-to-leaf, x[f] <= thr goes left.
+__device__ __forceinline__ int32_t predict_smem(const SmemTree &t, const double *x) {
+    if (t.n > kMaxTreeNodes) return predict_global(t.src, x);
+    int32_t i = 0;
+    while (t.node[i].feature >= 0) i = (x[t.node[i].feature] <= t.node[i].threshold) ? t.node[i].left : t.node[i].right;
+    return t.node[i].value;
 }
 
 // ------------------------------------------------------------------ fp64 epilogue
@@ -149,21 +154,29 @@ __device__ __forceinline__ void stats_accum(const O *__restrict__ off, int64_t n
     if constexpr (kVec) {
         constexpr int V = Vec16<O>::V;
         const int64_t nvec = n_rows / V;  // vector v covers rows v*V .. v*V+V-1
-        for (int64_t base = gwarp * 32; base < nvec; base += nwarps * 32) {
-            const int64_t v = base + lane;
-            const bool act = v < nvec;
-            int64_t e[V];
-            if (act) Vec16<O>::load(off + v * V, e);
-            else {
+        // two independent 16-byte vectors per lane per iteration (64 warps x 1 KB in flight per SM)
+        for (int64_t base = gwarp * 64; base < nvec; base += nwarps * 64) {
+            int64_t e[2][V];
 #pragma unroll
-                for (int k = 0; k < V; ++k) e[k] = 0;
+            for (int h = 0; h < 2; ++h) {
+                const int64_t v = base + h * 32 + lane;
+                if (v < nvec) Vec16<O>::load(off + v * V, e[h]);
+                else {
+#pragma unroll
+                    for (int k = 0; k < V; ++k) e[h][k] = 0;
+                }
             }
-            int64_t nxt = __shfl_down_sync(0xffffffffu, e[0], 1);
-            if (act && (lane == 31 || v + 1 >= nvec)) nxt = ldo(off + (v + 1) * V);
-            if (act) {
 #pragma unroll
-                for (int k = 0; k < V - 1; ++k) acc_len(e[k], e[k + 1], lo, hi, s2);
-                acc_len(e[V - 1], nxt, lo, hi, s2);
+            for (int h = 0; h < 2; ++h) {
+                const int64_t v = base + h * 32 + lane;
+                const bool act = v < nvec;
+                int64_t nxt = __shfl_down_sync(0xffffffffu, e[h][0], 1);
+                if (act && (lane == 31 || v + 1 >= nvec)) nxt = ldo(off + (v + 1) * V);
+                if (act) {
+#pragma unroll
+                    for (int k = 0; k < V - 1; ++k) acc_len(e[h][k], e[h][k + 1], lo, hi, s2);
+                    acc_len(e[h][V - 1], nxt, lo, hi, s2);
+                }
             }
         }
         // scalar tail rows [nvec*V, n_rows)
@@ -432,11 +445,11 @@ int grid_for(int64_t n_rows, int per_thread) {
 int launch_k1(K1Args a, int32_t off_type, cudaStream_t s) {
     const bool aligned = ((uintptr_t)a.off & 15) == 0;
     if (off_type == KP_I32) {
-        int g = grid_for(a.n_rows, 4);
+        int g = grid_for(a.n_rows, 8);
         if (aligned) k_row_stats<int32_t, true><<<g, kRedThreads, 0, s>>>(a);
         else k_row_stats<int32_t, false><<<g, kRedThreads, 0, s>>>(a);
     } else if (off_type == KP_I64) {
-        int g = grid_for(a.n_rows, 2);
+        int g = grid_for(a.n_rows, 4);
         if (aligned) k_row_stats<int64_t, true><<<g, kRedThreads, 0, s>>>(a);
         else k_row_stats<int64_t, false><<<g, kRedThreads, 0, s>>>(a);
     } else {

@@ -327,46 +327,6 @@ __global__ void __launch_bounds__(256) k_prep_ell(const PrepHeader *__restrict__
     }
 }
 
-// ================================================================= carries / fix-up
-// A unit u (COO chunk, merge tile, adaptive long piece) that leaves row rho unfinished
-// records carry_row[u] = rho, carry_val[u] = its partial (carry_row = -1: none).  The
-// unit that finishes rho wrote y[rho] = its own partial.  Fix-up: each warp takes 32
-// units; for every run start (carry_row[u] >= 0, != carry_row[u-1]) the whole warp
-// sums the run's carries (lane-strided, shuffle tree: fixed order) into y[rho].
-template <typename V>
-__global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__ crow, const V *__restrict__ cval,
-                                                     const int64_t *__restrict__ n_units_dev, int64_t n_units_host,
-                                                     V *__restrict__ y) {
-    const int64_t n_units = n_units_dev ? *n_units_dev : n_units_host;
-    const int lane = threadIdx.x & 31;
-    const int64_t wbase = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
-    if (wbase >= n_units) return;
-    const int64_t u = wbase + lane;
-    int32_t r = -1;
-    bool start = false;
-    if (u < n_units) {
-        r = crow[u];
-        start = r >= 0 && (u == 0 || crow[u - 1] != r);
-    }
-    unsigned starts = __ballot_sync(0xffffffffu, start);
-    while (starts) {
-        const int src = __ffs(starts) - 1;
-        starts &= starts - 1;
-        const int32_t rho = __shfl_sync(0xffffffffu, r, src);
-        const int64_t u0 = wbase + src;
-        V acc = 0;
-        for (int64_t b = u0;; b += 32) {
-            const int64_t q = b + lane;
-            const bool in = q < n_units && crow[q] == rho;
-            if (in) acc += cval[q];
-            const unsigned m = __ballot_sync(0xffffffffu, in);
-            if (m != 0xffffffffu) break;  // run ended inside this batch (runs are contiguous)
-        }
-        acc = group_sum<32>(acc);
-        if (lane == 0) y[rho] += acc;
-    }
-}
-
 // ================================================================= block-level segmented scan
 // Inclusive scan over threads of (flag, value) with op (fa,va)o(fb,vb) = (fa|fb, fb ? vb : va+vb).
 template <typename V>
@@ -405,6 +365,60 @@ __device__ __forceinline__ SegPair<V> block_seg_exscan(SegPair<V> p, SegPair<V> 
     if (w > 0) ex = seg_op(swarp[w - 1], ex);
     total = swarp[nw - 1];
     return ex;
+}
+
+// ================================================================= carries / fix-up
+// A unit u (COO chunk, merge tile, adaptive long piece) that leaves row rho unfinished
+// records carry_row[u] = rho, carry_val[u] = its partial (carry_row = -1: none).  The
+// unit that finishes rho wrote y[rho] = its own partial.  Fix-up: a warp takes 32
+// consecutive units (lane = unit), segments them by carry row with a shuffle scan
+// (fixed order) and the last lane of each run adds the run's sum to y[rho].  A run that
+// continues past the warp's 32 units is finished by the warp where it STARTED, which
+// walks the following units 32 at a time (lane-strided sum + shuffle tree); warps whose
+// first run started earlier skip it.  Deterministic, no atomics.
+template <typename V>
+__global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__ crow, const V *__restrict__ cval,
+                                                     const int64_t *__restrict__ n_units_dev, int64_t n_units_host,
+                                                     V *__restrict__ y) {
+    const int64_t n_units = n_units_dev ? *n_units_dev : n_units_host;
+    const int lane = threadIdx.x & 31;
+    const int64_t wbase = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
+    if (wbase >= n_units) return;
+    const int64_t u = wbase + lane;
+    const int32_t r = u < n_units ? crow[u] : -2;
+    const V v = (u < n_units && r >= 0) ? cval[u] : V(0);
+    int32_t prev = __shfl_up_sync(0xffffffffu, r, 1);
+    if (lane == 0) prev = wbase > 0 ? crow[wbase - 1] : -3;
+    const bool head = r != prev;
+    // inclusive segmented scan within the warp
+    SegPair<V> inc{head ? 1 : 0, v};
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        SegPair<V> t{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
+        if (lane >= o) inc = seg_op(t, inc);
+    }
+    int32_t next = __shfl_down_sync(0xffffffffu, r, 1);
+    if (lane == 31) next = (u + 1 < n_units) ? crow[u + 1] : -4;
+    // does this lane's run start inside this warp?  (lane of the run head)
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    const unsigned below = heads & ((lane == 31) ? 0xffffffffu : ((2u << lane) - 1u));
+    const bool started_here = below != 0;  // a head at or before this lane within the warp
+    const bool run_end_here = next != r;
+    if (r >= 0 && started_here && run_end_here) y[r] += inc.v;
+    // run open at the warp end that started in this warp: continue over later units
+    const bool cont = (lane == 31) && r >= 0 && started_here && !run_end_here;
+    if (__ballot_sync(0xffffffffu, cont)) {
+        const int32_t rho = __shfl_sync(0xffffffffu, r, 31);
+        V acc = 0;
+        for (int64_t b = wbase + 32;; b += 32) {
+            const int64_t q = b + lane;
+            const bool in = q < n_units && crow[q] == rho;
+            if (in) acc += cval[q];
+            if (__ballot_sync(0xffffffffu, in) != 0xffffffffu) break;  // run ends in this batch
+        }
+        acc = group_sum<32>(acc);
+        if (lane == 31) y[rho] += inc.v + acc;
+    }
 }
 
 // ================================================================= merge-path tiles (K6 MP, K7 WO)
@@ -574,15 +588,17 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     }
 }
 
-// K10: merge-path partition, one thread per unit boundary.
+// K10: merge-path partition, one WARP per unit boundary (32-ary search: 5 rounds of
+// parallel probes instead of a 25-step dependent binary search per thread).
 template <typename O>
-__global__ void k_prep_mp(const O *__restrict__ off, int64_t n_rows, int64_t nnz, int64_t n_tiles,
-                          int64_t *__restrict__ part) {
-    const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (p > n_tiles) return;
+__global__ void __launch_bounds__(256) k_prep_mp(const O *__restrict__ off, int64_t n_rows, int64_t nnz,
+                                                 int64_t n_tiles, int64_t *__restrict__ part) {
+    const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (p > n_tiles) return;  // warp-uniform
     const int64_t total = n_rows + nnz;
     const int64_t d = p * kWarpTile < total ? p * kWarpTile : total;
-    part[p] = merge_search_global(off, n_rows, nnz, d);
+    const int64_t i = merge_search_warp(off, n_rows, nnz, d);
+    if ((threadIdx.x & 31) == 0) part[p] = i;
 }
 
 // ================================================================= COO,WM (K8 + K11)
@@ -1106,7 +1122,7 @@ int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, 
         }
         case KP_CSR_MP: {
             const int64_t nt = merge_tiles(A);
-            const int64_t g = (nt + 1 + 255) / 256;
+            const int64_t g = ((nt + 1) * 32 + 255) / 256;
             k_prep_mp<O><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, nt, reinterpret_cast<int64_t *>(buf + L.a));
             KP_LAUNCHED();
             P->n_units = nt;
