@@ -410,11 +410,25 @@ __global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__
     if (__ballot_sync(0xffffffffu, cont)) {
         const int32_t rho = __shfl_sync(0xffffffffu, r, 31);
         V acc = 0;
-        for (int64_t b = wbase + 32;; b += 32) {
-            const int64_t q = b + lane;
-            const bool in = q < n_units && crow[q] == rho;
-            if (in) acc += cval[q];
-            if (__ballot_sync(0xffffffffu, in) != 0xffffffffu) break;  // run ends in this batch
+        // 8 batches of 32 units per trip, all loads issued first; rho never reappears after
+        // its run ends, so matches past the end of the run cannot occur
+        for (int64_t b = wbase + 32;; b += 256) {
+            int32_t rr[8];
+            V vv[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int64_t q = b + 32 * i + lane;
+                rr[i] = q < n_units ? crow[q] : -5;
+                vv[i] = q < n_units ? cval[q] : V(0);
+            }
+            bool open = true;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const bool in = rr[i] == rho;
+                if (in) acc += vv[i];
+                open = open && __ballot_sync(0xffffffffu, in) == 0xffffffffu;
+            }
+            if (!open) break;  // the run ended inside this trip
         }
         acc = group_sum<32>(acc);
         if (lane == 31) y[rho] += inc.v + acc;
@@ -588,17 +602,22 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     }
 }
 
-// K10: merge-path partition, one WARP per unit boundary (32-ary search: 5 rounds of
-// parallel probes instead of a 25-step dependent binary search per thread).
+// K10: merge-path partition without searches.  Row r's end item sits at merge position
+// q_r = off[r+1] + r (strictly increasing), and the coordinate of diagonal d is
+// #{r : q_r < d}; so every unit boundary p*256 in (q_{r-1}, q_r] has coordinate r.  One
+// thread per row scatters r to those boundaries: a single coalesced pass over the
+// offsets, each boundary written exactly once (the last one, d = R + Z, gets R).
 template <typename O>
 __global__ void __launch_bounds__(256) k_prep_mp(const O *__restrict__ off, int64_t n_rows, int64_t nnz,
                                                  int64_t n_tiles, int64_t *__restrict__ part) {
-    const int64_t p = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    if (p > n_tiles) return;  // warp-uniform
-    const int64_t total = n_rows + nnz;
-    const int64_t d = p * kWarpTile < total ? p * kWarpTile : total;
-    const int64_t i = merge_search_warp(off, n_rows, nnz, d);
-    if ((threadIdx.x & 31) == 0) part[p] = i;
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r == 0) part[n_tiles] = n_rows;
+    if (r >= n_rows) return;
+    const int64_t qa = r == 0 ? -1 : ldo(off + r) + r - 1;
+    const int64_t qb = ldo(off + r + 1) + r;
+    const int64_t p_lo = qa < 0 ? 0 : qa / kWarpTile + 1;
+    const int64_t p_hi = qb / kWarpTile;
+    for (int64_t p = p_lo; p <= p_hi; ++p) part[p] = r;
 }
 
 // ================================================================= COO,WM (K8 + K11)
@@ -1122,7 +1141,7 @@ int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, 
         }
         case KP_CSR_MP: {
             const int64_t nt = merge_tiles(A);
-            const int64_t g = ((nt + 1) * 32 + 255) / 256;
+            const int64_t g = (A->n_rows + 255) / 256 > 0 ? (A->n_rows + 255) / 256 : 1;
             k_prep_mp<O><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, nt, reinterpret_cast<int64_t *>(buf + L.a));
             KP_LAUNCHED();
             P->n_units = nt;
