@@ -483,19 +483,20 @@ __device__ __forceinline__ int64_t merge_search_warp(const O *off, int64_t n_row
 constexpr int kWarpTile = 32 * kIPT;  // 256 merge items per warp unit
 constexpr int kMergeWarps = 8;        // warps per CTA
 
-template <typename V>
-struct MergeWarpSmem {
-    int32_t rend[kWarpTile + 1];  // row ends relative to the tile's first nnz, clamped
-    V prod[kWarpTile];
-};
-
 // kPrep: unit coordinates from the K10 partition (CSR,MP); else searched in-kernel (CSR,WO).
+// Unit = merge items [d0, d1): rows r0..r1 (r1 in progress), nnz [j0, j1).  Lane l owns
+// the nnz positions 8l..8l+7 of the unit: (col, val) loads and x gathers straight into
+// registers; the row of each position comes from the unit's row ends staged in shared
+// memory (int32, relative to j0): one binary search for the lane's first position, then
+// a walk.  Thread-local + warp segmented scans (shuffles) give each finished row its sum;
+// rows with no entry inside the unit are written 0 (their carries, if any, arrive in the
+// fix-up); the trailing open row is the unit's carry.
 template <typename V, typename O, bool kPrep>
 __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     const O *__restrict__ off, const int32_t *__restrict__ col, const V *__restrict__ val, const V *__restrict__ x,
     V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, const int64_t *__restrict__ part,
     int32_t *__restrict__ crow, V *__restrict__ cval) {
-    __shared__ MergeWarpSmem<V> smw[kMergeWarps];
+    __shared__ int32_t s_rend[kMergeWarps][kWarpTile + 1];
     __shared__ int64_t s_coord[kMergeWarps + 1];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t tile0 = (int64_t)blockIdx.x * kMergeWarps;
@@ -518,88 +519,94 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     __syncthreads();
     const int64_t tile = tile0 + w;
     if (tile >= n_units) return;
-    MergeWarpSmem<V> &sm = smw[w];
+    int32_t *rend = s_rend[w];
     const int64_t d0 = tile * kWarpTile;
     const int64_t d1 = d0 + kWarpTile < total ? d0 + kWarpTile : total;
     const int64_t r0 = s_coord[w], r1 = s_coord[w + 1];
     const int64_t j0 = d0 - r0, j1 = d1 - r1;
-    const int nr = (int)(r1 - r0);  // row ends consumed in this unit
+    const int nr = (int)(r1 - r0);  // rows finished inside this unit
     const int nz = (int)(j1 - j0);
-    const int nre = (r1 < n_rows) ? nr + 1 : nr;  // + the row in progress at the end
-    {
-        int64_t re[kIPT + 1];
-        int32_t c[kIPT];
-        V v[kIPT];
+    // (col, val) of this lane's 8 positions + row ends, all loads issued before use
+    const int jb = lane * kIPT;
+    int32_t c[kIPT];
+    V v[kIPT];
 #pragma unroll
-        for (int i = 0; i <= kIPT; ++i) {
-            const int k = lane + i * 32;
-            re[i] = k < nre ? ldo(off + r0 + 1 + k) : 0;
-        }
-#pragma unroll
-        for (int i = 0; i < kIPT; ++i) {
-            const int k = lane + i * 32;
-            c[i] = k < nz ? ld_stream(col + j0 + k) : 0;
-            v[i] = k < nz ? ld_stream(val + j0 + k) : V(0);
-        }
-#pragma unroll
-        for (int i = 0; i <= kIPT; ++i) {
-            const int k = lane + i * 32;
-            if (k < nre) {
-                const int64_t rel = re[i] - j0;
-                sm.rend[k] = (int32_t)(rel < kWarpTile + 1 ? rel : kWarpTile + 1);
-            }
-        }
-#pragma unroll
-        for (int i = 0; i < kIPT; ++i) {
-            const int k = lane + i * 32;
-            if (k < nz) sm.prod[k] = v[i] * ld_x(x + c[i]);
-        }
+    for (int t = 0; t < kIPT; ++t) {
+        const bool in = jb + t < nz;
+        c[t] = in ? ld_stream(col + j0 + jb + t) : 0;
+        v[t] = in ? ld_stream(val + j0 + jb + t) : V(0);
     }
+    int64_t re[kIPT + 1];
+#pragma unroll
+    for (int i = 0; i <= kIPT; ++i) {
+        const int k = lane + i * 32;
+        re[i] = k < nr ? ldo(off + r0 + 1 + k) : 0;
+    }
+    V p[kIPT];
+#pragma unroll
+    for (int t = 0; t < kIPT; ++t) p[t] = v[t] * ld_x(x + c[t]);
+#pragma unroll
+    for (int i = 0; i <= kIPT; ++i) {
+        const int k = lane + i * 32;
+        if (k < nr) rend[k] = (int32_t)(re[i] - j0);  // <= nz for finished rows
+    }
+    if (lane == 0) rend[nr] = INT32_MAX;  // the open row never ends inside the unit
     __syncwarp();
-    // lane-local merge of kIPT items starting at local diagonal lane*kIPT
-    const int dt = lane * kIPT;
-    int i, jj;
+    // rows with no entry inside this unit: written 0 (fix-up adds carries from earlier units)
+    for (int i = lane; i < nr; i += 32) {
+        const int lo = i > 0 ? rend[i - 1] : 0;
+        if (rend[i] <= (lo > 0 ? lo : 0)) y[r0 + i] = V(0);
+    }
+    // row index of each owned position
+    int ri[kIPT];
     {
-        int lo = dt - nz > 0 ? dt - nz : 0;
-        int hi = dt < nr ? dt : nr;
+        int lo = 0, hi = nr;  // first i with rend[i] > jb  (rend[nr] = +inf)
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (sm.rend[mid] <= dt - mid - 1) lo = mid + 1;
+            if (rend[mid] <= jb) lo = mid + 1;
             else hi = mid;
         }
-        i = lo;
-        jj = dt - lo;
-    }
-    V acc = 0;
-    int first_row = -1;
-    V first_val = 0;
-    const int dend = dt + kIPT < nr + nz ? dt + kIPT : nr + nz;
-    for (int d = dt; d < dend; ++d) {
-        if (i < nr && sm.rend[i] <= jj) {  // row r0+i ends here
-            if (first_row < 0) { first_row = i; first_val = acc; }
-            else y[r0 + i] = acc;
-            acc = 0;
-            ++i;
-        } else {
-            acc += sm.prod[jj];
-            ++jj;
+        int i = lo;
+#pragma unroll
+        for (int t = 0; t < kIPT; ++t) {
+            while (rend[i] <= jb + t) ++i;
+            ri[t] = i;
         }
     }
-    // warp segmented scan: carry-in for this lane's first finished row
-    SegPair<V> inc{first_row >= 0 ? 1 : 0, acc};
+    // thread-local segmented scan (positions beyond nz carry p = 0 and never write)
+    V acc[kIPT];
+    int first_head = kIPT;
+    const int prev_last = __shfl_up_sync(0xffffffffu, ri[kIPT - 1], 1);
+#pragma unroll
+    for (int t = 0; t < kIPT; ++t) {
+        const bool head = t == 0 ? (lane == 0 || ri[0] != prev_last) : ri[t] != ri[t - 1];
+        if (head && first_head == kIPT) first_head = t;
+        acc[t] = (head || t == 0) ? p[t] : acc[t - 1] + p[t];
+    }
+    SegPair<V> inc{first_head < kIPT ? 1 : 0, acc[kIPT - 1]};
 #pragma unroll
     for (int o = 1; o < 32; o <<= 1) {
-        SegPair<V> t{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
-        if (lane >= o) inc = seg_op(t, inc);
+        SegPair<V> tt{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
+        if (lane >= o) inc = seg_op(tt, inc);
     }
-    V ex = __shfl_up_sync(0xffffffffu, inc.v, 1);
-    if (lane == 0) ex = V(0);
-    if (first_row >= 0) y[r0 + first_row] = first_val + ex;
-    if (lane == 31) {  // carry-out: the row in progress at the unit end
-        const bool has = r1 < n_rows && nz > 0;
-        crow[tile] = has ? (int32_t)r1 : -1;
-        cval[tile] = has ? inc.v : V(0);
+    V cin = __shfl_up_sync(0xffffffffu, inc.v, 1);
+    if (lane == 0) cin = V(0);
+    const int next_first = __shfl_down_sync(0xffffffffu, ri[0], 1);
+#pragma unroll
+    for (int t = 0; t < kIPT; ++t) {
+        const int pos = jb + t;
+        if (pos >= nz) break;
+        const int rnext = (t + 1 < kIPT) ? ri[t + 1] : next_first;
+        const bool last = pos == nz - 1;
+        const V val_t = t < first_head ? acc[t] + cin : acc[t];
+        if (ri[t] < nr && (last || rnext != ri[t])) y[r0 + ri[t]] = val_t;  // row finishes here
+        if (last) {  // unit carry: the open row's partial (or none)
+            const bool open = ri[t] == nr && r1 < n_rows;
+            crow[tile] = open ? (int32_t)r1 : -1;
+            cval[tile] = open ? val_t : V(0);
+        }
     }
+    if (nz == 0 && lane == 0) crow[tile] = -1;
 }
 
 // K10: merge-path partition without searches.  Row r's end item sits at merge position

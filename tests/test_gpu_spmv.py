@@ -17,7 +17,7 @@ def _edge_matrices():
     def mk(name, R, C, rows, cols):
         return gen.from_coo(name, R, C, torch.tensor(rows, dtype=torch.int64), torch.tensor(cols, dtype=torch.int64), 9)
     ms.append(mk("one_entry", 1000, 1000, [500], [3]))
-    ms.append(mk("single_row", 1, 5000, [0] * 3000, list(range(0, 6000, 2))[:3000]))
+    ms.append(mk("single_row", 1, 6000, [0] * 3000, list(range(0, 6000, 2))[:3000]))
     ms.append(mk("single_col", 3000, 1, list(range(3000)), [0] * 3000))
     ms.append(mk("empty_ends", 5000, 100, [2000, 2000, 2001, 2999], [1, 5, 7, 99]))
     # row lengths straddling tile / chunk / long-row thresholds
@@ -38,6 +38,8 @@ def mats():
     global MATS
     if MATS is None:
         MATS = [gen.config(c, small=True) for c in ("C1", "C2", "C3", "C4", "C5")] + _edge_matrices()
+        for m in MATS:
+            m.to_sparse_csr()  # every fixture must be a canonical, in-range CSR
     return MATS
 
 

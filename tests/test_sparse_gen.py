@@ -47,3 +47,9 @@ def test_skewed_has_dense_rows():
     m = gen.config("C4", small=True)
     ln = (m.row_offsets[1:] - m.row_offsets[:-1])
     assert int(ln.max()) >= 10_000
+
+
+def test_gpu_parity_fixtures_are_canonical():
+    """The GPU parity matrices themselves must be valid CSR (caught an out-of-range fixture)."""
+    import test_gpu_spmv as t
+    assert len(t.mats()) >= 13

@@ -1,0 +1,22 @@
+"""Run every kernel on the small parity matrices (for compute-sanitizer)."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tests"))
+import torch  # noqa: E402
+
+import test_gpu_spmv as t  # noqa: E402
+from paper_2403_17017_b200 import kernels  # noqa: E402
+
+ks = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "0,1,2,3,4,5,6,7").split(",")]
+for m in t.mats():
+    for dt in (torch.float32, torch.float64):
+        A = m.to_device_csr(dt, index="int32")
+        x = torch.rand(A.n_cols, device="cuda", dtype=dt)
+        for k in ks:
+            print(m.name, dt, kernels.KERNELS[k], flush=True)
+            kernels.spmv(A, x, k)
+            torch.cuda.synchronize()
+print("all ok")
