@@ -354,13 +354,25 @@ def run_ours(a):
         dist.destroy_process_group()
 
 
+DEVICE_KERNEL = {"Adaptive-CSR": "k_adaptive", "CSR,BM": "k_csr_bm", "CSR,MP": "k_csr_merge",
+                 "CSR,WM": "k_csr_wm", "CSR,WO": "k_csr_merge", "CSR,TM": "k_csr_tm", "COO,WM": "k_coo_wm",
+                 "ELL,TM": "k_ell_tm"}
+
+
 def _traffic_from_profiles(workload, kernel_label):
+    """DRAM read+write bytes per launch of the dominant kernel from the committed
+    `ncu --set full` capture (profiles/traffic.json, written by tools/ncu_summary.py)."""
     p = os.path.join(ROOT, "profiles", "traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get(workload, {}).get(kernel_label)
+            d = json.load(f).get(workload, {})
     except Exception:
         return None
+    name = DEVICE_KERNEL.get(kernel_label, "")
+    for k, v in d.items():
+        if k.split("<")[0] == name:
+            return v
+    return None
 
 
 def _e2e(a, A, x, dtype, dev, model, k, seer_step, stream):

@@ -497,6 +497,8 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, const int64_t *__restrict__ part,
     int32_t *__restrict__ crow, V *__restrict__ cval) {
     __shared__ int32_t s_rend[kMergeWarps][kWarpTile + 1];
+    // products, padded one slot per 32 so the blocked read (lane l, slot 8l+t) is conflict-free
+    __shared__ V s_prod[kMergeWarps][kWarpTile + kWarpTile / 32];
     __shared__ int64_t s_coord[kMergeWarps + 1];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t tile0 = (int64_t)blockIdx.x * kMergeWarps;
@@ -526,32 +528,41 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     const int64_t j0 = d0 - r0, j1 = d1 - r1;
     const int nr = (int)(r1 - r0);  // rows finished inside this unit
     const int nz = (int)(j1 - j0);
-    // (col, val) of this lane's 8 positions + row ends, all loads issued before use
+    // coalesced (striped) loads of this unit's (col, val) and row ends, all issued before
+    // use; products go through the padded smem slice to the blocked owner lanes
     const int jb = lane * kIPT;
-    int32_t c[kIPT];
-    V v[kIPT];
+    V *prod = s_prod[w];
+    {
+        int32_t c[kIPT];
+        V v[kIPT];
 #pragma unroll
-    for (int t = 0; t < kIPT; ++t) {
-        const bool in = jb + t < nz;
-        c[t] = in ? ld_stream(col + j0 + jb + t) : 0;
-        v[t] = in ? ld_stream(val + j0 + jb + t) : V(0);
-    }
-    int64_t re[kIPT + 1];
+        for (int t = 0; t < kIPT; ++t) {
+            const int k = lane + t * 32;
+            c[t] = k < nz ? ld_stream(col + j0 + k) : 0;
+            v[t] = k < nz ? ld_stream(val + j0 + k) : V(0);
+        }
+        int64_t re[kIPT + 1];
 #pragma unroll
-    for (int i = 0; i <= kIPT; ++i) {
-        const int k = lane + i * 32;
-        re[i] = k < nr ? ldo(off + r0 + 1 + k) : 0;
-    }
-    V p[kIPT];
+        for (int i = 0; i <= kIPT; ++i) {
+            const int k = lane + i * 32;
+            re[i] = k < nr ? ldo(off + r0 + 1 + k) : 0;
+        }
 #pragma unroll
-    for (int t = 0; t < kIPT; ++t) p[t] = v[t] * ld_x(x + c[t]);
+        for (int t = 0; t < kIPT; ++t) {
+            const int k = lane + t * 32;
+            prod[k + (k >> 5)] = v[t] * ld_x(x + c[t]);  // positions >= nz hold v = 0 -> 0
+        }
 #pragma unroll
-    for (int i = 0; i <= kIPT; ++i) {
-        const int k = lane + i * 32;
-        if (k < nr) rend[k] = (int32_t)(re[i] - j0);  // <= nz for finished rows
+        for (int i = 0; i <= kIPT; ++i) {
+            const int k = lane + i * 32;
+            if (k < nr) rend[k] = (int32_t)(re[i] - j0);  // <= nz for finished rows
+        }
     }
     if (lane == 0) rend[nr] = INT32_MAX;  // the open row never ends inside the unit
     __syncwarp();
+    V p[kIPT];
+#pragma unroll
+    for (int t = 0; t < kIPT; ++t) p[t] = prod[jb + t + ((jb + t) >> 5)];
     // rows with no entry inside this unit: written 0 (fix-up adds carries from earlier units)
     for (int i = lane; i < nr; i += 32) {
         const int lo = i > 0 ? rend[i - 1] : 0;
