@@ -38,7 +38,7 @@ def raw(rep):
     h, units = r[0], r[1]
     res = []
     for v in r[2:]:
-        d = {"kernel": v[h.index("Kernel Name")].split("(")[0].replace("void kp::<unnamed>::", "")}
+        d = {"kernel": short(v[h.index("Kernel Name")])}
         for m, lab in METRICS:
             if m in h:
                 d[lab] = f"{v[h.index(m)]} {units[h.index(m)]}".strip()
@@ -57,6 +57,13 @@ def raw(rep):
     return res
 
 
+def short(name: str) -> str:
+    """'void unnamed>::k_csr_merge<float, int, 1>(...)' -> 'k_csr_merge<float, int, 1>'."""
+    base = name.split("(")[0] if "<" not in name.split("(")[0] else name[: name.index(">(") + 1] if ">(" in name else name
+    base = base.replace("void ", "")
+    return base.split("::")[-1] if "::" in base.split("<")[0] else base
+
+
 def _scale(u):
     return {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(u.strip(), 1)
 
@@ -73,8 +80,8 @@ def launches(path):
     agg = collections.OrderedDict()
     total = 0.0
     for v in per.values():
-        n = v["name"].split("(")[0].replace("void kp::<unnamed>::", "").split("<")[0]
-        if not ("kp::" in v["name"] or n.startswith("k_")):
+        n = short(v["name"]).split("<")[0]
+        if not n.startswith("k_"):
             continue
         t = float(v.get("gpu__time_duration.sum", "0").replace(",", ""))
         agg.setdefault(n, []).append(t)
