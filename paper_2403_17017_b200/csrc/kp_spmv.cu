@@ -762,24 +762,38 @@ __device__ __forceinline__ int64_t upper_bound_off(const O *off, int64_t n_rows,
     return lo;
 }
 
+// Pass 1: c0[b] = row containing element b*2048, scattered by the rows themselves (a
+// non-empty row r covers the block starts in [off[r], off[r+1])): one coalesced pass over
+// the offsets, each block start written exactly once, no searches.
+template <typename O>
+__global__ void __launch_bounds__(256) k_prep_coo_starts(const O *__restrict__ off, int64_t n_rows,
+                                                         int32_t *__restrict__ c0) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n_rows) return;
+    const int64_t a = ldo(off + r), e = ldo(off + r + 1);
+    for (int64_t b = (a + kCooPrepItems - 1) / kCooPrepItems; b * kCooPrepItems < e; ++b) c0[b] = (int32_t)r;
+}
+
+// Pass 2: the rows starting inside block b are (c0[b], c0[b+1]] (non-empty ones; empty
+// rows in between share offsets and lose the atomicMax to the non-empty row).
 template <typename O>
 __global__ void __launch_bounds__(256) k_prep_coo(const O *__restrict__ off, int64_t n_rows, int64_t nnz,
-                                                  int32_t *__restrict__ rid) {
+                                                  const int32_t *__restrict__ c0s, int32_t *__restrict__ rid) {
     __shared__ int32_t s_mark[kCooPrepItems];
-    __shared__ int64_t s_r[3];
     __shared__ int32_t s_wmax[8];
     const int64_t j0 = (int64_t)blockIdx.x * kCooPrepItems;
     const int64_t j1 = j0 + kCooPrepItems < nnz ? j0 + kCooPrepItems : nnz;
+    const int64_t nb = (nnz + kCooPrepItems - 1) / kCooPrepItems;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    if (lane == 0 && w < 3) {
-        const int64_t v = w == 0 ? j0 : (w == 1 ? j0 : j1 - 1);
-        s_r[w] = upper_bound_off(off, n_rows, v);  // rows with off[r] <= v: [0, result)
-    }
     for (int k = tid; k < kCooPrepItems; k += 256) s_mark[k] = -1;
+    const int64_t c0 = c0s[blockIdx.x];  // row containing j0
+    const int64_t ra = c0 + 1;
+    const int64_t rb = blockIdx.x + 1 < nb ? (int64_t)c0s[blockIdx.x + 1] + 1 : n_rows;
     __syncthreads();
-    const int64_t c0 = s_r[0] - 1;  // row containing j0
-    const int64_t ra = s_r[1], rb = s_r[2];  // rows starting in (j0, j1)
-    for (int64_t r = ra + tid; r < rb; r += 256) atomicMax(&s_mark[(int)(ldo(off + r) - j0)], (int32_t)r);
+    for (int64_t r = ra + tid; r < rb; r += 256) {
+        const int64_t o = ldo(off + r);
+        if (o < j1) atomicMax(&s_mark[(int)(o - j0)], (int32_t)r);
+    }
     __syncthreads();
     // blocked max-scan: thread t owns positions 8t .. 8t+7
     int32_t v[kIPT];
@@ -1098,7 +1112,10 @@ Layout prep_layout(int32_t kernel, const kp_csr *A, int64_t cap) {
             L.b = o; o += align_up((size_t)cap * rpad * val_bytes(A));
             break;
         }
-        case KP_COO_WM: L.a = o; o += align_up((size_t)A->nnz * sizeof(int32_t) + 64); break;
+        case KP_COO_WM:
+            L.a = o; o += align_up((size_t)A->nnz * sizeof(int32_t) + 64);
+            L.b = o; o += align_up((size_t)((A->nnz + kCooPrepItems - 1) / kCooPrepItems + 1) * sizeof(int32_t));
+            break;
         case KP_CSR_MP: L.a = o; o += align_up((size_t)(merge_tiles(A) + 1) * sizeof(int64_t)); break;
         case KP_ADAPTIVE_CSR: {
             const int64_t U = ad_units_max(A);
@@ -1151,7 +1168,11 @@ int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, 
         case KP_COO_WM: {
             const int64_t g = (A->nnz + kCooPrepItems - 1) / kCooPrepItems;
             if (g > 0) {
-                k_prep_coo<O><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, reinterpret_cast<int32_t *>(buf + L.a));
+                int32_t *c0 = reinterpret_cast<int32_t *>(buf + L.b);
+                k_prep_coo_starts<O><<<(unsigned)((A->n_rows + 255) / 256), 256, 0, s>>>(off, A->n_rows, c0);
+                KP_LAUNCHED();
+                k_prep_coo<O><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, c0,
+                                                          reinterpret_cast<int32_t *>(buf + L.a));
                 KP_LAUNCHED();
             }
             P->n_units = coo_chunks(A);
