@@ -267,6 +267,10 @@ __global__ void __launch_bounds__(kRedThreads) k_row_stats(K1Args a) {
             }
             return;
         }
+        // gathered path: prefetch the gathered tree now (overlaps the offsets stream), so
+        // the last CTA evaluates it without two more round trips at the tail
+        __syncthreads();
+        load_tree(tree, a.gath);
     }
 
     int64_t lo = INT64_MAX, hi = INT64_MIN;
@@ -293,11 +297,6 @@ __global__ void __launch_bounds__(kRedThreads) k_row_stats(K1Args a) {
     }
     __syncthreads();
     block_reduce(lo, hi, s2);
-    if (a.mode == kModeSeer) {
-        __syncthreads();
-        load_tree(tree, a.gath);
-        __syncthreads();
-    }
     if (threadIdx.x == 0) {
         a.ws->ticket = 0;  // reusable without memset
         const int64_t n = a.n_rows;

@@ -499,6 +499,8 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     __shared__ int32_t s_rend[kMergeWarps][kWarpTile + 1];
     // products, padded one slot per 32 so the blocked read (lane l, slot 8l+t) is conflict-free
     __shared__ V s_prod[kMergeWarps][kWarpTile + kWarpTile / 32];
+    // per-position count of row ends (padded like s_prod): prefix sums give row indices
+    __shared__ int32_t s_cnt[kMergeWarps][kWarpTile + kWarpTile / 32];
     __shared__ int64_t s_coord[kMergeWarps + 1];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t tile0 = (int64_t)blockIdx.x * kMergeWarps;
@@ -532,6 +534,10 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     // use; products go through the padded smem slice to the blocked owner lanes
     const int jb = lane * kIPT;
     V *prod = s_prod[w];
+    int32_t *cnt = s_cnt[w];
+#pragma unroll
+    for (int t = 0; t < kIPT; ++t) cnt[jb + t + ((jb + t) >> 5)] = 0;
+    __syncwarp();
     {
         int32_t c[kIPT];
         V v[kIPT];
@@ -555,7 +561,11 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
 #pragma unroll
         for (int i = 0; i <= kIPT; ++i) {
             const int k = lane + i * 32;
-            if (k < nr) rend[k] = (int32_t)(re[i] - j0);  // <= nz for finished rows
+            if (k < nr) {
+                const int32_t rk = (int32_t)(re[i] - j0);  // in [0, nz] for finished rows
+                rend[k] = rk;
+                if (rk < nz) atomicAdd(&cnt[rk + (rk >> 5)], 1);  // rows after k start at rk
+            }
         }
     }
     if (lane == 0) rend[nr] = INT32_MAX;  // the open row never ends inside the unit
@@ -568,21 +578,25 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
         const int lo = i > 0 ? rend[i - 1] : 0;
         if (rend[i] <= (lo > 0 ? lo : 0)) y[r0 + i] = V(0);
     }
-    // row index of each owned position
+    // row index of each owned position: ri(p) = #{finished rows ending at or before p}
+    // = inclusive prefix of cnt (blocked per lane + warp exclusive scan of lane totals)
     int ri[kIPT];
     {
-        int lo = 0, hi = nr;  // first i with rend[i] > jb  (rend[nr] = +inf)
-        while (lo < hi) {
-            const int mid = (lo + hi) >> 1;
-            if (rend[mid] <= jb) lo = mid + 1;
-            else hi = mid;
-        }
-        int i = lo;
+        int run = 0;
 #pragma unroll
         for (int t = 0; t < kIPT; ++t) {
-            while (rend[i] <= jb + t) ++i;
-            ri[t] = i;
+            run += cnt[jb + t + ((jb + t) >> 5)];
+            ri[t] = run;
         }
+        int incl = run;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int q = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += q;
+        }
+        const int excl = incl - run;
+#pragma unroll
+        for (int t = 0; t < kIPT; ++t) ri[t] += excl;
     }
     // thread-local segmented scan (positions beyond nz carry p = 0 and never write)
     V acc[kIPT];
