@@ -190,6 +190,11 @@ KP_API int kp_shard_partition(const void *d_off, int32_t off_type, int64_t n_row
 KP_API const char *kp_version(void);
 /* Number of kernel launches issued by this library since load (instrumentation). */
 KP_API uint64_t kp_launch_count(void);
+/* Test hook: number of resident warps the persistent work distribution (CSR,MP / CSR,WO /
+ * COO,WM) targets; 0 = one full wave from the occupancy API (default).  Small values force
+ * many units per warp on small matrices.  Affects kp_prepare and kp_spmv alike; returns
+ * the previous value. */
+KP_API int64_t kp_debug_set_wave_warps(int64_t warps);
 
 #ifdef __cplusplus
 }

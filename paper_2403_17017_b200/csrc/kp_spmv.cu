@@ -480,176 +480,198 @@ __device__ __forceinline__ int64_t merge_search_warp(const O *off, int64_t n_row
     return lo + __popc(__ballot_sync(0xffffffffu, gr));
 }
 
-constexpr int kWarpTile = 32 * kIPT;  // 256 merge items per warp unit
+constexpr int kWarpTile = 32 * kIPT;  // 256 merge items per unit
 constexpr int kMergeWarps = 8;        // warps per CTA
 
-// kPrep: unit coordinates from the K10 partition (CSR,MP); else searched in-kernel (CSR,WO).
-// Unit = merge items [d0, d1): rows r0..r1 (r1 in progress), nnz [j0, j1).  Lane l owns
-// the nnz positions 8l..8l+7 of the unit: (col, val) loads and x gathers straight into
-// registers; the row of each position comes from the unit's row ends staged in shared
-// memory (int32, relative to j0): one binary search for the lane's first position, then
-// a walk.  Thread-local + warp segmented scans (shuffles) give each finished row its sum;
-// rows with no entry inside the unit are written 0 (their carries, if any, arrive in the
-// fix-up); the trailing open row is the unit's carry.
+// Persistent merge-path warps (Merrill & Garland, restructured for B200).  The merge of
+// A = row ends off[1..R] with B = nnz indices 0..Z-1 (row r's end item sits at merge
+// position q_r = off[r+1] + r) is cut into units of 256 items; warp `wid` owns the
+// contiguous RANGE of units [wid*upw, (wid+1)*upw), sized on the host so that one wave of
+// warps covers the matrix (upw = units per warp).  The warp finds its first coordinate
+// once (CSR,MP: from the K10 partition; CSR,WO: 32-ary warp search in-kernel) and then
+// walks its units: each unit's row count comes from a ballot over the next row ends
+// (q_r < d1), so no per-unit search or partition entry exists, and the open row's
+// partial is carried to the next unit in a register.  Only the carry left open at a
+// range end goes through k_carry_fixup (~one per warp instead of one per unit).
+// Per unit: striped (coalesced) col/val loads of up to 256 nnz from j0 (speculative past
+// the unit's nnz end; read-once, L1 no-allocate), x gathers, products staged in the
+// warp's padded smem slice and read back blocked (lane l -> positions 8l..8l+7); each
+// row end marks its relative end position (atomicMax of tag<<9 | k+1, the tag = unit
+// counter makes stale marks of earlier units lose, so nothing is cleared), a max-scan
+// gives every position its row, and a thread-local + warp segmented scan sums rows.
 template <typename V, typename O, bool kPrep>
 __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     const O *__restrict__ off, const int32_t *__restrict__ col, const V *__restrict__ val, const V *__restrict__ x,
-    V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, const int64_t *__restrict__ part,
-    int32_t *__restrict__ crow, V *__restrict__ cval) {
-    __shared__ int32_t s_rend[kMergeWarps][kWarpTile + 1];
-    // products, padded one slot per 32 so the blocked read (lane l, slot 8l+t) is conflict-free
-    __shared__ V s_prod[kMergeWarps][kWarpTile + kWarpTile / 32];
-    // per-position count of row ends (padded like s_prod): prefix sums give row indices
-    __shared__ int32_t s_cnt[kMergeWarps][kWarpTile + kWarpTile / 32];
-    __shared__ int64_t s_coord[kMergeWarps + 1];
+    V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, int64_t upw, int64_t n_ranges,
+    const int64_t *__restrict__ part, int32_t *__restrict__ crow, V *__restrict__ cval) {
+    constexpr int kPad = kWarpTile + kWarpTile / 32;
+    __shared__ V s_prod[kMergeWarps][kPad];
+    __shared__ int32_t s_mark[kMergeWarps][kPad];
+    __shared__ V s_rowv[kMergeWarps][kWarpTile + 1];  // value of each row ending in the unit (+ the open one)
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t tile0 = (int64_t)blockIdx.x * kMergeWarps;
+    const int64_t wid = (int64_t)blockIdx.x * kMergeWarps + w;
+    if (wid >= n_ranges) return;
     const int64_t total = n_rows + nnz;
-    if (kPrep) {
-        if (threadIdx.x <= kMergeWarps) {
-            const int64_t t = tile0 + threadIdx.x;
-            s_coord[threadIdx.x] = part[t < n_units ? t : n_units];
-        }
-    } else {
-        int64_t d = (tile0 + w) * kWarpTile;
-        int64_t i = merge_search_warp(off, n_rows, nnz, d < total ? d : total);
-        if (lane == 0) s_coord[w] = i;
-        if (w == 0) {
-            d = (tile0 + kMergeWarps) * kWarpTile;
-            i = merge_search_warp(off, n_rows, nnz, d < total ? d : total);
-            if (lane == 0) s_coord[kMergeWarps] = i;
-        }
-    }
-    __syncthreads();
-    const int64_t tile = tile0 + w;
-    if (tile >= n_units) return;
-    int32_t *rend = s_rend[w];
-    const int64_t d0 = tile * kWarpTile;
-    const int64_t d1 = d0 + kWarpTile < total ? d0 + kWarpTile : total;
-    const int64_t r0 = s_coord[w], r1 = s_coord[w + 1];
-    const int64_t j0 = d0 - r0, j1 = d1 - r1;
-    const int nr = (int)(r1 - r0);  // rows finished inside this unit
-    const int nz = (int)(j1 - j0);
-    // coalesced (striped) loads of this unit's (col, val) and row ends, all issued before
-    // use; products go through the padded smem slice to the blocked owner lanes
-    const int jb = lane * kIPT;
+    const int64_t u_begin = wid * upw;
+    const int64_t u_end = u_begin + upw < n_units ? u_begin + upw : n_units;
     V *prod = s_prod[w];
-    int32_t *cnt = s_cnt[w];
+    int32_t *mark = s_mark[w];
+    V *rowv = s_rowv[w];
+    for (int t = lane; t < kPad; t += 32) mark[t] = 0;
+    int64_t r0;
+    if (kPrep) r0 = part[wid];
+    else r0 = merge_search_warp(off, n_rows, nnz, u_begin * kWarpTile);
+    int64_t row_start = ldo(off + r0);  // r0 < n_rows: the range starts before the last item
+    V carry = V(0);
+    const int jb = lane * kIPT;
+    int32_t tag = 0;
+    for (int64_t u = u_begin; u < u_end; ++u) {
+        tag += 1 << 9;
+        const int64_t d0 = u * kWarpTile;
+        const int64_t d1 = d0 + kWarpTile < total ? d0 + kWarpTile : total;
+        const int64_t j0 = d0 - r0;
+        // round 0 of the row-end probe + speculative nnz loads, all issued before use
+        int64_t rr = r0 + lane;
+        int64_t re = rr < n_rows ? ldo(off + rr + 1) : INT64_MAX / 2;
+        V p[kIPT];
+        {
+            int32_t c[kIPT];
+            V v[kIPT];
+            if (j0 + kWarpTile <= nnz) {  // common case: unpredicated, immediate offsets
+                const int32_t *cp = col + j0 + lane;
+                const V *vp = val + j0 + lane;
 #pragma unroll
-    for (int t = 0; t < kIPT; ++t) cnt[jb + t + ((jb + t) >> 5)] = 0;
-    __syncwarp();
-    {
-        int32_t c[kIPT];
-        V v[kIPT];
+                for (int t = 0; t < kIPT; ++t) {
+                    c[t] = ld_stream(cp + t * 32);
+                    v[t] = ld_stream(vp + t * 32);
+                }
+            } else {
+#pragma unroll
+                for (int t = 0; t < kIPT; ++t) {
+                    const int64_t j = j0 + lane + t * 32;
+                    c[t] = j < nnz ? ld_stream(col + j) : 0;
+                    v[t] = j < nnz ? ld_stream(val + j) : V(0);
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < kIPT; ++t) p[t] = v[t] * ld_x(x + c[t]);
+        }
+        // row ends inside the unit: q = re + rr < d1 (monotone in rr -> ballot + popc)
+        int nr = 0;
+        int64_t prev_re = row_start;  // end of the row before the probed one (off[rr])
+        for (int round = 0;; ++round) {
+            const bool in = rr < n_rows && re + rr < d1;
+            const unsigned m = __ballot_sync(0xffffffffu, in);
+            const int cnt = __popc(m);
+            int64_t pre = __shfl_up_sync(0xffffffffu, re, 1);
+            if (lane == 0) pre = prev_re;
+            if (in) {
+                const int k = nr + lane;  // row r0 + k; rows with elements here are overwritten by the scan
+                rowv[k] = k == 0 ? carry : V(0);
+                const int rk = (int)(re - j0);  // relative end, < 256
+                atomicMax(&mark[rk + (rk >> 5)], tag | (k + 1));
+            }
+            if (cnt > 0) prev_re = __shfl_sync(0xffffffffu, re, cnt - 1);
+            nr += cnt;
+            if (cnt < 32) break;
+            rr += 32;
+            re = rr < n_rows ? ldo(off + rr + 1) : INT64_MAX / 2;
+        }
+        const int nz = (int)((d1 - d0) - nr);
+        if (lane == 0) rowv[nr] = V(0);  // open row: partial stays 0 unless it has elements here
+        // stage products (positions >= nz belong to the next unit: zero)
 #pragma unroll
         for (int t = 0; t < kIPT; ++t) {
             const int k = lane + t * 32;
-            c[t] = k < nz ? ld_stream(col + j0 + k) : 0;
-            v[t] = k < nz ? ld_stream(val + j0 + k) : V(0);
+            prod[k + (k >> 5)] = k < nz ? p[t] : V(0);
         }
-        int64_t re[kIPT + 1];
+        __syncwarp();
+        // blocked read-back: products and row index of every owned position
+        int ri[kIPT];
+        {
+            // max-scan of the RAW marks: current marks (tag | k+1) beat every stale one
+            // (smaller tag), so ri = max(raw - tag, 0) without decoding each mark
+            int run = 0;
 #pragma unroll
-        for (int i = 0; i <= kIPT; ++i) {
-            const int k = lane + i * 32;
-            re[i] = k < nr ? ldo(off + r0 + 1 + k) : 0;
+            for (int t = 0; t < kIPT; ++t) {
+                const int q = jb + t + ((jb + t) >> 5);
+                p[t] = prod[q];
+                run = max(run, mark[q]);
+                ri[t] = run;
+            }
+            int incl = run;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const int q = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl = max(incl, q);
+            }
+            int excl = __shfl_up_sync(0xffffffffu, incl, 1);
+            if (lane == 0) excl = 0;
+#pragma unroll
+            for (int t = 0; t < kIPT; ++t) ri[t] = max(max(ri[t], excl) - tag, 0);
         }
+        // thread-local segmented scan
+        V acc[kIPT];
+        int first_head = kIPT;
+        const int prev_last = __shfl_up_sync(0xffffffffu, ri[kIPT - 1], 1);
 #pragma unroll
         for (int t = 0; t < kIPT; ++t) {
-            const int k = lane + t * 32;
-            prod[k + (k >> 5)] = v[t] * ld_x(x + c[t]);  // positions >= nz hold v = 0 -> 0
+            const bool head = t == 0 ? (lane == 0 || ri[0] != prev_last) : ri[t] != ri[t - 1];
+            if (head && first_head == kIPT) first_head = t;
+            acc[t] = (head || t == 0) ? p[t] : acc[t - 1] + p[t];
         }
+        // warp segmented scan of the lanes' last-segment sums; the head flags travel as
+        // one ballot mask (lane l combines lane l-o unless a head lies in (l-o, l])
+        V inc = acc[kIPT - 1];
+        {
+            const unsigned heads = __ballot_sync(0xffffffffu, first_head < kIPT);
 #pragma unroll
-        for (int i = 0; i <= kIPT; ++i) {
-            const int k = lane + i * 32;
-            if (k < nr) {
-                const int32_t rk = (int32_t)(re[i] - j0);  // in [0, nz] for finished rows
-                rend[k] = rk;
-                if (rk < nz) atomicAdd(&cnt[rk + (rk >> 5)], 1);  // rows after k start at rk
+            for (int o = 1; o < 32; o <<= 1) {
+                const V up = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o && ((heads >> (lane - o + 1)) & ((1u << o) - 1u)) == 0) inc = up + inc;
             }
         }
-    }
-    if (lane == 0) rend[nr] = INT32_MAX;  // the open row never ends inside the unit
-    __syncwarp();
-    V p[kIPT];
-#pragma unroll
-    for (int t = 0; t < kIPT; ++t) p[t] = prod[jb + t + ((jb + t) >> 5)];
-    // rows with no entry inside this unit: written 0 (fix-up adds carries from earlier units)
-    for (int i = lane; i < nr; i += 32) {
-        const int lo = i > 0 ? rend[i - 1] : 0;
-        if (rend[i] <= (lo > 0 ? lo : 0)) y[r0 + i] = V(0);
-    }
-    // row index of each owned position: ri(p) = #{finished rows ending at or before p}
-    // = inclusive prefix of cnt (blocked per lane + warp exclusive scan of lane totals)
-    int ri[kIPT];
-    {
-        int run = 0;
+        V cin = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0) cin = V(0);
+        const int next_first = __shfl_down_sync(0xffffffffu, ri[0], 1);
 #pragma unroll
         for (int t = 0; t < kIPT; ++t) {
-            run += cnt[jb + t + ((jb + t) >> 5)];
-            ri[t] = run;
+            const int pos = jb + t;
+            const int rnext = (t + 1 < kIPT) ? ri[t + 1] : next_first;
+            if (pos < nz && (pos == nz - 1 || rnext != ri[t])) {  // last element of its row in the unit
+                V vt = t < first_head ? acc[t] + cin : acc[t];
+                if (ri[t] == 0) vt += carry;  // the row continued from earlier units
+                rowv[ri[t]] = vt;
+            }
         }
-        int incl = run;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int q = __shfl_up_sync(0xffffffffu, incl, o);
-            if (lane >= o) incl += q;
-        }
-        const int excl = incl - run;
-#pragma unroll
-        for (int t = 0; t < kIPT; ++t) ri[t] += excl;
+        __syncwarp();
+        // finished rows r0 .. r0+nr-1: coalesced stores; the open row's partial is the carry
+        for (int k = lane; k < nr; k += 32) y[r0 + k] = rowv[k];
+        carry = rowv[nr];
+        r0 += nr;
+        row_start = prev_re;
+        __syncwarp();
     }
-    // thread-local segmented scan (positions beyond nz carry p = 0 and never write)
-    V acc[kIPT];
-    int first_head = kIPT;
-    const int prev_last = __shfl_up_sync(0xffffffffu, ri[kIPT - 1], 1);
-#pragma unroll
-    for (int t = 0; t < kIPT; ++t) {
-        const bool head = t == 0 ? (lane == 0 || ri[0] != prev_last) : ri[t] != ri[t - 1];
-        if (head && first_head == kIPT) first_head = t;
-        acc[t] = (head || t == 0) ? p[t] : acc[t - 1] + p[t];
+    if (lane == 0) {
+        const bool open = r0 < n_rows;
+        crow[wid] = open ? (int32_t)r0 : -1;
+        cval[wid] = open ? carry : V(0);
     }
-    SegPair<V> inc{first_head < kIPT ? 1 : 0, acc[kIPT - 1]};
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        SegPair<V> tt{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
-        if (lane >= o) inc = seg_op(tt, inc);
-    }
-    V cin = __shfl_up_sync(0xffffffffu, inc.v, 1);
-    if (lane == 0) cin = V(0);
-    const int next_first = __shfl_down_sync(0xffffffffu, ri[0], 1);
-#pragma unroll
-    for (int t = 0; t < kIPT; ++t) {
-        const int pos = jb + t;
-        if (pos >= nz) break;
-        const int rnext = (t + 1 < kIPT) ? ri[t + 1] : next_first;
-        const bool last = pos == nz - 1;
-        const V val_t = t < first_head ? acc[t] + cin : acc[t];
-        if (ri[t] < nr && (last || rnext != ri[t])) y[r0 + ri[t]] = val_t;  // row finishes here
-        if (last) {  // unit carry: the open row's partial (or none)
-            const bool open = ri[t] == nr && r1 < n_rows;
-            crow[tile] = open ? (int32_t)r1 : -1;
-            cval[tile] = open ? val_t : V(0);
-        }
-    }
-    if (nz == 0 && lane == 0) crow[tile] = -1;
 }
 
-// K10: merge-path partition without searches.  Row r's end item sits at merge position
-// q_r = off[r+1] + r (strictly increasing), and the coordinate of diagonal d is
-// #{r : q_r < d}; so every unit boundary p*256 in (q_{r-1}, q_r] has coordinate r.  One
-// thread per row scatters r to those boundaries: a single coalesced pass over the
-// offsets, each boundary written exactly once (the last one, d = R + Z, gets R).
+// K10: merge-path partition = the first coordinate of every warp range (one warp per
+// range, 32-ary search over the row ends; O(#ranges) ~ one wave of warps, independent
+// of the matrix size).  part[n_ranges] = n_rows.
 template <typename O>
 __global__ void __launch_bounds__(256) k_prep_mp(const O *__restrict__ off, int64_t n_rows, int64_t nnz,
-                                                 int64_t n_tiles, int64_t *__restrict__ part) {
-    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (r == 0) part[n_tiles] = n_rows;
-    if (r >= n_rows) return;
-    const int64_t qa = r == 0 ? -1 : ldo(off + r) + r - 1;
-    const int64_t qb = ldo(off + r + 1) + r;
-    const int64_t p_lo = qa < 0 ? 0 : qa / kWarpTile + 1;
-    const int64_t p_hi = qb / kWarpTile;
-    for (int64_t p = p_lo; p <= p_hi; ++p) part[p] = r;
+                                                 int64_t upw, int64_t n_ranges, int64_t *__restrict__ part) {
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid > n_ranges) return;
+    const int64_t total = n_rows + nnz;
+    int64_t d = wid * upw * kWarpTile;
+    if (d > total) d = total;
+    const int64_t r = merge_search_warp(off, n_rows, nnz, d);
+    if ((threadIdx.x & 31) == 0) part[wid] = wid == n_ranges ? n_rows : r;
 }
 
 // ================================================================= COO,WM (K8 + K11)
@@ -1092,6 +1114,39 @@ int tm_rows_per_thread(const kp_csr *A, int cap) {
 }
 
 int64_t merge_tiles(const kp_csr *A) { return (A->n_rows + A->nnz + kWarpTile - 1) / kWarpTile; }
+// Persistent merge geometry: units of 256 merge items, `upw` consecutive units per warp so
+// that one wave of resident warps (occupancy API, cached per instantiation) covers the
+// matrix.  Used identically by the K10 partition and the SpMV launch.
+struct MergeGeom {
+    int64_t n_units, upw, n_ranges;
+};
+template <typename V, typename O>
+int merge_warps_per_sm() {
+    static int warps_per_sm = 0;
+    if (!warps_per_sm) {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_csr_merge<V, O, true>, kMergeWarps * 32, 0) !=
+                cudaSuccess ||
+            nb <= 0) {
+            cudaGetLastError();
+            nb = 4;
+        }
+        warps_per_sm = nb * kMergeWarps;
+    }
+    return warps_per_sm;
+}
+int64_t g_wave_warps = 0;  // kp_debug_set_wave_warps (0 = occupancy-derived)
+template <typename V, typename O>
+MergeGeom merge_geom(const kp_csr *A) {
+    const int warps_per_sm = merge_warps_per_sm<V, O>();
+    MergeGeom G;
+    G.n_units = merge_tiles(A);
+    const int64_t target = g_wave_warps > 0 ? g_wave_warps : (int64_t)num_sms() * warps_per_sm;
+    G.upw = (G.n_units + target - 1) / target;
+    if (G.upw < 1) G.upw = 1;
+    G.n_ranges = (G.n_units + G.upw - 1) / G.upw;
+    return G;
+}
 int64_t coo_chunks(const kp_csr *A) { return (A->nnz + kCooChunk - 1) / kCooChunk; }
 int64_t ad_units_max(const kp_csr *A) {
     return A->n_rows + A->nnz / kAdLongChunk + 2;
@@ -1193,11 +1248,12 @@ int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, 
             break;
         }
         case KP_CSR_MP: {
-            const int64_t nt = merge_tiles(A);
-            const int64_t g = (A->n_rows + 255) / 256 > 0 ? (A->n_rows + 255) / 256 : 1;
-            k_prep_mp<O><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, nt, reinterpret_cast<int64_t *>(buf + L.a));
+            const MergeGeom G = merge_geom<V, O>(A);
+            const int64_t g = ((G.n_ranges + 1) * 32 + 255) / 256;
+            k_prep_mp<O><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, G.upw, G.n_ranges,
+                                                      reinterpret_cast<int64_t *>(buf + L.a));
             KP_LAUNCHED();
-            P->n_units = nt;
+            P->n_units = G.n_ranges;
             break;
         }
         case KP_ADAPTIVE_CSR: {
@@ -1309,18 +1365,20 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
         }
         case KP_CSR_MP:
         case KP_CSR_WO: {
-            const int64_t nt = merge_tiles(A);
-            const unsigned g = (unsigned)((nt + kMergeWarps - 1) / kMergeWarps);
+            const MergeGeom G = merge_geom<V, O>(A);
+            const unsigned g = (unsigned)((G.n_ranges + kMergeWarps - 1) / kMergeWarps);
             if (kernel == KP_CSR_MP) {
                 if (!P || !P->buf) return KP_EINVAL;
                 const Layout L = prep_layout(KP_CSR_MP, A, 0);
                 k_csr_merge<V, O, true><<<g, kMergeWarps * 32, 0, s>>>(
-                    off, col, val, x, y, R, Z, nt, reinterpret_cast<const int64_t *>((unsigned char *)P->buf + L.a), crow, cval);
+                    off, col, val, x, y, R, Z, G.n_units, G.upw, G.n_ranges,
+                    reinterpret_cast<const int64_t *>((unsigned char *)P->buf + L.a), crow, cval);
             } else {
-                k_csr_merge<V, O, false><<<g, kMergeWarps * 32, 0, s>>>(off, col, val, x, y, R, Z, nt, nullptr, crow, cval);
+                k_csr_merge<V, O, false><<<g, kMergeWarps * 32, 0, s>>>(off, col, val, x, y, R, Z, G.n_units, G.upw,
+                                                                         G.n_ranges, nullptr, crow, cval);
             }
             KP_LAUNCHED();
-            k_carry_fixup<V><<<(unsigned)((nt * 32 + 255) / 256), 256, 0, s>>>(crow, cval, nullptr, nt, y);
+            k_carry_fixup<V><<<(unsigned)((G.n_ranges * 32 + 255) / 256), 256, 0, s>>>(crow, cval, nullptr, G.n_ranges, y);
             KP_LAUNCHED();
             return KP_OK;
         }
@@ -1358,6 +1416,11 @@ int kp::ensure_kernel_attrs() {
     if (!rc) rc = tm_attrs<float, int64_t>();
     if (!rc) rc = tm_attrs<double, int32_t>();
     if (!rc) rc = tm_attrs<double, int64_t>();
+    // occupancy queries cached outside any graph capture
+    merge_warps_per_sm<float, int32_t>();
+    merge_warps_per_sm<float, int64_t>();
+    merge_warps_per_sm<double, int32_t>();
+    merge_warps_per_sm<double, int64_t>();
     return rc;
 }
 
@@ -1426,6 +1489,12 @@ int kp_spmv(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d
     }
     return A->off_type == KP_I32 ? spmv_t<double, int32_t>(kernel, A, P, (const double *)d_x, (double *)d_y, ws, s)
                                  : spmv_t<double, int64_t>(kernel, A, P, (const double *)d_x, (double *)d_y, ws, s);
+}
+
+int64_t kp_debug_set_wave_warps(int64_t warps) {
+    const int64_t prev = g_wave_warps;
+    g_wave_warps = warps > 0 ? warps : 0;
+    return prev;
 }
 
 int kp_shard_partition(const void *d_off, int32_t off_type, int64_t n_rows, int32_t parts, int64_t *d_cuts,

@@ -97,3 +97,28 @@ def test_c2_full_size_every_kernel_agrees(orc):
         y = kernels.spmv(A, x, k)
         ok, r = orc.spmv_check(y.cpu().numpy(), yref, absy, 1e-5)
         assert ok, (kernels.KERNELS[k], r)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("warps", [1, 3, 7, 64])
+def test_persistent_ranges_many_units_per_warp(warps, dtype, orc):
+    """Force few resident warps so each warp walks many consecutive units (register
+    carries across units, rows spanning warp ranges -> fix-up runs) on every fixture."""
+    from paper_2403_17017_b200 import _lib
+    L = _lib.load()
+    prev = L.kp_debug_set_wave_warps(warps)
+    try:
+        for m in mats():
+            A = m.to_device_csr(dtype)
+            key = (m.name, dtype)
+            if key not in XS:
+                g = torch.Generator().manual_seed(3)
+                XS[key] = (torch.rand(m.n_cols, generator=g, dtype=torch.float64) * 2 - 1).to(dtype).cuda()
+            for kern in (kernels.kernel_index("CSR,MP"), kernels.kernel_index("CSR,WO"), kernels.kernel_index("COO,WM")):
+                y = torch.full((A.n_rows,), float("nan"), dtype=dtype, device="cuda")
+                kernels.spmv(A, XS[key], kern, y=y, prepared=kernels.prepare(A, kern, cache=False)
+                             if kern in kernels.NEEDS_PREP else None)
+                torch.cuda.synchronize()
+                _check(m, A, kern, y, orc)
+    finally:
+        L.kp_debug_set_wave_warps(prev)
