@@ -204,30 +204,48 @@ def run_ours(a):
             marks[1].record()
         return P
 
-    def timed(fn, steps, warm):
+    def timed(kk, steps, warm):
+        """Fixed kernel kk: prep + k SpMVs captured as one CUDA graph (launched like the
+        Seer plan), plus an eager pass with events around the SpMVs for the split."""
+        fixed_step(kk)
+        cs = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        gr = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(gr, stream=cs):
+            fixed_step(kk)
         for _ in range(warm):
-            fn(None)
+            gr.replay()
+            fixed_step(kk)
         torch.cuda.synchronize()
         tot, inner = [], []
         for _ in range(steps):
             flush.zero_()
-            e0, e1, m0, m1 = ev(), ev(), ev(), ev()
+            e0, e1 = ev(), ev()
             e0.record()
-            fn((m0, m1))
+            gr.replay()
             e1.record()
             e1.synchronize()
             tot.append(e0.elapsed_time(e1) * 1e-3)
+            flush.zero_()
+            m0, m1 = ev(), ev()
+            fixed_step(kk, (m0, m1))
+            m1.synchronize()
             inner.append(m0.elapsed_time(m1) * 1e-3)
+        del gr
         return tot, inner
 
     # ---------------------------------------------------------------- warmup + timed (value)
     # The step runs as ONE CUDA graph (seer.SeerPlan): select -> device-side SWITCH on the
     # chosen kernel -> its preprocessing -> k SpMVs; no host round trip inside the step.
     plan = seer.SeerPlan(model, A, x, y, k)
-    n0 = L.kp_launch_count()
-    o_eager, _ = seer_step(A, x, y)            # one host-dispatched step: counts our launches
+    o_eager, _ = seer_step(A, x, y)
     torch.cuda.synchronize()
-    launches_per_step = (L.kp_launch_count() - n0) + 1  # + the graph's set-switch kernel
+    # our kernels per graph step: the chosen body (prep + k SpMVs), + the selection kernel
+    # on a gathered-path plan (the known path is resolved at plan build, PAPER.md:141)
+    n0 = L.kp_launch_count()
+    fixed_step(int(o_eager.kernel))
+    torch.cuda.synchronize()
+    launches_per_step = (L.kp_launch_count() - n0) + (1 if o_eager.path else 0)
     for _ in range(a.warmup):
         plan.launch()
     torch.cuda.synchronize()
@@ -301,7 +319,7 @@ def run_ours(a):
         sweep = {}
         seer_mean = total / a.steps if world == 1 else sum(step_t) / a.steps
         for kk in range(len(kernels.KERNELS)):
-            tot, inner = timed(lambda mk, kk=kk: fixed_step(kk, mk), max(3, a.steps // 2), 2)
+            tot, inner = timed(kk, max(3, a.steps // 2), 2)
             t_tot, t_sp = statistics.mean(tot), statistics.mean(inner) / k
             w = None
             if kk == kernels.ELL_TM:
@@ -335,7 +353,9 @@ def run_ours(a):
             "seer": {"kernel": kernels.KERNELS[kern], "path": "gathered" if outcome.path else "known",
                      "features": [outcome.max_d, outcome.min_d, outcome.mean_d, outcome.var_d] if outcome.path else None,
                      "step_us_median": round(statistics.median(step_t) * 1e6, 2),
-                     "dispatch": "one CUDA graph, device-side SWITCH (kp_seer_plan)",
+                     "dispatch": ("one CUDA graph (kp_seer_plan): known path resolved on the device at plan "
+                                  "build (PAPER.md:141 zero overhead), graph = chosen body" if not outcome.path else
+                                  "one CUDA graph (kp_seer_plan): feature pass + gathered tree -> device-side SWITCH"),
                      "host_dispatched_step_us_median": round(statistics.median(eager_t) * 1e6, 2),
                      "spmv_us_mean": round(per_launch * 1e6, 2)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",

@@ -166,8 +166,12 @@ KP_API int kp_spmv(int32_t kernel, const kp_csr *A, const kp_prepared *P, const 
 
 /* ------------------------------------------------------------ Seer plan (one CUDA graph) */
 /* The whole pipeline -- kp_seer_select, then the chosen kernel's kp_prepare and
- * `iterations` kp_spmv -- as one CUDA graph whose conditional SWITCH node is steered on
- * the device by the selected kernel index (no host round trip).  The matrix, x, y, trees,
+ * `iterations` kp_spmv -- as one CUDA graph.  Creation evaluates the selector on the
+ * device for the plan's static (rows, cols, nnz, iterations): on the KNOWN path the known
+ * tree's kernel is fixed there too ("known at no additional runtime cost", PAPER.md:138,
+ * 141) and the graph is that kernel's body alone; on the GATHERED path every launch runs
+ * the feature pass + gathered tree, whose kernel index steers a conditional SWITCH node on
+ * the device (no host round trip).  d_out holds the outcome either way.  The matrix, x, y, trees,
  * outcome and reduction workspace are bound at creation; d_buf (kp_seer_plan_bytes) holds
  * every kernel's prepared format and the SpMV workspace.  `stream` must be a created
  * (non-legacy) stream; creation captures through it. */

@@ -1,7 +1,14 @@
 // kp_graph.cu -- the whole Seer pipeline as ONE CUDA graph with device-side dispatch.
 //
-//   [kp_seer_select] -> [k_set_switch: cudaGraphSetConditional(h, outcome.kernel)]
+// Known-path plans (selector -> USE_KNOWN on the plan's static shape, resolved on the device
+// at creation) are the chosen kernel's body alone.  Gathered-path plans:
+//   [k_seer_plan_select: selector -> feature pass -> tree, cudaGraphSetConditional(h, kernel)]
 //        -> SWITCH(h) { body i = kp_prepare(i) + iterations x kp_spmv(i), i = 0..7 }
+//
+// The three trees are copied to the host once at creation and passed BY VALUE to the
+// selection kernel (parameter space), which also sets the switch value: one launch before
+// the body.  Trees deeper than the parameter table fall back to kp_seer_select (trees in
+// device memory) + a separate set-switch kernel.
 //
 // SPEC.md:376-384 infer followed by the chosen kernel's preprocessing and k iterations
 // (SURVEY 8d T_seer) with no host round trip: the kernel index written by the selection
@@ -18,6 +25,7 @@ struct kp_seer_plan {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
     cudaGraphConditionalHandle handle = 0;
+    int32_t static_kernel = -1;  // >= 0: known-path plan (body only, no SWITCH)
     kp_prepared prep[KP_NUM_KERNELS] = {};
 };
 
@@ -89,6 +97,14 @@ int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap, co
     rc = ensure_kernel_attrs();  // no attribute calls inside the capture
     if (rc) return rc;
     unsigned char *base = reinterpret_cast<unsigned char *>(d_buf);
+    // trees small enough to travel by value (depth <= 6) -> single-kernel selection
+    ParamTrees *trees = new ParamTrees();
+    const bool use_param_trees = plan_trees_load(d_selector, d_known, d_gathered, trees) == KP_OK;
+    cudaGetLastError();
+    struct TreesGuard {
+        ParamTrees *t;
+        ~TreesGuard() { delete t; }
+    } guard{trees};
     kp_seer_plan *P = new kp_seer_plan();
     auto fail = [&](int code) {
         if (P->exec) cudaGraphExecDestroy(P->exec);
@@ -98,6 +114,34 @@ int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap, co
         return code;
     };
     if (cudaGraphCreate(&P->graph, 0) != cudaSuccess) return fail(KP_ECUDA);
+    void *ws = base + L.ws_off;
+    // 0) Known-feature decisions depend only on the plan's static shape (rows, cols, nnz,
+    //    iterations): "known at no additional runtime cost".  Evaluate
+    //    the selector (and, on the known path, the known tree) on the device once, now.
+    //    KNOWN -> the graph is the chosen kernel's body alone; GATHERED -> the feature pass
+    //    runs every launch and steers a SWITCH node on the device.
+    rc = kp_seer_select(A->row_offsets, A->off_type, A->n_rows, A->n_cols, A->nnz, iterations, d_selector, d_known,
+                        d_gathered, d_out, d_red_ws, s);
+    if (rc) return fail(rc);
+    kp_outcome o0;
+    if (cudaMemcpyAsync(&o0, d_out, sizeof(o0), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return fail(KP_ECUDA);
+    if (o0.path == KP_USE_KNOWN && o0.kernel >= 0 && o0.kernel < KP_NUM_KERNELS) {
+        const int k = o0.kernel;
+        if (cudaStreamBeginCaptureToGraph(s, P->graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
+            cudaSuccess)
+            return fail(KP_ECUDA);
+        rc = kp_prepare(k, A, k == KP_ELL_TM ? ell_cap : 0, base + L.prep_off[k], L.prep[k], &P->prep[k], s);
+        for (int64_t it = 0; rc == KP_OK && it < iterations; ++it)
+            rc = kp_spmv(k, A, &P->prep[k], d_x, d_y, ws, L.ws, s);
+        cudaGraph_t got = nullptr;
+        if (cudaStreamEndCapture(s, &got) != cudaSuccess || rc != KP_OK) return fail(rc ? rc : KP_ECUDA);
+        P->static_kernel = k;
+        if (cudaGraphInstantiate(&P->exec, P->graph, 0) != cudaSuccess) return fail(KP_ECUDA);
+        *plan_out = P;
+        return KP_OK;
+    }
     if (cudaGraphConditionalHandleCreate(&P->handle, P->graph, KP_NUM_KERNELS, cudaGraphCondAssignDefault) !=
         cudaSuccess)
         return fail(KP_ECUDA);
@@ -105,11 +149,17 @@ int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap, co
     if (cudaStreamBeginCaptureToGraph(s, P->graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=
         cudaSuccess)
         return fail(KP_ECUDA);
-    rc = kp_seer_select(A->row_offsets, A->off_type, A->n_rows, A->n_cols, A->nnz, iterations, d_selector, d_known,
-                        d_gathered, d_out, d_red_ws, s);
-    if (rc == KP_OK) {
-        k_set_switch<<<1, 1, 0, s>>>(P->handle, d_out);
-        ++g_launches;
+    if (use_param_trees) {
+        // one kernel: selection with the trees in its parameter space, sets the SWITCH value
+        rc = launch_plan_select(A->row_offsets, A->off_type, A->n_rows, A->n_cols, A->nnz, iterations, *trees, d_out,
+                                d_red_ws, P->handle, s);
+    } else {
+        rc = kp_seer_select(A->row_offsets, A->off_type, A->n_rows, A->n_cols, A->nnz, iterations, d_selector,
+                            d_known, d_gathered, d_out, d_red_ws, s);
+        if (rc == KP_OK) {
+            k_set_switch<<<1, 1, 0, s>>>(P->handle, d_out);
+            ++g_launches;
+        }
     }
     cudaGraph_t captured = nullptr;
     if (cudaStreamEndCapture(s, &captured) != cudaSuccess || rc != KP_OK) return fail(rc ? rc : KP_ECUDA);
@@ -134,7 +184,6 @@ int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap, co
     cp.conditional.size = KP_NUM_KERNELS;
     cudaGraphNode_t cnode;
     if (cudaGraphAddNode(&cnode, P->graph, &leaf, 1, &cp) != cudaSuccess) return fail(KP_ECUDA);
-    void *ws = base + L.ws_off;
     for (int k = 0; k < KP_NUM_KERNELS; ++k) {
         cudaGraph_t body = cp.conditional.phGraph_out[k];
         if (cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal) !=

@@ -31,6 +31,19 @@ extern unsigned long long g_launches;  // kp_launch_count()
 
 int num_sms();
 
+// Trees by value for the plan's selection kernel (kp_reduce.cu, used by kp_graph.cu).
+constexpr int kParamTreeNodes = 127;  // depth <= 6
+struct ParamTrees {
+    int32_t n[3];
+    int32_t pad;
+    kp_tree_node node[3][kParamTreeNodes];
+};
+
+int plan_trees_load(const void *d_sel, const void *d_known, const void *d_gath, ParamTrees *T);
+int launch_plan_select(const void *d_off, int32_t off_type, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                       int64_t iters, const ParamTrees &T, kp_outcome *d_out, void *d_ws,
+                       cudaGraphConditionalHandle h, cudaStream_t s);
+
 // ----------------------------------------------------------------- load helpers
 // Streamed (read-once) data: non-coherent path, do not allocate in L1 so the x
 // gathers keep the L1.

@@ -235,11 +235,45 @@ struct K1Args {
     RedWorkspace *ws;
 };
 
+// Grid-wide (min, max, sum of squares) of row lengths; returns true in the LAST CTA to
+// finish (valid in thread 0), which has folded all CTA partials in fixed order and reset
+// the ticket so the workspace is reusable without a memset.
+template <typename O, bool kVec>
+__device__ __forceinline__ bool k1_pass(const K1Args &a, const O *off, int64_t &lo, int64_t &hi, uint64_t &s2) {
+    __shared__ bool s_last;
+    lo = INT64_MAX; hi = INT64_MIN; s2 = 0;
+    stats_accum<O, kVec>(off, a.n_rows, lo, hi, s2);
+    block_reduce(lo, hi, s2);
+    if (threadIdx.x == 0) {
+        a.ws->part[blockIdx.x] = Partial{lo, hi, s2, 0};
+        __threadfence();
+        unsigned t = atomicAdd(&a.ws->ticket, 1u);
+        s_last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (!s_last) return false;
+    __threadfence();
+    lo = INT64_MAX; hi = INT64_MIN; s2 = 0;
+    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
+        const Partial *p = &a.ws->part[i];
+        const int64_t plo = __ldcg(&p->lo), phi = __ldcg(&p->hi);
+        lo = plo < lo ? plo : lo;
+        hi = phi > hi ? phi : hi;
+        s2 += (uint64_t)__ldcg((const unsigned long long *)&p->s2);
+    }
+    __syncthreads();
+    block_reduce(lo, hi, s2);
+    if (threadIdx.x == 0) {
+        a.ws->ticket = 0;
+        if (a.n_rows <= 0) { lo = hi = 0; s2 = 0; }
+    }
+    return true;
+}
+
 template <typename O, bool kVec>
 __global__ void __launch_bounds__(kRedThreads) k_row_stats(K1Args a) {
     __shared__ SmemTree tree;
     __shared__ int s_path;
-    __shared__ bool s_last;
     const O *off = reinterpret_cast<const O *>(a.off);
 
     if (a.mode == kModeSeer) {
@@ -273,34 +307,11 @@ __global__ void __launch_bounds__(kRedThreads) k_row_stats(K1Args a) {
         load_tree(tree, a.gath);
     }
 
-    int64_t lo = INT64_MAX, hi = INT64_MIN;
-    uint64_t s2 = 0;
-    stats_accum<O, kVec>(off, a.n_rows, lo, hi, s2);
-    block_reduce(lo, hi, s2);
+    int64_t lo, hi;
+    uint64_t s2;
+    if (!k1_pass<O, kVec>(a, off, lo, hi, s2)) return;
     if (threadIdx.x == 0) {
-        a.ws->part[blockIdx.x] = Partial{lo, hi, s2, 0};
-        __threadfence();
-        unsigned t = atomicAdd(&a.ws->ticket, 1u);
-        s_last = (t == gridDim.x - 1);
-    }
-    __syncthreads();
-    if (!s_last) return;
-    __threadfence();
-    // Last CTA: fold partials in fixed order.
-    lo = INT64_MAX; hi = INT64_MIN; s2 = 0;
-    for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) {
-        const Partial *p = &a.ws->part[i];
-        const int64_t plo = __ldcg(&p->lo), phi = __ldcg(&p->hi);
-        lo = plo < lo ? plo : lo;
-        hi = phi > hi ? phi : hi;
-        s2 += (uint64_t)__ldcg((const unsigned long long *)&p->s2);
-    }
-    __syncthreads();
-    block_reduce(lo, hi, s2);
-    if (threadIdx.x == 0) {
-        a.ws->ticket = 0;  // reusable without memset
         const int64_t n = a.n_rows;
-        if (n <= 0) { lo = hi = 0; s2 = 0; }
         const int64_t s1 = n > 0 ? (int64_t)((uint64_t)ldo(off + n) - (uint64_t)ldo(off)) : 0;
         if (a.mode == kModeStats) {
             a.out4[0] = lo; a.out4[1] = hi; a.out4[2] = s1; a.out4[3] = (int64_t)s2;
@@ -316,6 +327,61 @@ __global__ void __launch_bounds__(kRedThreads) k_row_stats(K1Args a) {
             }
             *a.out = o;
         }
+    }
+}
+
+// ------------------------------------------------------------------ plan select (K15, graph)
+// The graph flavour of kp_seer_select: the three trees travel BY VALUE in the kernel's
+// parameter space (constant bank: every thread walks the selector with broadcast loads,
+// no global / smem round trip), and the chosen kernel index steers the plan's SWITCH node
+// directly (cudaGraphSetConditional) -- no separate set-switch launch.
+__device__ __forceinline__ double feat(const double *x, int f, int nf) {
+    double v = x[0];
+#pragma unroll
+    for (int i = 1; i < 8; ++i)
+        if (i < nf && f == i) v = x[i];
+    return v;
+}
+template <int NF>
+__device__ __forceinline__ int32_t predict_param(const ParamTrees &T, int t, const double (&x)[NF]) {
+    int32_t i = 0;
+    while (T.node[t][i].feature >= 0)
+        i = (feat(x, T.node[t][i].feature, NF) <= T.node[t][i].threshold) ? T.node[t][i].left : T.node[t][i].right;
+    return T.node[t][i].value;
+}
+
+template <typename O, bool kVec>
+__global__ void __launch_bounds__(kRedThreads) k_seer_plan_select(K1Args a, const __grid_constant__ ParamTrees T,
+                                                                   cudaGraphConditionalHandle h) {
+    const O *off = reinterpret_cast<const O *>(a.off);
+    const double xk[4] = {(double)a.n_rows, (double)a.n_cols, (double)a.nnz, (double)a.iters};
+    if (predict_param(T, 0, xk) == KP_USE_KNOWN) {  // the matrix is never read
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            kp_outcome o = {};
+            o.kernel = predict_param(T, 1, xk);
+            o.path = KP_USE_KNOWN;
+            o.status = KP_OK;
+            *a.out = o;
+            cudaGraphSetConditional(h, (o.kernel >= 0 && o.kernel < KP_NUM_KERNELS) ? (unsigned)o.kernel
+                                                                                   : (unsigned)KP_NUM_KERNELS);
+        }
+        return;
+    }
+    int64_t lo, hi;
+    uint64_t s2;
+    if (!k1_pass<O, kVec>(a, off, lo, hi, s2)) return;
+    if (threadIdx.x == 0) {
+        const int64_t n = a.n_rows;
+        const int64_t s1 = (int64_t)((uint64_t)ldo(off + n) - (uint64_t)ldo(off));
+        kp_outcome o = {};
+        epilogue(lo, hi, s1, (int64_t)s2, n, a.n_cols, &o);
+        o.path = KP_USE_GATHERED;
+        const double xg[8] = {(double)a.n_rows, (double)a.n_cols, (double)a.nnz, (double)a.iters,
+                              o.max_d, o.min_d, o.mean_d, o.var_d};
+        o.kernel = predict_param(T, 2, xg);
+        *a.out = o;
+        cudaGraphSetConditional(h, (o.kernel >= 0 && o.kernel < KP_NUM_KERNELS) ? (unsigned)o.kernel
+                                                                               : (unsigned)KP_NUM_KERNELS);
     }
 }
 
@@ -487,6 +553,56 @@ int launch_wave(const O *off, int64_t n_rows, int64_t div, int64_t wave, int64_t
 }
 
 }  // namespace
+
+// ---- plan select (graph flavour of K15): trees copied once to the host at plan creation
+int plan_trees_load(const void *d_sel, const void *d_known, const void *d_gath, ParamTrees *T) {
+    const void *src[3] = {d_sel, d_known, d_gath};
+    *T = ParamTrees{};
+    for (int t = 0; t < 3; ++t) {
+        kp_tree_header h;
+        KP_CUDA_TRY(cudaMemcpy(&h, src[t], sizeof(h), cudaMemcpyDeviceToHost));
+        if (h.n_nodes < 1 || h.n_nodes > kParamTreeNodes) return KP_EINVAL;
+        KP_CUDA_TRY(cudaMemcpy(T->node[t], reinterpret_cast<const kp_tree_header *>(src[t]) + 1,
+                               (size_t)h.n_nodes * sizeof(kp_tree_node), cudaMemcpyDeviceToHost));
+        for (int i = 0; i < h.n_nodes; ++i) {  // a malformed tree must not walk out of the table
+            const kp_tree_node &nd = T->node[t][i];
+            if (nd.feature >= 0 && (nd.left <= i || nd.right <= i || nd.left >= h.n_nodes || nd.right >= h.n_nodes ||
+                                    nd.feature >= (t == 2 ? 8 : 4)))
+                return KP_EINVAL;
+        }
+        T->n[t] = h.n_nodes;
+    }
+    return KP_OK;
+}
+
+int launch_plan_select(const void *d_off, int32_t off_type, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                       int64_t iters, const ParamTrees &T, kp_outcome *d_out, void *d_ws,
+                       cudaGraphConditionalHandle h, cudaStream_t s) {
+    K1Args a = {};
+    a.off = d_off; a.n_rows = n_rows; a.n_cols = n_cols; a.nnz = nnz; a.iters = iters;
+    a.mode = kModeSeer; a.out = d_out; a.ws = (RedWorkspace *)d_ws;
+    // launch-shape hint only: the kernel evaluates the selector on the device every run;
+    // for a KNOWN-path plan (static shape) one CTA answers, else a full feature-pass grid
+    const double xk[4] = {(double)n_rows, (double)n_cols, (double)nnz, (double)iters};
+    int32_t i = 0;
+    while (T.node[0][i].feature >= 0) i = (xk[T.node[0][i].feature] <= T.node[0][i].threshold) ? T.node[0][i].left : T.node[0][i].right;
+    const bool known = T.node[0][i].value == KP_USE_KNOWN;
+    const bool aligned = ((uintptr_t)d_off & 15) == 0;
+    if (off_type == KP_I32) {
+        const int g = known ? 1 : grid_for(n_rows, 8);
+        if (aligned) k_seer_plan_select<int32_t, true><<<g, kRedThreads, 0, s>>>(a, T, h);
+        else k_seer_plan_select<int32_t, false><<<g, kRedThreads, 0, s>>>(a, T, h);
+    } else if (off_type == KP_I64) {
+        const int g = known ? 1 : grid_for(n_rows, 4);
+        if (aligned) k_seer_plan_select<int64_t, true><<<g, kRedThreads, 0, s>>>(a, T, h);
+        else k_seer_plan_select<int64_t, false><<<g, kRedThreads, 0, s>>>(a, T, h);
+    } else {
+        return KP_EINVAL;
+    }
+    KP_LAUNCHED();
+    return KP_OK;
+}
+
 }  // namespace kp
 
 using namespace kp;

@@ -589,9 +589,9 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
         // blocked read-back: products and row index of every owned position
         int ri[kIPT];
         {
-            // max-scan of the RAW marks: current marks (tag | k+1) beat every stale one
-            // (smaller tag), so ri = max(raw - tag, 0) without decoding each mark
-            int run = 0;
+            // max-scan of the RAW marks floored at `tag`: current marks (tag | k+1) beat
+            // every stale one (smaller tag), so ri holds tag + row index without decoding
+            int run = tag;
 #pragma unroll
             for (int t = 0; t < kIPT; ++t) {
                 const int q = jb + t + ((jb + t) >> 5);
@@ -608,7 +608,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
             int excl = __shfl_up_sync(0xffffffffu, incl, 1);
             if (lane == 0) excl = 0;
 #pragma unroll
-            for (int t = 0; t < kIPT; ++t) ri[t] = max(max(ri[t], excl) - tag, 0);
+            for (int t = 0; t < kIPT; ++t) ri[t] = max(ri[t], excl);
         }
         // thread-local segmented scan
         V acc[kIPT];
@@ -640,8 +640,8 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
             const int rnext = (t + 1 < kIPT) ? ri[t + 1] : next_first;
             if (pos < nz && (pos == nz - 1 || rnext != ri[t])) {  // last element of its row in the unit
                 V vt = t < first_head ? acc[t] + cin : acc[t];
-                if (ri[t] == 0) vt += carry;  // the row continued from earlier units
-                rowv[ri[t]] = vt;
+                if (ri[t] == tag) vt += carry;  // row index 0: continued from earlier units
+                rowv[ri[t] - tag] = vt;
             }
         }
         __syncwarp();
