@@ -320,7 +320,7 @@ def run_ours(a):
         seer_mean = total / a.steps if world == 1 else sum(step_t) / a.steps
         for kk in range(len(kernels.KERNELS)):
             tot, inner = timed(kk, max(3, a.steps // 2), 2)
-            t_tot, t_sp = statistics.mean(tot), statistics.mean(inner) / k
+            t_tot, t_sp = statistics.median(tot), statistics.median(inner) / k
             w = None
             if kk == kernels.ELL_TM:
                 P = kernels.prepare(A, kk, cache=False)

@@ -154,24 +154,28 @@ __device__ __forceinline__ void stats_accum(const O *__restrict__ off, int64_t n
     if constexpr (kVec) {
         constexpr int V = Vec16<O>::V;
         const int64_t nvec = n_rows / V;  // vector v covers rows v*V .. v*V+V-1
-        // two independent 16-byte vectors per lane per iteration (64 warps x 1 KB in flight per SM)
-        for (int64_t base = gwarp * 64; base < nvec; base += nwarps * 64) {
-            int64_t e[2][V];
+        // kH independent 16-byte vectors per lane per iteration, plus (lane 31 / the last
+        // vector) the following offset, all issued before any use
+        constexpr int kH = 4;
+        for (int64_t base = gwarp * (32 * kH); base < nvec; base += nwarps * (32 * kH)) {
+            int64_t e[kH][V];
+            int64_t nx[kH];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kH; ++h) {
                 const int64_t v = base + h * 32 + lane;
                 if (v < nvec) Vec16<O>::load(off + v * V, e[h]);
                 else {
 #pragma unroll
                     for (int k = 0; k < V; ++k) e[h][k] = 0;
                 }
+                nx[h] = (v < nvec && (lane == 31 || v + 1 >= nvec)) ? ldo(off + (v + 1) * V) : 0;
             }
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
+            for (int h = 0; h < kH; ++h) {
                 const int64_t v = base + h * 32 + lane;
                 const bool act = v < nvec;
                 int64_t nxt = __shfl_down_sync(0xffffffffu, e[h][0], 1);
-                if (act && (lane == 31 || v + 1 >= nvec)) nxt = ldo(off + (v + 1) * V);
+                if (act && (lane == 31 || v + 1 >= nvec)) nxt = nx[h];
                 if (act) {
 #pragma unroll
                     for (int k = 0; k < V - 1; ++k) acc_len(e[h][k], e[h][k + 1], lo, hi, s2);
@@ -309,10 +313,11 @@ __global__ void __launch_bounds__(kRedThreads) k_row_stats(K1Args a) {
 
     int64_t lo, hi;
     uint64_t s2;
+    // sum = off[n] - off[0] telescopes; loaded up front so the last CTA's tail has no extra round trip
+    const int64_t n = a.n_rows;
+    const int64_t s1 = (threadIdx.x == 0 && n > 0) ? (int64_t)((uint64_t)ldo(off + n) - (uint64_t)ldo(off)) : 0;
     if (!k1_pass<O, kVec>(a, off, lo, hi, s2)) return;
     if (threadIdx.x == 0) {
-        const int64_t n = a.n_rows;
-        const int64_t s1 = n > 0 ? (int64_t)((uint64_t)ldo(off + n) - (uint64_t)ldo(off)) : 0;
         if (a.mode == kModeStats) {
             a.out4[0] = lo; a.out4[1] = hi; a.out4[2] = s1; a.out4[3] = (int64_t)s2;
         } else {
@@ -369,10 +374,10 @@ __global__ void __launch_bounds__(kRedThreads) k_seer_plan_select(K1Args a, cons
     }
     int64_t lo, hi;
     uint64_t s2;
+    const int64_t n = a.n_rows;
+    const int64_t s1 = threadIdx.x == 0 ? (int64_t)((uint64_t)ldo(off + n) - (uint64_t)ldo(off)) : 0;
     if (!k1_pass<O, kVec>(a, off, lo, hi, s2)) return;
     if (threadIdx.x == 0) {
-        const int64_t n = a.n_rows;
-        const int64_t s1 = (int64_t)((uint64_t)ldo(off + n) - (uint64_t)ldo(off));
         kp_outcome o = {};
         epilogue(lo, hi, s1, (int64_t)s2, n, a.n_cols, &o);
         o.path = KP_USE_GATHERED;
@@ -501,7 +506,7 @@ __global__ void k_tree_predict(const void *tree, const double *__restrict__ x, i
 // ------------------------------------------------------------------ launch helpers
 int grid_for(int64_t n_rows, int per_thread) {
     int64_t want = (n_rows + (int64_t)kRedThreads * per_thread - 1) / ((int64_t)kRedThreads * per_thread);
-    int cap = num_sms() * 8;
+    int cap = num_sms() * 2;  // fewer, fuller CTAs: per-CTA fixed cost (ticket, reduce) amortised
     if (cap > kMaxRedBlocks) cap = kMaxRedBlocks;
     if (want < 1) want = 1;
     return (int)(want < cap ? want : cap);
@@ -510,11 +515,11 @@ int grid_for(int64_t n_rows, int per_thread) {
 int launch_k1(K1Args a, int32_t off_type, cudaStream_t s) {
     const bool aligned = ((uintptr_t)a.off & 15) == 0;
     if (off_type == KP_I32) {
-        int g = grid_for(a.n_rows, 8);
+        int g = grid_for(a.n_rows, 16);
         if (aligned) k_row_stats<int32_t, true><<<g, kRedThreads, 0, s>>>(a);
         else k_row_stats<int32_t, false><<<g, kRedThreads, 0, s>>>(a);
     } else if (off_type == KP_I64) {
-        int g = grid_for(a.n_rows, 4);
+        int g = grid_for(a.n_rows, 8);
         if (aligned) k_row_stats<int64_t, true><<<g, kRedThreads, 0, s>>>(a);
         else k_row_stats<int64_t, false><<<g, kRedThreads, 0, s>>>(a);
     } else {
@@ -589,11 +594,11 @@ int launch_plan_select(const void *d_off, int32_t off_type, int64_t n_rows, int6
     const bool known = T.node[0][i].value == KP_USE_KNOWN;
     const bool aligned = ((uintptr_t)d_off & 15) == 0;
     if (off_type == KP_I32) {
-        const int g = known ? 1 : grid_for(n_rows, 8);
+        const int g = known ? 1 : grid_for(n_rows, 16);
         if (aligned) k_seer_plan_select<int32_t, true><<<g, kRedThreads, 0, s>>>(a, T, h);
         else k_seer_plan_select<int32_t, false><<<g, kRedThreads, 0, s>>>(a, T, h);
     } else if (off_type == KP_I64) {
-        const int g = known ? 1 : grid_for(n_rows, 4);
+        const int g = known ? 1 : grid_for(n_rows, 8);
         if (aligned) k_seer_plan_select<int64_t, true><<<g, kRedThreads, 0, s>>>(a, T, h);
         else k_seer_plan_select<int64_t, false><<<g, kRedThreads, 0, s>>>(a, T, h);
     } else {

@@ -675,107 +675,128 @@ __global__ void __launch_bounds__(256) k_prep_mp(const O *__restrict__ off, int6
 }
 
 // ================================================================= COO,WM (K8 + K11)
-// Each warp owns 256 consecutive nnz; lane l the 8 at [base + 8l, base + 8l + 8)
-// (blocked; 32-byte vector loads).  Warp segmented scan by row id; a row finished in
-// the chunk is written, the row left open at the chunk end becomes the carry.
-// Empty rows (gaps between consecutive row ids) are zero-filled by the element
-// that follows the gap, so y needs no memset.
+// Persistent warps over row-sorted COO: warp `wid` owns the contiguous RANGE of 256-nnz
+// chunks [wid*cpw, (wid+1)*cpw) (cpw sized on the host so one wave of resident warps covers
+// the matrix); lane l holds the chunk's 8 nnz at [base + 8l, base + 8l + 8) (blocked;
+// 32-byte vector loads of row ids and cols).  Warp segmented scan by row id; a row
+// finished inside the chunk is written, the row open at the chunk end carries to the next
+// chunk in a register, and only the row open at the RANGE end goes through k_carry_fixup.
+// Empty rows (gaps between consecutive row ids) are zero-filled by the element that
+// follows the gap, so y needs no memset.
 template <typename V>
 __global__ void __launch_bounds__(256) k_coo_wm(const int32_t *__restrict__ rid, const int32_t *__restrict__ col,
                                                 const V *__restrict__ val, const V *__restrict__ x,
-                                                V *__restrict__ y, int64_t n_rows, int64_t nnz,
-                                                int32_t *__restrict__ crow, V *__restrict__ cval) {
+                                                V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_chunks,
+                                                int64_t cpw, int64_t n_ranges, int32_t *__restrict__ crow,
+                                                V *__restrict__ cval) {
     const int lane = threadIdx.x & 31;
-    const int64_t chunk = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int64_t base = chunk * kCooChunk;
-    if (base >= nnz) return;
-    const int64_t j0 = base + lane * kIPT;
-    int32_t r[kIPT];
-    V p[kIPT];
-    const bool full = base + kCooChunk <= nnz;
-    if (full) {
-        const int4 *rp = reinterpret_cast<const int4 *>(rid + j0);
-        const int4 *cp = reinterpret_cast<const int4 *>(col + j0);
-        int4 ra = ld_stream4(rp), rb = ld_stream4(rp + 1);
-        int4 ca = ld_stream4(cp), cb = ld_stream4(cp + 1);
-        r[0] = ra.x; r[1] = ra.y; r[2] = ra.z; r[3] = ra.w; r[4] = rb.x; r[5] = rb.y; r[6] = rb.z; r[7] = rb.w;
-        const int32_t c[kIPT] = {ca.x, ca.y, ca.z, ca.w, cb.x, cb.y, cb.z, cb.w};
-        V vv[kIPT];
-        const int4 *vp = reinterpret_cast<const int4 *>(val + j0);  // 8 values = 2 (fp32) / 4 (fp64) x 16 B
+    const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    if (wid >= n_ranges) return;
+    const int64_t c_begin = wid * cpw;
+    const int64_t c_end = c_begin + cpw < n_chunks ? c_begin + cpw : n_chunks;
+    // row of the element before the range, and the partial of that row accumulated inside
+    // this range (0 at the range start: earlier ranges publish their own carries)
+    int32_t prow = c_begin > 0 ? __ldg(rid + c_begin * kCooChunk - 1) : -1;
+    V carry = V(0);
+    bool open = false;
+    // chunk loader: 32-byte vector loads for full chunks, predicated scalars for the last
+    auto load = [&](int64_t base, int32_t (&r)[kIPT], int32_t (&c)[kIPT], V (&v)[kIPT]) {
+        const int64_t j0 = base + lane * kIPT;
+        if (base + kCooChunk <= nnz) {
+            const int4 *rp = reinterpret_cast<const int4 *>(rid + j0);
+            const int4 *cp = reinterpret_cast<const int4 *>(col + j0);
+            const int4 ra = ld_stream4(rp), rb = ld_stream4(rp + 1);
+            const int4 ca = ld_stream4(cp), cb = ld_stream4(cp + 1);
+            r[0] = ra.x; r[1] = ra.y; r[2] = ra.z; r[3] = ra.w; r[4] = rb.x; r[5] = rb.y; r[6] = rb.z; r[7] = rb.w;
+            c[0] = ca.x; c[1] = ca.y; c[2] = ca.z; c[3] = ca.w; c[4] = cb.x; c[5] = cb.y; c[6] = cb.z; c[7] = cb.w;
+            const int4 *vp = reinterpret_cast<const int4 *>(val + j0);  // 8 values = 2 (fp32) / 4 (fp64) x 16 B
 #pragma unroll
-        for (int q = 0; q < (int)(kIPT * sizeof(V) / 16); ++q) {
-            const int4 w = ld_stream4(vp + q);
-            memcpy(&vv[q * 16 / sizeof(V)], &w, 16);
-        }
+            for (int q = 0; q < (int)(kIPT * sizeof(V) / 16); ++q) {
+                const int4 w = ld_stream4(vp + q);
+                memcpy(&v[q * 16 / sizeof(V)], &w, 16);
+            }
+        } else {
 #pragma unroll
-        for (int k = 0; k < kIPT; ++k) p[k] = vv[k] * ld_x(x + c[k]);
-    } else {
-#pragma unroll
-        for (int k = 0; k < kIPT; ++k) {
-            const int64_t j = j0 + k;
-            if (j < nnz) {
-                r[k] = ld_stream(rid + j);
-                p[k] = ld_stream(val + j) * ld_x(x + ld_stream(col + j));
-            } else {
-                r[k] = INT32_MAX;  // sentinel past the end: never written
-                p[k] = 0;
+            for (int k = 0; k < kIPT; ++k) {
+                const int64_t j = j0 + k;
+                r[k] = j < nnz ? ld_stream(rid + j) : INT32_MAX;  // sentinel past the end: never written
+                c[k] = j < nnz ? ld_stream(col + j) : 0;
+                v[k] = j < nnz ? ld_stream(val + j) : V(0);
             }
         }
-    }
-    // previous element's row (for heads and gap fill)
-    int32_t prev = __shfl_up_sync(0xffffffffu, r[kIPT - 1], 1);
-    if (lane == 0) prev = base > 0 ? __ldg(rid + base - 1) : -1;
-    // next element's row (for row ends)
-    int32_t next = __shfl_down_sync(0xffffffffu, r[0], 1);
-    if (lane == 31) next = (base + kCooChunk < nnz) ? __ldg(rid + base + kCooChunk) : INT32_MAX;
-    // thread-local segmented inclusive scan; elements before the lane's first head
-    // continue the previous lane's segment (carry_in from the warp scan below)
-    V acc[kIPT];
-    int first_head_k = kIPT;
-    {
+    };
+    for (int64_t chunk = c_begin; chunk < c_end; ++chunk) {
+        const int64_t base = chunk * kCooChunk;
+        const int64_t j0 = base + lane * kIPT;
+        int32_t r[kIPT];
+        V p[kIPT];
+        const bool full = base + kCooChunk <= nnz;
+        {
+            int32_t c[kIPT];
+            V vv[kIPT];
+            load(base, r, c, vv);
+#pragma unroll
+            for (int k = 0; k < kIPT; ++k) p[k] = vv[k] * ld_x(x + c[k]);
+        }
+        // first row of the next chunk (row-end test of the chunk's last element)
+        const int32_t nxt_chunk = (lane == 31 && base + kCooChunk < nnz) ? __ldg(rid + base + kCooChunk) : INT32_MAX;
+        int32_t prev = __shfl_up_sync(0xffffffffu, r[kIPT - 1], 1);
+        if (lane == 0) prev = prow;
+        int32_t next = __shfl_down_sync(0xffffffffu, r[0], 1);
+        if (lane == 31) next = nxt_chunk;
+        // thread-local segmented inclusive scan; elements before the lane's first head
+        // continue the previous lane's segment (carry_in from the warp scan below)
+        V acc[kIPT];
+        int first_head_k = kIPT;
+        {
+            int32_t pr = prev;
+#pragma unroll
+            for (int k = 0; k < kIPT; ++k) {
+                const bool head = r[k] != pr;
+                if (head && first_head_k == kIPT) first_head_k = k;
+                acc[k] = (head || k == 0) ? p[k] : acc[k - 1] + p[k];
+                pr = r[k];
+            }
+        }
+        // warp segmented scan of the lanes' last-segment sums (head flags as a ballot mask)
+        V inc = acc[kIPT - 1];
+        {
+            const unsigned heads = __ballot_sync(0xffffffffu, first_head_k < kIPT);
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const V up = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o && ((heads >> (lane - o + 1)) & ((1u << o) - 1u)) == 0) inc = up + inc;
+            }
+        }
+        V carry_in = __shfl_up_sync(0xffffffffu, inc, 1);
+        if (lane == 0) carry_in = V(0);
+        // gap fill + row ends
         int32_t pr = prev;
+        V vlast = V(0);
 #pragma unroll
         for (int k = 0; k < kIPT; ++k) {
-            const bool head = r[k] != pr;
-            if (head && first_head_k == kIPT) first_head_k = k;
-            acc[k] = (head || k == 0) ? p[k] : acc[k - 1] + p[k];
-            pr = r[k];
+            const int32_t rk = r[k];
+            if (rk != INT32_MAX) {
+                for (int64_t g = (int64_t)pr + 1; g < rk; ++g) y[g] = V(0);  // rows strictly between are empty
+                const int32_t nx = (k + 1 < kIPT) ? r[k + 1] : next;
+                V v = (k < first_head_k) ? acc[k] + carry_in : acc[k];
+                if (rk == prow) v += carry;  // row continued from the previous chunk of this range
+                if (nx != rk) y[rk] = v;     // row ends here
+                if (j0 + k == nnz - 1)       // trailing empty rows after the very last nnz
+                    for (int64_t g = (int64_t)rk + 1; g < n_rows; ++g) y[g] = V(0);
+                vlast = v;
+                pr = rk;
+            }
         }
+        // the row open at the chunk end carries to the next chunk (lane 31 holds it)
+        const int32_t rl = __shfl_sync(0xffffffffu, r[kIPT - 1], 31);
+        open = __shfl_sync(0xffffffffu, next == r[kIPT - 1] && full && base + kCooChunk < nnz, 31);
+        carry = open ? __shfl_sync(0xffffffffu, vlast, 31) : V(0);
+        prow = rl;
     }
-    // warp exclusive segmented scan of (has_head, last-segment sum)
-    SegPair<V> inc{first_head_k < kIPT ? 1 : 0, acc[kIPT - 1]};
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        SegPair<V> t{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
-        if (lane >= o) inc = seg_op(t, inc);
-    }
-    SegPair<V> ex{__shfl_up_sync(0xffffffffu, inc.f, 1), __shfl_up_sync(0xffffffffu, inc.v, 1)};
-    if (lane == 0) ex = SegPair<V>{0, V(0)};
-    const V carry_in = ex.v;  // applies to elements before this lane's first head
-    // gap fill + row ends
-    int32_t pr = prev;
-#pragma unroll
-    for (int k = 0; k < kIPT; ++k) {
-        const int32_t rk = r[k];
-        if (rk != INT32_MAX) {
-            // rows strictly between pr and rk are empty
-            for (int64_t g = (int64_t)pr + 1; g < rk; ++g) y[g] = V(0);
-            const int32_t nx = (k + 1 < kIPT) ? r[k + 1] : next;
-            const V v = (k < first_head_k) ? acc[k] + carry_in : acc[k];
-            // row ends here (rows continued from earlier chunks get their carries in the fix-up)
-            if (nx != rk) y[rk] = v;
-            // trailing empty rows after the very last nnz
-            if (j0 + k == nnz - 1)
-                for (int64_t g = (int64_t)rk + 1; g < n_rows; ++g) y[g] = V(0);
-            pr = rk;
-        }
-    }
-    // carry: the row open at the chunk end continues into the next chunk
-    if (lane == 31) {
-        const int32_t rl = r[kIPT - 1];
-        const bool open = (base + kCooChunk < nnz) && next == rl;
-        crow[chunk] = open ? rl : -1;
-        cval[chunk] = open ? ((kIPT - 1 < first_head_k) ? acc[kIPT - 1] + carry_in : acc[kIPT - 1]) : V(0);
+    if (lane == 0) {
+        crow[wid] = open ? prow : -1;
+        cval[wid] = open ? carry : V(0);
     }
 }
 
@@ -1148,6 +1169,25 @@ MergeGeom merge_geom(const kp_csr *A) {
     return G;
 }
 int64_t coo_chunks(const kp_csr *A) { return (A->nnz + kCooChunk - 1) / kCooChunk; }
+template <typename V>
+MergeGeom coo_geom(const kp_csr *A) {
+    static int warps_per_sm = 0;
+    if (!warps_per_sm) {
+        int nb = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_coo_wm<V>, 256, 0) != cudaSuccess || nb <= 0) {
+            cudaGetLastError();
+            nb = 8;
+        }
+        warps_per_sm = nb * 8;
+    }
+    MergeGeom G;
+    G.n_units = coo_chunks(A);
+    const int64_t target = g_wave_warps > 0 ? g_wave_warps : (int64_t)num_sms() * warps_per_sm;
+    G.upw = (G.n_units + target - 1) / target;
+    if (G.upw < 1) G.upw = 1;
+    G.n_ranges = (G.n_units + G.upw - 1) / G.upw;
+    return G;
+}
 int64_t ad_units_max(const kp_csr *A) {
     return A->n_rows + A->nnz / kAdLongChunk + 2;
 }
@@ -1354,12 +1394,12 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
         case KP_COO_WM: {
             if (!P || !P->buf) return KP_EINVAL;
             const Layout L = prep_layout(KP_COO_WM, A, 0);
-            const int64_t chunks = coo_chunks(A);
-            const int64_t g = (chunks * 32 + 255) / 256;
+            const MergeGeom G = coo_geom<V>(A);
+            const int64_t g = (G.n_ranges * 32 + 255) / 256;
             k_coo_wm<V><<<(unsigned)g, 256, 0, s>>>(reinterpret_cast<const int32_t *>((unsigned char *)P->buf + L.a), col,
-                                                    val, x, y, R, Z, crow, cval);
+                                                    val, x, y, R, Z, G.n_units, G.upw, G.n_ranges, crow, cval);
             KP_LAUNCHED();
-            k_carry_fixup<V><<<(unsigned)((chunks * 32 + 255) / 256), 256, 0, s>>>(crow, cval, nullptr, chunks, y);
+            k_carry_fixup<V><<<(unsigned)((G.n_ranges * 32 + 255) / 256), 256, 0, s>>>(crow, cval, nullptr, G.n_ranges, y);
             KP_LAUNCHED();
             return KP_OK;
         }
@@ -1417,6 +1457,9 @@ int kp::ensure_kernel_attrs() {
     if (!rc) rc = tm_attrs<double, int32_t>();
     if (!rc) rc = tm_attrs<double, int64_t>();
     // occupancy queries cached outside any graph capture
+    kp_csr dummy = {};
+    coo_geom<float>(&dummy);
+    coo_geom<double>(&dummy);
     merge_warps_per_sm<float, int32_t>();
     merge_warps_per_sm<float, int64_t>();
     merge_warps_per_sm<double, int32_t>();
