@@ -145,6 +145,15 @@ KP_API int kp_seer_select(const void *d_off, int32_t off_type, int64_t n_rows, i
                    const void *d_known, const void *d_gathered, kp_outcome *d_out,
                    void *d_ws, void *stream);
 
+/* Row-sharded seer-core.infer (multi-GPU): d_parts holds n_parts rows of
+ * (lo, hi, s1, s2) = kp_length_stats of each rank's row block (one 32-byte all-gather);
+ * they combine exactly (min, max, wrapping sums) into the single-matrix reduction, so the
+ * outcome equals kp_seer_select on the whole matrix.  n_rows / n_cols / nnz are GLOBAL. */
+KP_API int kp_seer_select_partials(const int64_t *d_parts, int32_t n_parts, int64_t n_rows,
+                                   int64_t n_cols, int64_t nnz, int64_t iterations,
+                                   const void *d_selector, const void *d_known,
+                                   const void *d_gathered, kp_outcome *d_out, void *stream);
+
 /* ------------------------------------------------------------ preprocessing */
 /* Bytes the caller must provide for kp_prepare(kernel, A).  ell_cap (ELL only) is
  * the width reserved for the padded part; rows longer than the actual width

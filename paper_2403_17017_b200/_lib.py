@@ -26,6 +26,7 @@ EXPORTS = (
     "kp_tree_predict", "kp_seer_select", "kp_prepare_bytes", "kp_prepare",
     "kp_spmv_workspace_bytes", "kp_spmv", "kp_seer_plan_bytes", "kp_seer_plan_create", "kp_seer_plan_launch",
     "kp_seer_plan_destroy", "kp_shard_partition", "kp_version", "kp_launch_count", "kp_debug_set_wave_warps",
+    "kp_seer_select_partials",
 )
 
 
@@ -93,6 +94,7 @@ def load(require: bool = True):
         "kp_version": (ctypes.c_char_p, []),
         "kp_launch_count": (ctypes.c_uint64, []),
         "kp_debug_set_wave_warps": (ctypes.c_int64, [i64]),
+        "kp_seer_select_partials": (ctypes.c_int, [p, i32, i64, i64, i64, i64, p, p, p, p, p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

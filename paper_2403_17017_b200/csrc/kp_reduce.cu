@@ -557,6 +557,40 @@ int launch_wave(const O *off, int64_t n_rows, int64_t div, int64_t wave, int64_t
     return KP_OK;
 }
 
+// Multi-GPU K15: every rank holds the (lo, hi, s1, s2) partials of all ranks' row blocks
+// (one 32-byte all-gather); combine exactly (min / max / wrapping sums = the single-matrix
+// reduction, _core.pyx:25-32), then the same selector / epilogue / tree path as K1+K15.
+__global__ void k_seer_select_partials(const int64_t *__restrict__ parts, int32_t n_parts, int64_t n_rows,
+                                       int64_t n_cols, int64_t nnz, int64_t iters, const void *sel, const void *known,
+                                       const void *gath, kp_outcome *out) {
+    if (threadIdx.x != 0) return;
+    const double xk[4] = {(double)n_rows, (double)n_cols, (double)nnz, (double)iters};
+    double xkk[4] = {xk[0], xk[1], xk[2], xk[3]};
+    kp_outcome o = {};
+    if (predict_global(sel, xkk) == KP_USE_KNOWN) {
+        o.kernel = predict_global(known, xkk);
+        o.path = KP_USE_KNOWN;
+        o.status = KP_OK;
+        *out = o;
+        return;
+    }
+    int64_t lo = INT64_MAX, hi = INT64_MIN;
+    uint64_t s1 = 0, s2 = 0;
+    for (int p = 0; p < n_parts; ++p) {
+        const int64_t *q = parts + 4 * p;
+        lo = q[0] < lo ? q[0] : lo;
+        hi = q[1] > hi ? q[1] : hi;
+        s1 += (uint64_t)q[2];
+        s2 += (uint64_t)q[3];
+    }
+    if (n_rows <= 0) { lo = hi = 0; s1 = s2 = 0; }
+    epilogue(lo, hi, (int64_t)s1, (int64_t)s2, n_rows, n_cols, &o);
+    o.path = KP_USE_GATHERED;
+    double xg[8] = {xk[0], xk[1], xk[2], xk[3], o.max_d, o.min_d, o.mean_d, o.var_d};
+    o.kernel = predict_global(gath, xg);
+    *out = o;
+}
+
 }  // namespace
 
 // ---- plan select (graph flavour of K15): trees copied once to the host at plan creation
@@ -673,6 +707,17 @@ int kp_tree_predict(const void *d_tree, const double *d_x, int64_t n, int32_t n_
     int64_t want = (n + 255) / 256;
     int g = (int)(want < num_sms() * 8 ? want : num_sms() * 8);
     k_tree_predict<<<g, 256, 0, (cudaStream_t)stream>>>(d_tree, d_x, n, n_feat, d_out);
+    KP_LAUNCHED();
+    return KP_OK;
+}
+
+int kp_seer_select_partials(const int64_t *d_parts, int32_t n_parts, int64_t n_rows, int64_t n_cols, int64_t nnz,
+                            int64_t iterations, const void *d_selector, const void *d_known, const void *d_gathered,
+                            kp_outcome *d_out, void *stream) {
+    if (n_parts < 1 || n_rows <= 0 || n_cols <= 0 || !d_parts || !d_out || !d_selector || !d_known || !d_gathered)
+        return KP_EINVAL;
+    k_seer_select_partials<<<1, 32, 0, (cudaStream_t)stream>>>(d_parts, n_parts, n_rows, n_cols, nnz, iterations,
+                                                               d_selector, d_known, d_gathered, d_out);
     KP_LAUNCHED();
     return KP_OK;
 }

@@ -286,3 +286,70 @@ def train_tree(X, y, max_depth: int = 5, min_samples_leaf: int = 1, n_classes: i
     # leaves keep their class; split nodes carry value -1 -> normalise to 0 for packing
     t.value = [v if f < 0 else 0 for f, v in zip(t.feature, t.value)]
     return t
+
+
+def train_cost_tree(X, C, max_depth: int = 5, min_samples_leaf: int = 1, feature_names=()) -> DecisionTree:
+    """Cost-sensitive CART (extension; same tree format and ``predict`` as SPEC's CART).
+
+    ``C[i, j]`` is the loss of predicting class j for example i (e.g. log(t_j / t_best)).
+    A leaf predicts argmin_j sum_i C[i, j] (lowest class on ties); a split minimises the
+    children's summed leaf losses, thresholds at midpoints between distinct sorted values,
+    ``x <= thr`` goes left, first (feature, threshold) wins ties -- deterministic like
+    ``train_tree``.  Kernel families with 100-1000x outliers make the label-purity
+    criterion (Gini) a poor proxy for the time a wrong pick costs; this optimises it."""
+    X = np.asarray(X, dtype=np.float64)
+    C = np.asarray(C, dtype=np.float64)
+    if C.ndim != 2 or X.ndim != 2 or X.shape[0] != C.shape[0] or C.shape[0] == 0:
+        raise ValueError("X (n, f) and C (n, classes) must be non-empty and aligned")
+    if not np.all(np.isfinite(C)):
+        raise ValueError("costs must be finite (cap missing kernels first)")
+    k = C.shape[1]
+    t = DecisionTree(n_classes=k, n_features=X.shape[1], max_depth=max_depth, feature_names=list(feature_names))
+
+    def leaf(idx):
+        s = C[idx].sum(axis=0)
+        j = int(np.argmin(s))
+        return j, float(s[j])
+
+    def split(idx):
+        best = None
+        _, here = leaf(idx)
+        for f in range(X.shape[1]):
+            xs = X[idx, f]
+            order = np.argsort(xs, kind="stable")
+            xv = xs[order]
+            cs = np.cumsum(C[idx][order], axis=0)
+            tot = cs[-1]
+            n = xv.size
+            # candidate cut after position p (left = 0..p): distinct neighbours, leaf sizes
+            p = np.arange(min_samples_leaf - 1, n - min_samples_leaf)
+            p = p[xv[p] < xv[p + 1]]
+            if p.size == 0:
+                continue
+            loss = cs[p].min(axis=1) + (tot - cs[p]).min(axis=1)
+            q = int(np.argmin(loss))
+            if best is None or loss[q] < best[2] - 1e-12:
+                best = (f, _midpoint(float(xv[p[q]]), float(xv[p[q] + 1])), float(loss[q]))
+        if best is None or best[2] >= here - 1e-12:
+            return None  # no split lowers the loss
+        return best
+
+    def grow(idx: np.ndarray, depth: int) -> int:
+        node = t._add(-1, 0.0, leaf(idx)[0])
+        if depth >= max_depth or idx.size < 2 * min_samples_leaf:
+            return node
+        s = split(idx)
+        if s is None:
+            return node
+        f, thr, _ = s
+        go_left = X[idx, f] <= thr
+        t.feature[node] = f
+        t.threshold[node] = thr
+        t.value[node] = -1
+        t.left[node] = grow(idx[go_left], depth + 1)
+        t.right[node] = grow(idx[~go_left], depth + 1)
+        return node
+
+    grow(np.arange(C.shape[0]), 0)
+    t.value = [v if f < 0 else 0 for f, v in zip(t.feature, t.value)]
+    return t

@@ -260,7 +260,8 @@ def selector_label(row, known_pred: int, gathered_pred: int, k: int) -> int:
 
 
 def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int = 1,
-               kernels=KERNELS, meta: dict | None = None, weighting: str = "none") -> SeerModel:
+               kernels=KERNELS, meta: dict | None = None, weighting: str = "none",
+               near_best: float = 0.0) -> SeerModel:
     """labels = fastest_kernel per (matrix, k); known tree on the known
     schema, gathered tree on the full schema, selector on labels from the two
     sub-models' own predictions on the training rows.
@@ -270,8 +271,23 @@ def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int 
     kernel trees by log1p(mean relative regret over the other kernels), the selector by
     |log(realised gathered-path cost / realised known-path cost)| -- measured kernel
     families have 100-1000x outliers (thread-mapped schedules on 1M-nnz rows) that
-    unweighted CART treats like a 1% miss."""
+    unweighted CART treats like a 1% miss.
+
+    near_best > 0 (extension) relabels each example with the kernel that is most often
+    within (1 + near_best) x the best time across the training set, among the kernels
+    within that factor on this example: ties between near-equal kernels stop being label
+    noise for CART (the realised cost changes by < near_best)."""
     nk = len(kernels)
+    pref = np.zeros(nk)
+    if near_best > 0:
+        for r in rows:
+            for k in iterations:
+                c = [r.cost(j, k) for j in range(nk)]
+                b = min(c)
+                if np.isfinite(b):
+                    for j in range(nk):
+                        if c[j] <= b * (1 + near_best):
+                            pref[j] += 1
     Xk, Xg, y, ex, wk = [], [], [], [], []
     for r in rows:
         if r.gathered is None:
@@ -281,6 +297,10 @@ def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int 
                 lab = fastest_kernel(r.timings(), k)
             except Exception:
                 continue
+            if near_best > 0:
+                b = r.cost(lab, k)
+                cands = [j for j in range(nk) if r.cost(j, k) <= b * (1 + near_best)]
+                lab = max(cands, key=lambda j: (pref[j], -j))
             kv = known_vector(*r.known, k)
             Xk.append(kv)
             Xg.append(kv + tuple(r.gathered))
@@ -292,8 +312,10 @@ def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int 
             wk.append(float(np.log1p(np.mean(regrets))) if regrets else 0.0)
     if not y:
         raise ValueError("no labelled examples")
+    if weighting in ("cost-log", "cost-rel"):
+        return _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, weighting)
     if weighting not in ("none", "regret"):
-        raise ValueError("weighting must be 'none' or 'regret'")
+        raise ValueError("weighting must be 'none', 'regret', 'cost-log' or 'cost-rel'")
     w = None if weighting == "none" else np.asarray(wk) + 1e-3
     kt = train_tree(Xk, y, max_depth, min_samples_leaf, nk, KNOWN_SCHEMA, w)
     gt = train_tree(Xg, y, max_depth, min_samples_leaf, nk, GATHERED_SCHEMA, w)
@@ -307,6 +329,35 @@ def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int 
     st = train_tree(Xk, ys, max_depth, min_samples_leaf, 2, KNOWN_SCHEMA, ws)
     meta = dict(meta or {})
     meta.setdefault("weighting", weighting)
+    return SeerModel(kt, gt, st, kernels, meta)
+
+
+def _loss(costs, kind: str, cap: float = 1e3):
+    c = np.asarray(costs, dtype=np.float64)
+    b = np.min(c[np.isfinite(c)])
+    r = np.where(np.isfinite(c), c / b, cap)
+    r = np.minimum(r, cap)
+    return np.log(r) if kind == "cost-log" else r - 1.0
+
+
+def _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, kind) -> SeerModel:
+    """Cost-sensitive trio (extension): kernel trees minimise the summed loss of the
+    realised per-iteration-count cost (log or relative regret vs the example's best
+    kernel), the selector minimises the loss of the realised known vs gathered path
+    (collection time charged, SPEC.md:367-375 costs)."""
+    from .dtree import train_cost_tree
+    nk = len(kernels)
+    Ck = np.stack([_loss([r.cost(j, k) for j in range(nk)], kind) for r, k in ex])
+    kt = train_cost_tree(Xk, Ck, max_depth, min_samples_leaf, KNOWN_SCHEMA)
+    gt = train_cost_tree(Xg, Ck, max_depth, min_samples_leaf, GATHERED_SCHEMA)
+    Cs = []
+    for (r, k), xk, xg in zip(ex, Xk, Xg):
+        ck = r.cost(kt.predict(xk), k)
+        cg = r.cost(gt.predict(xg), k) + r.collection_time
+        Cs.append(_loss([ck, cg], kind))
+    st = train_cost_tree(Xk, np.stack(Cs), max_depth, min_samples_leaf, KNOWN_SCHEMA)
+    meta = dict(meta or {})
+    meta.setdefault("weighting", kind)
     return SeerModel(kt, gt, st, kernels, meta)
 
 

@@ -139,3 +139,34 @@ def test_determinism():
     X = rng.normal(size=(500, 8))
     y = rng.integers(0, 8, 500)
     assert dtree.train_tree(X, y).serialize() == dtree.train_tree(X, y).serialize()
+
+
+def test_cost_tree_minimises_realised_loss():
+    """Cost-sensitive CART: leaves pick argmin summed loss, splits only when they lower it."""
+    import numpy as np
+    from paper_2403_17017_b200.dtree import train_cost_tree
+    X = np.array([[0.0], [1.0], [2.0], [3.0]])
+    # class 1 is cheap on the left half, class 0 on the right; Gini on argmin labels agrees,
+    # but the 3rd example's tiny preference must not outweigh the 4th's large one
+    C = np.array([[5.0, 0.0], [5.0, 0.0], [0.0, 0.01], [0.0, 9.0]])
+    t = train_cost_tree(X, C, max_depth=3)
+    assert [t.predict(x) for x in X] == [1, 1, 0, 0]
+    assert t.threshold[0] == 1.5 and t.depth() == 1
+    # a single leaf when no split lowers the loss
+    t2 = train_cost_tree(X, np.array([[0.0, 1.0]] * 4), max_depth=3)
+    assert t2.n_nodes == 1 and t2.predict([7.0]) == 0
+
+
+def test_cost_seer_training_runs_on_corpus_rows():
+    import os
+    from paper_2403_17017_b200 import dataset, seer
+    root = os.path.join(os.path.dirname(os.path.dirname(__file__)), "paper_2403_17017_b200", "models", "corpus")
+    import csv
+    known = {r["name"]: (int(r["rows"]), int(r["cols"]), int(r["nnz"]))
+             for r in csv.DictReader(open(os.path.join(root, "known.csv")))}
+    rd = lambda f: open(os.path.join(root, f)).read()  # noqa: E731
+    rows = dataset.read_tables(rd("elapsed.csv"), rd("preprocess.csv"), rd("metadata.csv"), known)[:120]
+    m = seer.train_seer(rows, (1, 10), 4, 1, weighting="cost-log")
+    for r in rows[:20]:
+        cost, kern, path = seer.realized_cost(m, r, 1)
+        assert 0 <= kern < 8 and path in (0, 1) and cost > 0

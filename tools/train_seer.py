@@ -76,14 +76,16 @@ def main():
     ap.add_argument("--report", default=None)
     ap.add_argument("--max-depth", type=int, default=5)
     ap.add_argument("--seed", type=int, default=2403)
-    ap.add_argument("--weighting", default="regret", choices=["none", "regret"])
+    ap.add_argument("--weighting", default="regret", choices=["none", "regret", "cost-log", "cost-rel"])
+    ap.add_argument("--near-best", type=float, default=0.0, help="relabel within this fraction of the best")
     a = ap.parse_args()
     rows = load(a.corpus)
     train, test = dataset.split_train_test(rows, a.seed, 0.8)
     model = seer.train_seer(train, ITERS, a.max_depth, 1, kernels.KERNELS,
                             {"source": "B200-measured corpus (tools/collect_corpus.py)", "corpus": os.path.relpath(a.corpus, ROOT),
                              "iterations": list(ITERS), "max_depth": a.max_depth, "split_seed": a.seed,
-                             "n_train": len(train), "n_test": len(test)}, weighting=a.weighting)
+                             "n_train": len(train), "n_test": len(test), "near_best": a.near_best},
+                            weighting=a.weighting, near_best=a.near_best)
     model.save(a.out)
     plain = seer.train_seer(train, ITERS, a.max_depth, 1, kernels.KERNELS, weighting="none")
     rep = {"weighting": a.weighting, "n_train": len(train), "n_test": len(test),
