@@ -55,7 +55,7 @@ def _args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--iters", type=int, default=None, help="SpMV iterations k (default per config)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -68,6 +68,8 @@ CFG = {  # BASELINE.json configs -> (k, dtype, description)
     "C2": (1, "float32", "R-MAT s20 ef16 (0.57/0.19/0.19/0.05) permuted CSR 1M x 1M, ~16.1M nnz, fp32, k=1"),
     "C3": (100, "float32", "27-point stencil 159^3 (R=4,019,679, 107.2M nnz), fp32, k=100"),
     "C4": (1, "float64", "skewed 2M rows: Poisson(8) + 4 rows x 1M nnz, fp64, k=1"),
+    "C5": (20, "float32", "R-MAT s26 ef16 row-stochastic (64M rows, ~1.0B nnz), fp32, 20 power iterations, "
+                          "row-sharded over the ranks with an NCCL all-gather of y per iteration"),
 }
 
 
@@ -531,10 +533,110 @@ def run_reference(a):
     }), flush=True)
 
 
+# ------------------------------------------------------------------------ C5: row-sharded
+def run_sharded(a):
+    """BASELINE configs[4]: the matrix is row-sharded over the ranks (nnz-balanced, K14),
+    x replicated in the rank-padded layout, y local; each iteration's y slices are
+    all-gathered in place over NVLink (NCCL) into the next x.  Selection = global
+    features from the ranks' K1 partials (one 32-byte all-gather).  One step = the
+    chosen kernel's preprocessing + k iterations; total work fixed as N grows (strong)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2403_17017_b200 import _lib, dist as kdist, gen, kernels
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    L = _lib.load()
+    k_default, dt_name, desc = CFG["C5"]
+    k = a.iters or k_default
+    dtype = getattr(torch, dt_name)
+    t0 = time.time()
+    m = gen.config("C5", device=dev)  # every rank generates the same global matrix (counter hash)
+    R, C, Z = m.n_rows, m.n_cols, m.nnz
+    A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, C, rank, world, dtype)
+    del m
+    torch.cuda.empty_cache()
+    t_gen = time.time() - t0
+    model, model_src = _load_model()
+    run = kdist.ShardedSeer(model, A, plan, k, R, C, Z)
+    kern = run.kernel
+    x0 = torch.full((world * plan.r_max,), 1.0 / R, dtype=dtype, device=dev)
+    sv, so = 4 if dtype == torch.float32 else 8, 4
+    bytes_csr = csr_bytes(R, C, Z, sv, so)
+    for _ in range(a.warmup):
+        run.step(x0)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    n0 = L.kp_launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(a.steps):
+        run.step(x0)
+    e1.record()
+    e1.synchronize()
+    launches = L.kp_launch_count() - n0
+    total = e0.elapsed_time(e1) * 1e-3
+    if world > 1:
+        dist.barrier()
+        tt = torch.tensor([total], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total = float(tt.item())
+    # this rank's SpMV alone (dominant kernel) for the roofline
+    P = kernels.prepare(A, kern) if kern in kernels.NEEDS_PREP else None
+    ys = run.bufs[1][plan.rank * plan.r_max: plan.rank * plan.r_max + plan.local_rows]
+    ts = []
+    for _ in range(5):
+        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        m0.record()
+        kernels.spmv(A, run.bufs[0], kern, y=ys, prepared=P)
+        m1.record()
+        m1.synchronize()
+        ts.append(m0.elapsed_time(m1) * 1e-3)
+    clk = clocks.stop()
+    peak, peak_src = _peak_hbm()
+    kb = A.byte_model(kern, None if kern != kernels.ELL_TM else int(min(int(P.buf[:64].cpu().view(torch.int64)[3]), P.ell_cap)))
+    per = statistics.median(ts)
+    value = a.steps * k * bytes_csr / total / 1e9
+    if rank == 0:
+        print(json.dumps({
+            "metric": "Seer-selected SpMV GB/s (% HBM roofline) and geomean speedup vs best fixed kernel",
+            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "ms_per_step": round(total / a.steps * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32" if dtype == torch.float32 else "f64",
+            "data": "synthetic (counter-hash R-MAT generated on device)",
+            "config": {"workload": "C5", "desc": desc, "rows": R, "cols": C, "nnz": Z, "iterations": k,
+                       "parallelism": f"row-sharded x{world} (nnz-balanced, NCCL all-gather of y)",
+                       "l2": "inputs larger than L2 (A: %.1f GB)" % (bytes_csr / 1e9), "model": model_src,
+                       "byte_model": "nnz*(4+sv)+(R+1)*so+C*sv+R*sv per iteration, x counted once",
+                       "generation_s": round(t_gen, 1)},
+            "seer": {"kernel": kernels.KERNELS[kern], "path": "gathered" if run.outcome.path else "known",
+                     "dispatch": "global selection from the ranks' K1 partials at setup (device)"},
+            "roofline": {"bound": "hbm", "achieved": round(kb / per / 1e9, 1), "peak": peak, "unit": "GB/s",
+                         "frac": round(kb / per / 1e9 / peak, 4), "traffic": None, "kernel": kernels.KERNELS[kern],
+                         "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
+                         "note": "rank 0's local SpMV"},
+            "e2e": None, "gpu_launches": int(launches), "cpu_baseline": None, "clocks": clk,
+        }), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
 def main():
     a = _args()
     if a.impl == "reference":
         run_reference(a)
+    elif a.workload == "C5":
+        run_sharded(a)
     else:
         run_ours(a)
 

@@ -683,7 +683,7 @@ __global__ void __launch_bounds__(256) k_prep_mp(const O *__restrict__ off, int6
 // chunk in a register, and only the row open at the RANGE end goes through k_carry_fixup.
 // Empty rows (gaps between consecutive row ids) are zero-filled by the element that
 // follows the gap, so y needs no memset.
-template <typename V>
+template <typename V, bool kVec>
 __global__ void __launch_bounds__(256) k_coo_wm(const int32_t *__restrict__ rid, const int32_t *__restrict__ col,
                                                 const V *__restrict__ val, const V *__restrict__ x,
                                                 V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_chunks,
@@ -702,7 +702,7 @@ __global__ void __launch_bounds__(256) k_coo_wm(const int32_t *__restrict__ rid,
     // chunk loader: 32-byte vector loads for full chunks, predicated scalars for the last
     auto load = [&](int64_t base, int32_t (&r)[kIPT], int32_t (&c)[kIPT], V (&v)[kIPT]) {
         const int64_t j0 = base + lane * kIPT;
-        if (base + kCooChunk <= nnz) {
+        if (kVec && base + kCooChunk <= nnz) {
             const int4 *rp = reinterpret_cast<const int4 *>(rid + j0);
             const int4 *cp = reinterpret_cast<const int4 *>(col + j0);
             const int4 ra = ld_stream4(rp), rb = ld_stream4(rp + 1);
@@ -1174,7 +1174,7 @@ MergeGeom coo_geom(const kp_csr *A) {
     static int warps_per_sm = 0;
     if (!warps_per_sm) {
         int nb = 0;
-        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_coo_wm<V>, 256, 0) != cudaSuccess || nb <= 0) {
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_coo_wm<V, true>, 256, 0) != cudaSuccess || nb <= 0) {
             cudaGetLastError();
             nb = 8;
         }
@@ -1396,8 +1396,14 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
             const Layout L = prep_layout(KP_COO_WM, A, 0);
             const MergeGeom G = coo_geom<V>(A);
             const int64_t g = (G.n_ranges * 32 + 255) / 256;
-            k_coo_wm<V><<<(unsigned)g, 256, 0, s>>>(reinterpret_cast<const int32_t *>((unsigned char *)P->buf + L.a), col,
-                                                    val, x, y, R, Z, G.n_units, G.upw, G.n_ranges, crow, cval);
+            // 32-byte vector loads need 16-byte aligned col / val (row ids: our buffer)
+            const int32_t *rid = reinterpret_cast<const int32_t *>((unsigned char *)P->buf + L.a);
+            if ((((uintptr_t)col | (uintptr_t)val) & 15) == 0)
+                k_coo_wm<V, true><<<(unsigned)g, 256, 0, s>>>(rid, col, val, x, y, R, Z, G.n_units, G.upw, G.n_ranges,
+                                                              crow, cval);
+            else
+                k_coo_wm<V, false><<<(unsigned)g, 256, 0, s>>>(rid, col, val, x, y, R, Z, G.n_units, G.upw, G.n_ranges,
+                                                               crow, cval);
             KP_LAUNCHED();
             k_carry_fixup<V><<<(unsigned)((G.n_ranges * 32 + 255) / 256), 256, 0, s>>>(crow, cval, nullptr, G.n_ranges, y);
             KP_LAUNCHED();

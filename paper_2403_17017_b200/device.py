@@ -62,9 +62,12 @@ class DeviceCSR:
         if n_rows > _I32_MAX - 1 or n_cols > _I32_MAX:
             raise ValueError("device layout supports < 2^31 rows / columns")
         self.n_rows, self.n_cols = int(n_rows), int(n_cols)
-        self.row_offsets = row_offsets.contiguous()
-        self.col_indices = col_indices.contiguous()
-        self.values = values.contiguous()
+        # the device layout is 256-byte aligned (vector loads, 1-D TMA); views into a
+        # larger tensor (e.g. a row block) are copied once to an aligned allocation
+        al = lambda t: t.contiguous() if t.contiguous().data_ptr() % 256 == 0 else t.contiguous().clone()  # noqa: E731
+        self.row_offsets = al(row_offsets)
+        self.col_indices = al(col_indices)
+        self.values = al(values)
         self.nnz = int(col_indices.numel())
         if values.numel() != self.nnz:
             raise ValueError("values and col_indices lengths differ")

@@ -146,3 +146,112 @@ class ShardedSpMV:
                                              group=self.group)
             cur = nxt
         return p.unpad(self.bufs[cur])
+
+
+# ---------------------------------------------------------------------- device path (GPU)
+def shard_device(row_offsets, col_indices, values, n_cols: int, rank: int, world: int, dtype=None):
+    """This rank's row block of a GLOBAL CSR held in device tensors (any int / float
+    dtypes): nnz-balanced cut by K14 on the device, rows rebased, columns remapped into
+    the rank-padded x layout, stored in the device layout (int32 offsets when the block's
+    nnz < 2^31, int32 cols, fp32/fp64 values).  Returns (DeviceCSR, ShardPlan, cuts)."""
+    import torch
+    from . import _lib
+    from .device import DeviceCSR
+    _lib.require_cuda()
+    n_rows = int(row_offsets.numel()) - 1
+    off = row_offsets.contiguous()
+    if off.dtype not in (torch.int32, torch.int64):
+        off = off.to(torch.int64)
+    cuts_d = torch.empty(world + 1, dtype=torch.int64, device=off.device)
+    _lib.check(_lib.load().kp_shard_partition(off.data_ptr(), _lib.KP_I32 if off.dtype == torch.int32 else _lib.KP_I64,
+                                              n_rows, world, cuts_d.data_ptr(), _lib.stream_handle()),
+               "kp_shard_partition")
+    cuts = cuts_d.cpu().numpy()
+    plan = ShardPlan(rank, world, cuts, n_rows)
+    s, e = int(off[plan.r0]), int(off[plan.r1])
+    loff = (off[plan.r0: plan.r1 + 1].to(torch.int64) - s)
+    loff = loff.to(torch.int32 if e - s < 2**31 - 1 else torch.int64)
+    lc = remap_columns(col_indices[s:e], cuts_d, plan.r_max)
+    dt = dtype or torch.float32
+    lv = values[s:e].to(dt)
+    A = DeviceCSR(plan.local_rows, world * plan.r_max, loff, lc.to(torch.int32), lv)
+    return A, plan, cuts_d
+
+
+def _length_partials(A):
+    """(lo, hi, s1, s2) of this rank's row lengths on the device (K1); an empty block
+    gives the neutral element of the combine (lo = INT64_MAX, hi = INT64_MIN)."""
+    import torch
+    from . import _lib
+    from .device import reduce_workspace
+    if A.n_rows == 0:
+        return torch.tensor([2**63 - 1, -2**63, 0, 0], dtype=torch.int64, device=A.device)
+    out = torch.empty(4, dtype=torch.int64, device=A.device)
+    _lib.check(_lib.load().kp_length_stats(A.row_offsets.data_ptr(), A.off_type, A.n_rows + 1, out.data_ptr(),
+                                           reduce_workspace(A.device).data_ptr(), _lib.stream_handle()),
+               "kp_length_stats")
+    return out
+
+
+def select_sharded(model, A, world: int, n_rows: int, n_cols: int, nnz: int, k: int, group=None, out=None):
+    """Row-sharded seer-core.infer: local K1 partials -> one 32-byte all-gather ->
+    kp_seer_select_partials (exact combine + epilogue + trees) on every rank, so the
+    outcome equals the single-matrix selection.  Returns the device outcome buffer."""
+    import torch
+    import torch.distributed as tdist
+    from . import _lib
+    part = _length_partials(A)
+    if world > 1:
+        parts = torch.empty(4 * world, dtype=torch.int64, device=A.device)
+        tdist.all_gather_into_tensor(parts, part, group=group)
+    else:
+        parts = part
+    sel, kn, ga = model.device_trees(A.device)
+    if out is None:
+        out = torch.empty(_lib.OUTCOME_BYTES, dtype=torch.uint8, device=A.device)
+    _lib.check(_lib.load().kp_seer_select_partials(parts.data_ptr(), world, n_rows, n_cols, nnz, int(k),
+                                                   sel.data_ptr(), kn.data_ptr(), ga.data_ptr(), out.data_ptr(),
+                                                   _lib.stream_handle()), "kp_seer_select_partials")
+    return out
+
+
+class ShardedSeer:
+    """Row-sharded Seer + iterative SpMV (power iteration x <- A x) on this rank's block.
+
+    Setup: global selection from the ranks' partials (device), the chosen kernel's
+    preprocessing of the local block.  ``step(x_full_pad)``: the chosen kernel's
+    preprocessing (charged every step) + k x (local SpMV into this rank's
+    slice of the next x, in-place NCCL all-gather of the slices over NVLink)."""
+
+    def __init__(self, model, A, plan: ShardPlan, k: int, n_rows: int, n_cols: int, nnz: int, group=None):
+        import torch
+        from . import kernels
+        from .features import decode_outcome
+        self.A, self.plan, self.k, self.group = A, plan, int(k), group
+        self.outcome = decode_outcome(select_sharded(model, A, plan.world, n_rows, n_cols, nnz, k, group))
+        self.kernel = int(self.outcome.kernel)
+        dt = A.values.dtype
+        self.bufs = [torch.zeros(plan.world * plan.r_max, dtype=dt, device=A.device) for _ in range(2)]
+        self._kernels = kernels
+
+    def _slice(self, buf):
+        p = self.plan
+        return buf[p.rank * p.r_max: p.rank * p.r_max + p.local_rows]
+
+    def step(self, x_pad=None):
+        """One timed unit: prep + k iterations; returns the final padded x buffer."""
+        import torch.distributed as tdist
+        K = self._kernels
+        p = self.plan
+        if x_pad is not None:
+            self.bufs[0].copy_(x_pad)
+        P = K.prepare(self.A, self.kernel, cache=False) if self.kernel in K.NEEDS_PREP else None
+        cur = 0
+        for _ in range(self.k):
+            nxt = 1 - cur
+            K.spmv(self.A, self.bufs[cur], self.kernel, y=self._slice(self.bufs[nxt]), prepared=P)
+            if p.world > 1:
+                tdist.all_gather_into_tensor(self.bufs[nxt], self.bufs[nxt][p.rank * p.r_max:(p.rank + 1) * p.r_max],
+                                             group=self.group)
+            cur = nxt
+        return self.bufs[cur]

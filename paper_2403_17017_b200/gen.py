@@ -138,7 +138,9 @@ def rmat(scale: int, edge_factor: int = 16, abc=(0.57, 0.19, 0.19), seed: int = 
         rows_all.append(r)
         cols_all.append(cc)
     rows = torch.cat(rows_all)
+    del rows_all
     cols = torch.cat(cols_all)
+    del cols_all
     if permute:
         idx = torch.arange(n, dtype=torch.int64, device=device)
         prow = torch.argsort(hash2(seed + 1, idx))

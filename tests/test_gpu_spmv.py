@@ -122,3 +122,28 @@ def test_persistent_ranges_many_units_per_warp(warps, dtype, orc):
                 _check(m, A, kern, y, orc)
     finally:
         L.kp_debug_set_wave_warps(prev)
+
+
+def test_coo_misaligned_user_arrays(orc):
+    """kp_spmv on col / val pointers that are not 16-byte aligned (a caller's view into a
+    larger buffer): COO,WM takes its scalar-load path instead of faulting."""
+    import ctypes
+    from paper_2403_17017_b200 import _lib
+    m = gen.config("C2", small=True)
+    A = m.to_device_csr(torch.float32)
+    colb = torch.empty(A.nnz + 1, dtype=torch.int32, device="cuda")
+    valb = torch.empty(A.nnz + 1, dtype=torch.float32, device="cuda")
+    colb[1:].copy_(A.col_indices)
+    valb[1:].copy_(A.values)
+    st = _lib.kp_csr(A.n_rows, A.n_cols, A.nnz, A.off_type, A.val_type, A.row_offsets.data_ptr(),
+                     colb[1:].data_ptr(), valb[1:].data_ptr())
+    x = (torch.rand(A.n_cols, dtype=torch.float64) * 2 - 1).float().cuda()
+    P = kernels.prepare(A, kernels.COO_WM, cache=False)
+    ws = kernels.spmv_workspace(A, kernels.COO_WM)
+    y = torch.empty(A.n_rows, dtype=torch.float32, device="cuda")
+    _lib.check(_lib.load().kp_spmv(kernels.COO_WM, ctypes.byref(st), ctypes.byref(P.struct), x.data_ptr(),
+                                   y.data_ptr(), ws.data_ptr(), ws.numel(), _lib.stream_handle()), "kp_spmv")
+    torch.cuda.synchronize()
+    off, col, val = A.to_host()
+    yref, absy = orc.spmv_csr(off, col, val, x.cpu().numpy())
+    assert orc.spmv_check(y.cpu().numpy(), yref, absy, 1e-5)[0]

@@ -94,6 +94,7 @@ def corpus(quick: bool, extra: int = 400):
             C.append(("skewed", dict(n_rows=R, n_dense=nd, dense_len=dl, seed=sd)))
         else:
             C.append(("stencil", dict(n=int(lu(8, 170)))))
+    C += large_tier()
     if quick:
         C = C[::6]
     uniq, seen = [], set()  # random draws can repeat a grid point (e.g. a stencil size)
@@ -103,6 +104,20 @@ def corpus(quick: bool, extra: int = 400):
             seen.add(key)
             uniq.append((fam, p))
     return uniq
+
+
+def large_tier():
+    """134M - 1.07B nnz (BASELINE C5 scale), so the trees do not extrapolate there."""
+    C = [("rmat", dict(scale=sc, edge_factor=ef, seed=sc * 7 + ef))
+         for sc, ef in ((23, 16), (24, 8), (24, 16), (25, 8), (25, 16), (26, 8), (26, 16))]
+    C += [("uniform", dict(n_rows=32_000_000, n_cols=32_000_000, n_pairs=512_000_000, seed=77)),
+          ("const", dict(n_rows=64_000_000, length=8, seed=78)),
+          ("band", dict(n_rows=16_000_000, width=27)),
+          ("band", dict(n_rows=64_000_000, width=7)),
+          ("stencil", dict(n=280)),
+          ("powerlaw", dict(n_rows=32_000_000, mean=16.0, alpha=1.5, seed=79)),
+          ("skewed", dict(n_rows=16_000_000, n_dense=16, dense_len=4_000_000, seed=80))]
+    return C
 
 
 def build(fam, p, dev):
@@ -130,6 +145,7 @@ def main():
     ap.add_argument("--extra", type=int, default=400, help="seeded random draws on top of the grid")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cap-ms", type=float, default=40.0)
+    ap.add_argument("--only-large", action="store_true", help="only the large tier (append to a corpus)")
     a = ap.parse_args()
     os.makedirs(a.out, exist_ok=True)
     dev = torch.device("cuda", 0)
@@ -137,7 +153,7 @@ def main():
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     rows_el, rows_pp, rows_md, rows_kn = [], [], [], []
     t_start = time.time()
-    for fam, p in corpus(a.quick, a.extra):
+    for fam, p in (large_tier() if a.only_large else corpus(a.quick, a.extra)):
         m = build(fam, p, dev)
         name = fam + "_" + "_".join(f"{k}{v}" for k, v in p.items())
         A = m.to_device_csr(torch.float32, device=dev)

@@ -32,6 +32,7 @@ MATS = {
     "band2k": lambda d: (gen.banded(65_536, 2048, device=d), torch.float32),
     "pl": lambda d: (gen.powerlaw_rows(4_000_000, 16.0, 1.5, device=d), torch.float32),
     "const32": lambda d: (gen.constant_rows(4_000_000, 32, device=d), torch.float32),
+    "C5": lambda d: (gen.config("C5", device=d), torch.float32),
 }
 
 
