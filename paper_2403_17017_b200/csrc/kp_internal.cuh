@@ -79,6 +79,9 @@ __device__ __forceinline__ longlong2 ld_stream2ll(const longlong2 *p) {
                  : "=l"(r.x), "=l"(r.y) : "l"(p));
     return r;
 }
+__device__ __forceinline__ void prefetch_l2(const void *p) {
+    asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 // x gathers: read-only path, L1-allocating (reuse across rows / lanes).
 template <typename T>
 __device__ __forceinline__ T ld_x(const T *p) { return __ldg(p); }

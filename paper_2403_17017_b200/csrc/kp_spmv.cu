@@ -280,13 +280,28 @@ __global__ void __launch_bounds__(256) k_ell_tm(const PrepHeader *__restrict__ h
     const int64_t slab = (row >> 5) * 32 * W + (row & 31);
     const int32_t *pc = ecol + slab;
     const V *pv = evalv + slab;
+    // software pipeline: slots k+8..k+15 are loading while slots k..k+7 gather x
+    int32_t nc[8];
+    V nv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        nc[i] = i < W ? ld_stream(pc + i * 32) : 0;
+        nv[i] = i < W ? ld_stream(pv + i * 32) : V(0);
+    }
     for (int64_t k = 0; k < W; k += 8) {
         int32_t c[8];
         V v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-            c[i] = k + i < W ? ld_stream(pc + (k + i) * 32) : 0;
-            v[i] = k + i < W ? ld_stream(pv + (k + i) * 32) : V(0);
+            c[i] = nc[i];
+            v[i] = nv[i];
+        }
+        if (k + 8 < W) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                nc[i] = k + 8 + i < W ? ld_stream(pc + (k + 8 + i) * 32) : 0;
+                nv[i] = k + 8 + i < W ? ld_stream(pv + (k + 8 + i) * 32) : V(0);
+            }
         }
 #pragma unroll
         for (int i = 0; i < 8; ++i)
@@ -578,6 +593,15 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
             re = rr < n_rows ? ldo(off + rr + 1) : INT64_MAX / 2;
         }
         const int nz = (int)((d1 - d0) - nr);
+        if (nr == 0) {
+            // the whole unit is one row's elements (long rows): no row ends, no marks, no
+            // scans -- lane sums + a shuffle tree into the running carry (fixed order)
+            V sum = V(0);
+#pragma unroll
+            for (int t = 0; t < kIPT; ++t) sum += (lane + t * 32 < nz) ? p[t] : V(0);
+            carry += group_sum<32>(sum);
+            continue;
+        }
         if (lane == 0) rowv[nr] = V(0);  // open row: partial stays 0 unless it has elements here
         // stage products (positions >= nz belong to the next unit: zero)
 #pragma unroll
