@@ -139,7 +139,7 @@ constexpr int kTmStages = 3;
 constexpr int kTmMaxRpt = 4;
 template <typename V, typename O>
 struct TmCfg {
-    static constexpr int kCap = sizeof(V) == 4 ? 4096 : 2048;                    // nnz per stage
+    static constexpr int kCap = sizeof(V) == 4 ? 2048 : 1024;                    // nnz per stage
     static constexpr int kOffs = kTmRows * kTmMaxRpt + 8;                          // offsets per stage
     static constexpr size_t kOffBytes = (kOffs * sizeof(O) + 127) / 128 * 128;
     static constexpr size_t kColBytes = (size_t)kCap * 4;
