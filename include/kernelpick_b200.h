@@ -193,6 +193,20 @@ KP_API int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_
 KP_API int kp_seer_plan_launch(kp_seer_plan *plan, void *stream);
 KP_API int kp_seer_plan_destroy(kp_seer_plan *plan);
 
+/* ------------------------------------------------------------ canonicalisation (COO -> CSR) */
+/* Scratch bytes kp_csr_from_coo needs for n triples (n < 2^31). */
+KP_API int kp_coo_workspace_bytes(int64_t n, int64_t n_rows, int64_t n_cols, size_t *bytes);
+/* sparse.csr_from_coo (sparse.py:87-103) on the device: stable sort of the triples by
+ * (row, col) (np.lexsort), duplicates summed exactly as np.add.reduceat does (first value +
+ * numpy pairwise sum of the rest, input order), offsets from the per-row counts.
+ * d_rows / d_cols int64[n], d_vals f64[n]; outputs d_off int64[n_rows+1], d_col int32[<= n],
+ * d_val f64[<= n] and d_out2 (device int64[2]) = {nnz, number of out-of-range triples}
+ * (the caller rejects the result when the second is non-zero). */
+KP_API int kp_csr_from_coo(int64_t n_rows, int64_t n_cols, const int64_t *d_rows,
+                           const int64_t *d_cols, const double *d_vals, int64_t n, int64_t *d_off,
+                           int32_t *d_col, double *d_val, int64_t *d_out2, void *d_ws,
+                           size_t ws_bytes, void *stream);
+
 /* ------------------------------------------------------------ multi-GPU (K14) */
 /* nnz-balanced row cut: d_cuts[p] = lower_bound(row_offsets, p*nnz/parts), p = 0..parts
  * (d_cuts[parts] = n_rows). */

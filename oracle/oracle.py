@@ -13,6 +13,8 @@ Every function cites the reference file:line (or SPEC.md line) it restates:
   PARITY UNPINNED: the reference ships no SpMV.
 * tree_predict / infer / total_cost / fastest_kernel -- SPEC.md:296-301, 376-384,
   205-222.  PARITY UNPINNED: the reference ships no tree code.
+* csr_from_coo -- sparse.py:87-103 (lexsort, np.add.reduceat, bincount + cumsum);
+  pinned by tests/golden/reference_coo_golden.json (bit-exact values).
 
 The C restatement (kp_oracle.c -> liboracle.so) carries the O(nnz) loops; the
 numpy forms below are the small-case cross-checks.  ``ref_core()`` loads the
@@ -181,6 +183,26 @@ def spmv_check(y_dev, y_ref, absy, tol: float) -> tuple[bool, float]:
     bound = tol * absy + np.finfo(np.float64).tiny
     ratio = float(np.max(err / bound)) if err.size else 0.0
     return bool(np.all(err <= bound)), ratio
+
+
+# --------------------------------------------------------------------------- COO -> CSR
+def csr_from_coo(n_rows: int, n_cols: int, rows, cols, vals):
+    """sparse.py:87-103 restated: (row_offsets int64, col_indices int64, values f64)."""
+    r = np.asarray(rows, dtype=np.int64)
+    c = np.asarray(cols, dtype=np.int64)
+    v = np.asarray(vals, dtype=np.float64)
+    order = np.lexsort((c, r))  # stable: duplicates keep input order (sparse.py:92)
+    r, c, v = r[order], c[order], v[order]
+    if r.size:
+        first = np.empty(r.size, dtype=bool)
+        first[0] = True
+        first[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+        starts = np.flatnonzero(first)
+        v = np.add.reduceat(v, starts)  # per run: v0 + numpy pairwise sum of the rest
+        r, c = r[starts], c[starts]
+    off = np.zeros(n_rows + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=n_rows), out=off[1:])
+    return off, c, v
 
 
 def threads() -> int:

@@ -26,7 +26,7 @@ EXPORTS = (
     "kp_tree_predict", "kp_seer_select", "kp_prepare_bytes", "kp_prepare",
     "kp_spmv_workspace_bytes", "kp_spmv", "kp_seer_plan_bytes", "kp_seer_plan_create", "kp_seer_plan_launch",
     "kp_seer_plan_destroy", "kp_shard_partition", "kp_version", "kp_launch_count", "kp_debug_set_wave_warps",
-    "kp_seer_select_partials",
+    "kp_seer_select_partials", "kp_coo_workspace_bytes", "kp_csr_from_coo",
 )
 
 
@@ -95,6 +95,8 @@ def load(require: bool = True):
         "kp_launch_count": (ctypes.c_uint64, []),
         "kp_debug_set_wave_warps": (ctypes.c_int64, [i64]),
         "kp_seer_select_partials": (ctypes.c_int, [p, i32, i64, i64, i64, i64, p, p, p, p, p]),
+        "kp_coo_workspace_bytes": (ctypes.c_int, [i64, i64, i64, P(sz)]),
+        "kp_csr_from_coo": (ctypes.c_int, [i64, i64, p, p, p, i64, p, p, p, p, p, sz, p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

@@ -70,3 +70,22 @@ def test_cpu_spmv_oracle_matches_dense(orc):
     assert np.all(a >= np.abs(y) - 1e-12)
     y32 = orc.spmv_native(off.astype(np.int32), cols.astype(np.int32), vals.astype(np.float32), x.astype(np.float32))
     assert np.allclose(y32, dense @ x, atol=1e-5)
+
+
+def test_csr_from_coo_oracle_matches_reference_golden():
+    """oracle.csr_from_coo == the UNMODIFIED reference's csr_from_coo, bit for bit."""
+    import json
+    import os
+    import sys
+    import numpy as np
+    from oracle import oracle as orc
+    here = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+    sys.path.insert(0, here)
+    from make_golden_coo import coo_case
+    doc = json.load(open(os.path.join(here, "reference_coo_golden.json")))
+    for case in doc["cases"]:
+        R, C, rows, cols, vals = coo_case(case["spec"])
+        off, col, val = orc.csr_from_coo(R, C, rows, cols, vals)
+        assert off.tolist() == case["row_offsets"], case["spec"]["name"]
+        assert col.tolist() == case["col_indices"], case["spec"]["name"]
+        assert [float(v).hex() for v in val] == case["values"], case["spec"]["name"]
