@@ -60,6 +60,8 @@ def _args():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--exchange", default="auto", choices=["auto", "fused", "nccl"],
+                    help="C5: y exchange (fused epilogue stores over NVLink, or NCCL all-gather)")
     return ap.parse_args()
 
 
@@ -550,6 +552,14 @@ def run_sharded(a):
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:  # a 1-rank group so the fused exchange (symmetric memory) runs the N-rank code path
+        import socket
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     L = _lib.load()
     k_default, dt_name, desc = CFG["C5"]
@@ -563,7 +573,7 @@ def run_sharded(a):
     torch.cuda.empty_cache()
     t_gen = time.time() - t0
     model, model_src = _load_model()
-    run = kdist.ShardedSeer(model, A, plan, k, R, C, Z)
+    run = kdist.ShardedSeer(model, A, plan, k, R, C, Z, exchange=a.exchange)
     kern = run.kernel
     x0 = torch.full((world * plan.r_max,), 1.0 / R, dtype=dtype, device=dev)
     sv, so = 4 if dtype == torch.float32 else 8, 4
@@ -593,7 +603,7 @@ def run_sharded(a):
         total = float(tt.item())
     # this rank's SpMV alone (dominant kernel) for the roofline
     P = kernels.prepare(A, kern) if kern in kernels.NEEDS_PREP else None
-    ys = run.bufs[1][plan.rank * plan.r_max: plan.rank * plan.r_max + plan.local_rows]
+    ys = torch.empty(plan.local_rows, dtype=dtype, device=dev)
     ts = []
     for _ in range(5):
         m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -620,15 +630,17 @@ def run_sharded(a):
                        "byte_model": "nnz*(4+sv)+(R+1)*so+C*sv+R*sv per iteration, x counted once",
                        "generation_s": round(t_gen, 1)},
             "seer": {"kernel": kernels.KERNELS[kern], "path": "gathered" if run.outcome.path else "known",
-                     "dispatch": "global selection from the ranks' K1 partials at setup (device)"},
+                     "dispatch": "global selection from the ranks' K1 partials at setup (device)",
+                     "exchange": ("fused: SpMV epilogue stores y into every rank's next x over NVLink "
+                                  "(symmetric memory, kp_spmv_bcast) + device barrier" if run.exchange == "fused"
+                                  else "NCCL in-place all-gather of y after each SpMV")},
             "roofline": {"bound": "hbm", "achieved": round(kb / per / 1e9, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(kb / per / 1e9 / peak, 4), "traffic": None, "kernel": kernels.KERNELS[kern],
                          "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
                          "note": "rank 0's local SpMV"},
             "e2e": None, "gpu_launches": int(launches), "cpu_baseline": None, "clocks": clk,
         }), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
+    dist.destroy_process_group()
 
 
 def main():

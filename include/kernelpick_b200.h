@@ -58,6 +58,7 @@ extern "C" {
 #define KP_COO_WM 6
 #define KP_ELL_TM 7
 #define KP_NUM_KERNELS 8
+#define KP_MAX_PEERS 8
 
 /* Seer path. */
 #define KP_USE_KNOWN 0
@@ -172,6 +173,22 @@ KP_API int kp_spmv_workspace_bytes(int32_t kernel, const kp_csr *A, size_t *byte
  * identical bits. */
 KP_API int kp_spmv(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x,
             void *d_y, void *d_ws, size_t ws_bytes, void *stream);
+
+/* Fused row-sharded exchange: destinations of a rank's y slice.  y[p] = this rank's slice
+ * inside rank p's next-x buffer (device pointers valid in this process: NVLink peer / NVLS
+ * mappings of a symmetric allocation, or plain local buffers); y[self] is this rank's own
+ * copy.  n <= KP_MAX_PEERS. */
+typedef struct kp_peers {
+    void *y[KP_MAX_PEERS];
+    int32_t n, self;
+} kp_peers;
+/* kp_spmv whose y stores go to every destination in `peers` from the kernel's own epilogue
+ * (and its carry fix-up), replacing the y all-gather of a row-sharded iteration (SURVEY
+ * 8e) -- the transfer overlaps the SpMV tile by tile.  The caller orders the next read of x
+ * after a cross-rank barrier.  Merge-path kernels (KP_CSR_MP, KP_CSR_WO); other kernels
+ * return KP_EINVAL (use kp_spmv + an all-gather). */
+KP_API int kp_spmv_bcast(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x,
+                         const kp_peers *peers, void *d_ws, size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------ Seer plan (one CUDA graph) */
 /* The whole pipeline -- kp_seer_select, then the chosen kernel's kp_prepare and

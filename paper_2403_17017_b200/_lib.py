@@ -26,7 +26,7 @@ EXPORTS = (
     "kp_tree_predict", "kp_seer_select", "kp_prepare_bytes", "kp_prepare",
     "kp_spmv_workspace_bytes", "kp_spmv", "kp_seer_plan_bytes", "kp_seer_plan_create", "kp_seer_plan_launch",
     "kp_seer_plan_destroy", "kp_shard_partition", "kp_version", "kp_launch_count", "kp_debug_set_wave_warps",
-    "kp_seer_select_partials", "kp_coo_workspace_bytes", "kp_csr_from_coo",
+    "kp_seer_select_partials", "kp_coo_workspace_bytes", "kp_csr_from_coo", "kp_spmv_bcast",
 )
 
 
@@ -55,6 +55,13 @@ class kp_outcome(ctypes.Structure):
 class kp_prepared(ctypes.Structure):
     _fields_ = [("kernel", ctypes.c_int32), ("group", ctypes.c_int32), ("n_units", ctypes.c_int64),
                 ("ell_cap", ctypes.c_int64), ("buf", ctypes.c_void_p), ("bytes", ctypes.c_size_t)]
+
+
+KP_MAX_PEERS = 8
+
+
+class kp_peers(ctypes.Structure):
+    _fields_ = [("y", ctypes.c_void_p * KP_MAX_PEERS), ("n", ctypes.c_int32), ("self", ctypes.c_int32)]
 
 
 OUTCOME_BYTES = ctypes.sizeof(kp_outcome)  # 96
@@ -97,6 +104,7 @@ def load(require: bool = True):
         "kp_seer_select_partials": (ctypes.c_int, [p, i32, i64, i64, i64, i64, p, p, p, p, p]),
         "kp_coo_workspace_bytes": (ctypes.c_int, [i64, i64, i64, P(sz)]),
         "kp_csr_from_coo": (ctypes.c_int, [i64, i64, p, p, p, i64, p, p, p, p, p, sz, p]),
+        "kp_spmv_bcast": (ctypes.c_int, [i32, P(kp_csr), P(kp_prepared), p, P(kp_peers), p, sz, p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

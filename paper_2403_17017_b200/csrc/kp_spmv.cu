@@ -57,6 +57,19 @@ constexpr int64_t kAdLongChunk = 8192;    // adaptive: nnz per long-row piece
 template <typename V>
 __device__ __forceinline__ V fma_acc(V acc, V a, V b) { return fma(a, b, acc); }
 
+// Fused row-sharded exchange (kp_spmv_bcast): the SpMV's y stores go straight to every
+// rank's next-x buffer (this rank's slice of it) through NVLink peer mappings, so no
+// separate all-gather runs after the kernel.  y[self] is the local copy the fix-up reads.
+template <typename V>
+struct YDst {
+    V *y[KP_MAX_PEERS];
+    int32_t n, self;
+    __device__ __forceinline__ void put(int64_t i, V v) const {
+#pragma unroll 1
+        for (int p = 0; p < n; ++p) y[p][i] = v;
+    }
+};
+
 // ================================================================= CSR,WM (K4)
 // Predicated batch of U strided elements: all U (col, val) loads are issued before the
 // first x gather, so a lane keeps 2U + U requests in flight instead of one chain.
@@ -391,10 +404,10 @@ __device__ __forceinline__ SegPair<V> block_seg_exscan(SegPair<V> p, SegPair<V> 
 // continues past the warp's 32 units is finished by the warp where it STARTED, which
 // walks the following units 32 at a time (lane-strided sum + shuffle tree); warps whose
 // first run started earlier skip it.  Deterministic, no atomics.
-template <typename V>
+template <typename V, bool kB = false>
 __global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__ crow, const V *__restrict__ cval,
                                                      const int64_t *__restrict__ n_units_dev, int64_t n_units_host,
-                                                     V *__restrict__ y) {
+                                                     V *__restrict__ y, YDst<V> dst = YDst<V>{}) {
     const int64_t n_units = n_units_dev ? *n_units_dev : n_units_host;
     const int lane = threadIdx.x & 31;
     const int64_t wbase = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
@@ -419,7 +432,10 @@ __global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__
     const unsigned below = heads & ((lane == 31) ? 0xffffffffu : ((2u << lane) - 1u));
     const bool started_here = below != 0;  // a head at or before this lane within the warp
     const bool run_end_here = next != r;
-    if (r >= 0 && started_here && run_end_here) y[r] += inc.v;
+    if (r >= 0 && started_here && run_end_here) {
+        if constexpr (kB) dst.put(r, dst.y[dst.self][r] + inc.v);
+        else y[r] += inc.v;
+    }
     // run open at the warp end that started in this warp: continue over later units
     const bool cont = (lane == 31) && r >= 0 && started_here && !run_end_here;
     if (__ballot_sync(0xffffffffu, cont)) {
@@ -446,7 +462,10 @@ __global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__
             if (!open) break;  // the run ended inside this trip
         }
         acc = group_sum<32>(acc);
-        if (lane == 31) y[rho] += inc.v + acc;
+        if (lane == 31) {
+            if constexpr (kB) dst.put(rho, dst.y[dst.self][rho] + (inc.v + acc));
+            else y[rho] += inc.v + acc;
+        }
     }
 }
 
@@ -514,11 +533,11 @@ constexpr int kMergeWarps = 8;        // warps per CTA
 // row end marks its relative end position (atomicMax of tag<<9 | k+1, the tag = unit
 // counter makes stale marks of earlier units lose, so nothing is cleared), a max-scan
 // gives every position its row, and a thread-local + warp segmented scan sums rows.
-template <typename V, typename O, bool kPrep>
+template <typename V, typename O, bool kPrep, bool kB = false>
 __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     const O *__restrict__ off, const int32_t *__restrict__ col, const V *__restrict__ val, const V *__restrict__ x,
     V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, int64_t upw, int64_t n_ranges,
-    const int64_t *__restrict__ part, int32_t *__restrict__ crow, V *__restrict__ cval) {
+    const int64_t *__restrict__ part, int32_t *__restrict__ crow, V *__restrict__ cval, YDst<V> dst = YDst<V>{}) {
     constexpr int kPad = kWarpTile + kWarpTile / 32;
     __shared__ V s_prod[kMergeWarps][kPad];
     __shared__ int32_t s_mark[kMergeWarps][kPad];
@@ -670,7 +689,10 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
         }
         __syncwarp();
         // finished rows r0 .. r0+nr-1: coalesced stores; the open row's partial is the carry
-        for (int k = lane; k < nr; k += 32) y[r0 + k] = rowv[k];
+        for (int k = lane; k < nr; k += 32) {
+            if constexpr (kB) dst.put(r0 + k, rowv[k]);
+            else y[r0 + k] = rowv[k];
+        }
         carry = rowv[nr];
         r0 += nr;
         row_start = prev_re;
@@ -1357,7 +1379,7 @@ int tm_attrs() {
 
 template <typename V, typename O>
 int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V *y, unsigned char *ws,
-           cudaStream_t s) {
+           cudaStream_t s, const kp_peers *peers = nullptr) {
     const O *off = reinterpret_cast<const O *>(A->row_offsets);
     const int32_t *col = A->col_indices;
     const V *val = reinterpret_cast<const V *>(A->values);
@@ -1437,6 +1459,27 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
         case KP_CSR_WO: {
             const MergeGeom G = merge_geom<V, O>(A);
             const unsigned g = (unsigned)((G.n_ranges + kMergeWarps - 1) / kMergeWarps);
+            if (peers) {  // fused exchange: y stores to every rank's next-x slice
+                YDst<V> d{};
+                for (int p = 0; p < peers->n; ++p) d.y[p] = reinterpret_cast<V *>(peers->y[p]);
+                d.n = peers->n;
+                d.self = peers->self;
+                const int64_t *part = nullptr;
+                if (kernel == KP_CSR_MP) {
+                    if (!P || !P->buf) return KP_EINVAL;
+                    part = reinterpret_cast<const int64_t *>((unsigned char *)P->buf + prep_layout(KP_CSR_MP, A, 0).a);
+                    k_csr_merge<V, O, true, true><<<g, kMergeWarps * 32, 0, s>>>(
+                        off, col, val, x, d.y[d.self], R, Z, G.n_units, G.upw, G.n_ranges, part, crow, cval, d);
+                } else {
+                    k_csr_merge<V, O, false, true><<<g, kMergeWarps * 32, 0, s>>>(
+                        off, col, val, x, d.y[d.self], R, Z, G.n_units, G.upw, G.n_ranges, nullptr, crow, cval, d);
+                }
+                KP_LAUNCHED();
+                k_carry_fixup<V, true><<<(unsigned)((G.n_ranges * 32 + 255) / 256), 256, 0, s>>>(
+                    crow, cval, nullptr, G.n_ranges, d.y[d.self], d);
+                KP_LAUNCHED();
+                return KP_OK;
+            }
             if (kernel == KP_CSR_MP) {
                 if (!P || !P->buf) return KP_EINVAL;
                 const Layout L = prep_layout(KP_CSR_MP, A, 0);
@@ -1568,6 +1611,32 @@ int64_t kp_debug_set_wave_warps(int64_t warps) {
     const int64_t prev = g_wave_warps;
     g_wave_warps = warps > 0 ? warps : 0;
     return prev;
+}
+
+int kp_spmv_bcast(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x, const kp_peers *peers,
+                  void *d_ws, size_t ws_bytes, void *stream) {
+    if (!valid_csr(A) || !peers || peers->n < 1 || peers->n > KP_MAX_PEERS || peers->self < 0 ||
+        peers->self >= peers->n || (kernel != KP_CSR_MP && kernel != KP_CSR_WO) || (A->n_cols > 0 && !d_x))
+        return KP_EINVAL;
+    for (int p = 0; p < peers->n; ++p)
+        if (!peers->y[p]) return KP_EINVAL;
+    size_t need = 0;
+    kp_spmv_workspace_bytes(kernel, A, &need);
+    if (ws_bytes < need || (need && !d_ws)) return KP_ENOMEM;
+    if (P && P->buf && P->kernel != kernel) return KP_EINVAL;
+    cudaStream_t s = (cudaStream_t)stream;
+    if (A->n_rows == 0) return KP_OK;
+    if (A->nnz == 0) {
+        for (int p = 0; p < peers->n; ++p)
+            KP_CUDA_TRY(cudaMemsetAsync(peers->y[p], 0, (size_t)A->n_rows * val_bytes(A), s));
+        return KP_OK;
+    }
+    unsigned char *ws = reinterpret_cast<unsigned char *>(d_ws);
+    if (A->val_type == KP_F32)
+        return A->off_type == KP_I32 ? spmv_t<float, int32_t>(kernel, A, P, (const float *)d_x, nullptr, ws, s, peers)
+                                     : spmv_t<float, int64_t>(kernel, A, P, (const float *)d_x, nullptr, ws, s, peers);
+    return A->off_type == KP_I32 ? spmv_t<double, int32_t>(kernel, A, P, (const double *)d_x, nullptr, ws, s, peers)
+                                 : spmv_t<double, int64_t>(kernel, A, P, (const double *)d_x, nullptr, ws, s, peers);
 }
 
 int kp_shard_partition(const void *d_off, int32_t off_type, int64_t n_rows, int32_t parts, int64_t *d_cuts,

@@ -223,16 +223,53 @@ class ShardedSeer:
     preprocessing (charged every step) + k x (local SpMV into this rank's
     slice of the next x, in-place NCCL all-gather of the slices over NVLink)."""
 
-    def __init__(self, model, A, plan: ShardPlan, k: int, n_rows: int, n_cols: int, nnz: int, group=None):
+    def __init__(self, model, A, plan: ShardPlan, k: int, n_rows: int, n_cols: int, nnz: int, group=None,
+                 exchange: str = "auto", kernel=None):
         import torch
         from . import kernels
         from .features import decode_outcome
         self.A, self.plan, self.k, self.group = A, plan, int(k), group
-        self.outcome = decode_outcome(select_sharded(model, A, plan.world, n_rows, n_cols, nnz, k, group))
-        self.kernel = int(self.outcome.kernel)
+        if kernel is None:  # Seer selection over the whole (sharded) matrix
+            self.outcome = decode_outcome(select_sharded(model, A, plan.world, n_rows, n_cols, nnz, k, group))
+            self.kernel = int(self.outcome.kernel)
+        else:  # a fixed kernel (the sweep's baselines)
+            self.outcome = None
+            self.kernel = kernels.kernel_index(kernel)
         dt = A.values.dtype
-        self.bufs = [torch.zeros(plan.world * plan.r_max, dtype=dt, device=A.device) for _ in range(2)]
         self._kernels = kernels
+        # exchange: "fused" = the SpMV epilogue stores y into every rank's next-x buffer over
+        # NVLink peer mappings of a symmetric allocation (kp_spmv_bcast) + a device-side
+        # barrier; "nccl" = local SpMV then an in-place all-gather.  "auto" = fused when the
+        # chosen kernel supports it and symmetric memory rendezvous works.
+        self.exchange = "nccl"
+        if exchange in ("auto", "fused") and self.kernel in (kernels.CSR_MP, kernels.CSR_WO):
+            try:
+                self._setup_fused(dt)
+                self.exchange = "fused"
+            except Exception as exc:  # no peer mappings / symm-mem backend: keep NCCL
+                if exchange == "fused":
+                    raise
+                self.fused_error = repr(exc)
+        if self.exchange == "nccl":
+            self.bufs = [torch.zeros(plan.world * plan.r_max, dtype=dt, device=A.device) for _ in range(2)]
+
+    def _setup_fused(self, dt):
+        import torch
+        import torch.distributed as tdist
+        import torch.distributed._symmetric_memory as symm
+        if not tdist.is_initialized():
+            raise RuntimeError("fused exchange needs an initialised process group")
+        p = self.plan
+        grp = self.group or tdist.group.WORLD
+        n = p.world * p.r_max
+        self.bufs = [symm.empty(n, dtype=dt, device=self.A.device) for _ in range(2)]
+        for b in self.bufs:
+            b.zero_()
+        self.hdl = [symm.rendezvous(b, grp.group_name) for b in self.bufs]
+        # dests[i][q] = this rank's slice inside rank q's buffer i (peer-mapped)
+        self.dests = [[h.get_buffer(q, (n,), dt)[p.rank * p.r_max: p.rank * p.r_max + p.local_rows]
+                       for q in range(p.world)] for h in self.hdl]
+        self.hdl[0].barrier(channel=0)
 
     def _slice(self, buf):
         p = self.plan
@@ -247,6 +284,17 @@ class ShardedSeer:
             self.bufs[0].copy_(x_pad)
         P = K.prepare(self.A, self.kernel, cache=False) if self.kernel in K.NEEDS_PREP else None
         cur = 0
+        if self.exchange == "fused":
+            if x_pad is not None:
+                self.hdl[0].barrier(channel=0)  # every rank's buffer 0 holds x before anyone reads
+            for _ in range(self.k):
+                nxt = 1 - cur
+                # y -> every rank's next-x slice from the kernel epilogue; the barrier orders
+                # all ranks' stores before the next iteration's reads (and frees buffer cur)
+                K.spmv_bcast(self.A, self.bufs[cur], self.kernel, self.dests[nxt], p.rank, prepared=P)
+                self.hdl[nxt].barrier(channel=0)
+                cur = nxt
+            return self.bufs[cur]
         for _ in range(self.k):
             nxt = 1 - cur
             K.spmv(self.A, self.bufs[cur], self.kernel, y=self._slice(self.bufs[nxt]), prepared=P)

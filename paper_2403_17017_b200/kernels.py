@@ -121,3 +121,30 @@ def spmv(A, x, kernel, *, y=None, prepared: Prepared | None = None, stream=None)
                              _lib.stream_handle(stream))
     _lib.check(rc, f"kp_spmv[{KERNELS[k]}]")
     return y
+
+
+def spmv_bcast(A, x, kernel, dests, self_index: int, *, prepared: Prepared | None = None, stream=None):
+    """kp_spmv_bcast: y = A.x written from the kernel's own epilogue into every tensor of
+    ``dests`` (this rank's slice of each rank's next-x buffer; peer-mapped symmetric memory
+    or local tensors), ``dests[self_index]`` being the local copy.  Merge-path kernels only."""
+    torch = _lib.require_cuda()
+    A = as_device(A)
+    k = kernel_index(kernel)
+    if k not in (CSR_MP, CSR_WO):
+        raise ValueError("fused exchange is implemented for the merge-path kernels (CSR,MP / CSR,WO)")
+    if not 1 <= len(dests) <= _lib.KP_MAX_PEERS or not 0 <= self_index < len(dests):
+        raise ValueError("1..8 destinations and a valid self index")
+    for d in dests:
+        if d.dtype != A.values.dtype or d.numel() < A.n_rows:
+            raise ValueError("each destination needs n_rows elements of the matrix value dtype")
+    if k in NEEDS_PREP and prepared is None:
+        prepared = prepare(A, k, stream=stream)
+    pe = _lib.kp_peers()
+    for i, d in enumerate(dests):
+        pe.y[i] = d.data_ptr()
+    pe.n, pe.self = len(dests), int(self_index)
+    ws = spmv_workspace(A, k)
+    P = ctypes.byref(prepared.struct) if prepared is not None else None
+    _lib.check(_lib.load().kp_spmv_bcast(k, ctypes.byref(A.struct), P, x.data_ptr(), ctypes.byref(pe),
+                                         0 if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
+                                         _lib.stream_handle(stream)), f"kp_spmv_bcast[{KERNELS[k]}]")

@@ -84,3 +84,65 @@ def test_sharded_seer_world1_power_iteration(orc):
     for _ in range(3):
         ref, _ = orc.spmv_csr(off, col.astype(np.int32), val, ref)
     assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("world", [2, 3, 8])
+@pytest.mark.parametrize("kern", [kernels.CSR_WO, kernels.CSR_MP])
+def test_fused_exchange_loopback(world, kern, orc):
+    """kp_spmv_bcast on one GPU with `world` simulated ranks: every rank's kernel stores its
+    y slice into ALL ranks' next-x buffers (distinct local tensors standing in for the peer
+    mappings); afterwards every buffer must hold the full next x (= the oracle's A.x)."""
+    from paper_2403_17017_b200 import _lib
+    L = _lib.load()
+    prev = L.kp_debug_set_wave_warps(7)  # many units per warp: range-end carries -> fix-up broadcast
+    try:
+        m = gen.config("C5", small=True, device="cuda")
+        off, col, val = m.numpy()
+        x = np.random.default_rng(11).uniform(0, 1, m.n_cols)
+        yref, absy = orc.spmv_csr(off, col.astype(np.int32), val, x)
+        shards = [kdist.shard_device(m.row_offsets, m.col_indices, m.values, m.n_cols, r, world, torch.float64)
+                  for r in range(world)]
+        plan0 = shards[0][1]
+        n = world * plan0.r_max
+        nxt = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(world)]
+        for r, (A, plan, _) in enumerate(shards):
+            xp = plan.pad(torch.from_numpy(x).cuda())
+            dests = [nxt[q][r * plan.r_max: r * plan.r_max + plan.local_rows] for q in range(world)]
+            kernels.spmv_bcast(A, xp, kern, dests, r)
+        torch.cuda.synchronize()
+        for q in range(world):
+            got = plan0.unpad(nxt[q]).cpu().numpy()
+            ok, ratio = orc.spmv_check(got, yref, absy, 1e-12)
+            assert ok, (world, q, ratio)
+    finally:
+        L.kp_debug_set_wave_warps(prev)
+
+
+def test_sharded_seer_fused_symmetric_memory_world1(orc):
+    """ShardedSeer with exchange="fused" through torch symmetric memory at world size 1
+    (the same code path as N ranks: symm-mem rendezvous, peer-mapped destinations,
+    device barrier), vs the oracle power iteration."""
+    import socket
+    import torch.distributed as tdist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    tdist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                             device_id=torch.device("cuda", 0))
+    try:
+        m = gen.config("C5", small=True, device="cuda")
+        A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, m.n_cols, 0, 1, torch.float64)
+        model = _model()
+        run = kdist.ShardedSeer(model, A, plan, 3, m.n_rows, m.n_cols, m.nnz, exchange="fused",
+                                kernel=kernels.CSR_WO)
+        assert run.exchange == "fused"
+        x0 = torch.full((m.n_rows,), 1.0 / m.n_rows, dtype=torch.float64, device="cuda")
+        got = run.step(x0).cpu().numpy()
+        off, col, val = m.numpy()
+        ref = x0.cpu().numpy()
+        for _ in range(3):
+            ref, _ = orc.spmv_csr(off, col.astype(np.int32), val, ref)
+        assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+    finally:
+        tdist.destroy_process_group()
