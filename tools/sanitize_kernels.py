@@ -11,6 +11,17 @@ import test_gpu_spmv as t  # noqa: E402
 from paper_2403_17017_b200 import kernels  # noqa: E402
 
 ks = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "0,1,2,3,4,5,6,7").split(",")]
+from paper_2403_17017_b200 import _lib, device  # noqa: E402
+import numpy as np  # noqa: E402
+# few resident warps -> many units per persistent warp (register carries, range fix-ups)
+_lib.load().kp_debug_set_wave_warps(int(os.environ.get("KP_WAVE_WARPS", "0")))
+# device csr_from_coo (radix sort, run sums, offsets) on a duplicate-heavy input
+rng = np.random.default_rng(1)
+n = 50000
+rows, cols = rng.integers(0, 300, n), rng.integers(0, 200, n)
+device.csr_from_coo(300, 200, rows, cols, rng.normal(size=n))
+torch.cuda.synchronize()
+print("csr_from_coo ok", flush=True)
 for m in t.mats():
     for dt in (torch.float32, torch.float64):
         A = m.to_device_csr(dt, index="int32")
