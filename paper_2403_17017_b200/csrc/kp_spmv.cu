@@ -60,6 +60,24 @@ __device__ __forceinline__ V fma_acc(V acc, V a, V b) { return fma(a, b, acc); }
 // Fused row-sharded exchange (kp_spmv_bcast): the SpMV's y stores go straight to every
 // rank's next-x buffer (this rank's slice of it) through NVLink peer mappings, so no
 // separate all-gather runs after the kernel.  y[self] is the local copy the fix-up reads.
+// Launch with programmatic stream serialization (PDL): the dependent kernel's CTAs are
+// scheduled while the previous kernel drains and block in griddepcontrol.wait, hiding the
+// launch gap between a SpMV and its carry fix-up (captured as a programmatic graph edge).
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(block);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 template <typename V>
 struct YDst {
     V *y[KP_MAX_PEERS];
@@ -408,6 +426,9 @@ template <typename V, bool kB = false>
 __global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__ crow, const V *__restrict__ cval,
                                                      const int64_t *__restrict__ n_units_dev, int64_t n_units_host,
                                                      V *__restrict__ y, YDst<V> dst = YDst<V>{}) {
+    // programmatic dependent launch: this grid may be resident before the producing SpMV
+    // grid finishes; wait here until its carries are complete and visible
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     const int64_t n_units = n_units_dev ? *n_units_dev : n_units_host;
     const int lane = threadIdx.x & 31;
     const int64_t wbase = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
@@ -1451,7 +1472,8 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
                 k_coo_wm<V, false><<<(unsigned)g, 256, 0, s>>>(rid, col, val, x, y, R, Z, G.n_units, G.upw, G.n_ranges,
                                                                crow, cval);
             KP_LAUNCHED();
-            k_carry_fixup<V><<<(unsigned)((G.n_ranges * 32 + 255) / 256), 256, 0, s>>>(crow, cval, nullptr, G.n_ranges, y);
+            KP_CUDA_TRY(launch_pdl(k_carry_fixup<V, false>, (unsigned)((G.n_ranges * 32 + 255) / 256), 256, s, crow,
+                                   cval, (const int64_t *)nullptr, G.n_ranges, y, YDst<V>{}));
             KP_LAUNCHED();
             return KP_OK;
         }
@@ -1491,7 +1513,8 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
                                                                          G.n_ranges, nullptr, crow, cval);
             }
             KP_LAUNCHED();
-            k_carry_fixup<V><<<(unsigned)((G.n_ranges * 32 + 255) / 256), 256, 0, s>>>(crow, cval, nullptr, G.n_ranges, y);
+            KP_CUDA_TRY(launch_pdl(k_carry_fixup<V, false>, (unsigned)((G.n_ranges * 32 + 255) / 256), 256, s, crow,
+                                   cval, (const int64_t *)nullptr, G.n_ranges, y, YDst<V>{}));
             KP_LAUNCHED();
             return KP_OK;
         }
