@@ -40,6 +40,7 @@ extern "C" {
 #define KP_ENOMEM (-3)      /* caller workspace too small                           */
 #define KP_EUNSUPPORTED (-4)
 #define KP_ERANGE (-5)      /* value outside the exactly-representable range        */
+#define KP_EPARSE (-6)      /* malformed input text (reference: ParseError)           */
 
 /* ---------------------------------------------------------------- type codes   */
 #define KP_I32 0
@@ -223,6 +224,26 @@ KP_API int kp_csr_from_coo(int64_t n_rows, int64_t n_cols, const int64_t *d_rows
                            const int64_t *d_cols, const double *d_vals, int64_t n, int64_t *d_off,
                            int32_t *d_col, double *d_val, int64_t *d_out2, void *d_ws,
                            size_t ws_bytes, void *stream);
+
+/* ------------------------------------------------------------ Matrix Market ingest (host) */
+/* sparse.parse_matrix_market (sparse.py:106-196): header / size line / entry grammar,
+ * checks and 1-based error lines as the reference (Python splitlines / strip / int / float
+ * semantics for ASCII text); symmetric and skew-symmetric storage mirrored right after each
+ * entry; pattern values 1.0.  Parallel native parse (OpenMP, n_threads <= 0: all). */
+typedef struct kp_mm_info {
+    int64_t n_rows, n_cols, n_entries;  /* size line                                  */
+    int64_t n_triples;                  /* triples after symmetric expansion          */
+    int32_t field;                      /* 0 real, 1 integer, 2 pattern               */
+    int32_t symmetry;                   /* 0 general, 1 symmetric, 2 skew-symmetric   */
+    int64_t err_line;                   /* KP_EPARSE: 1-based line of the first error */
+    char err[192];                      /* KP_EPARSE: the reference's message         */
+} kp_mm_info;
+/* Header + size line only (capacity planning: n_entries x (symmetry ? 2 : 1)). */
+KP_API int kp_mm_header(const char *buf, size_t len, kp_mm_info *info);
+/* Full parse into caller arrays (0-based int64 rows / cols, f64 values, input order);
+ * KP_ENOMEM with info->n_triples set when capacity is too small. */
+KP_API int kp_mm_parse(const char *buf, size_t len, int64_t *rows, int64_t *cols, double *vals,
+                       int64_t capacity, int32_t n_threads, kp_mm_info *info);
 
 /* ------------------------------------------------------------ multi-GPU (K14) */
 /* nnz-balanced row cut: d_cuts[p] = lower_bound(row_offsets, p*nnz/parts), p = 0..parts

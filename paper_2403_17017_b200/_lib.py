@@ -27,6 +27,7 @@ EXPORTS = (
     "kp_spmv_workspace_bytes", "kp_spmv", "kp_seer_plan_bytes", "kp_seer_plan_create", "kp_seer_plan_launch",
     "kp_seer_plan_destroy", "kp_shard_partition", "kp_version", "kp_launch_count", "kp_debug_set_wave_warps",
     "kp_seer_select_partials", "kp_coo_workspace_bytes", "kp_csr_from_coo", "kp_spmv_bcast",
+    "kp_mm_header", "kp_mm_parse",
 )
 
 
@@ -58,6 +59,13 @@ class kp_prepared(ctypes.Structure):
 
 
 KP_MAX_PEERS = 8
+KP_EPARSE = -6
+
+
+class kp_mm_info(ctypes.Structure):
+    _fields_ = [("n_rows", ctypes.c_int64), ("n_cols", ctypes.c_int64), ("n_entries", ctypes.c_int64),
+                ("n_triples", ctypes.c_int64), ("field", ctypes.c_int32), ("symmetry", ctypes.c_int32),
+                ("err_line", ctypes.c_int64), ("err", ctypes.c_char * 192)]
 
 
 class kp_peers(ctypes.Structure):
@@ -105,6 +113,8 @@ def load(require: bool = True):
         "kp_coo_workspace_bytes": (ctypes.c_int, [i64, i64, i64, P(sz)]),
         "kp_csr_from_coo": (ctypes.c_int, [i64, i64, p, p, p, i64, p, p, p, p, p, sz, p]),
         "kp_spmv_bcast": (ctypes.c_int, [i32, P(kp_csr), P(kp_prepared), p, P(kp_peers), p, sz, p]),
+        "kp_mm_header": (ctypes.c_int, [ctypes.c_char_p, sz, P(kp_mm_info)]),
+        "kp_mm_parse": (ctypes.c_int, [ctypes.c_char_p, sz, p, p, p, i64, i32, P(kp_mm_info)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

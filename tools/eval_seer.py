@@ -1,0 +1,164 @@
+"""Live end-to-end evaluation of the frozen Seer bundle on B200 (GPU): the paper's headline
+comparisons measured on real runs, not on the
+training tables.
+
+    python tools/eval_seer.py [--split test] [--iters 1,10] [--out profiles/seer_live_eval_r01.json]
+
+For every matrix of the held-out split (same seed as tools/train_seer.py) plus the BASELINE
+configs C1-C4: the Seer plan (kp_seer_plan: selection -> chosen preprocessing -> k SpMVs,
+one graph) and every fixed kernel's prep + k SpMVs (captured as a graph the same way) are
+timed with CUDA events, L2 flushed, median of --reps.  Kernels whose single SpMV exceeds
+--cap-ms are timed once and extrapolated (prep + k x t) -- they are never the best.
+Reported per k: per-matrix geomean of T_best_fixed_kernel / T_seer (the north star's "beats
+the best single fixed kernel in geomean"), aggregate T_best_fixed / T_seer (paper's 2x),
+geomean over kernels of T_K / T_seer (paper's 6.5x), T_seer / T_oracle, and selection
+agreement with the host restatement of the trees (bit-exact selection).
+"""
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "tools"))
+import torch  # noqa: E402
+
+import collect_corpus as cc  # noqa: E402
+from paper_2403_17017_b200 import dataset, features, gen, kernels, seer  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--split", default="test", choices=["test", "all"])
+    ap.add_argument("--iters", default="1,10")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--cap-ms", type=float, default=5.0)
+    ap.add_argument("--limit", type=int, default=0)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    iters = [int(v) for v in a.iters.split(",")]
+    model = seer.SeerModel.load(os.path.join(ROOT, "paper_2403_17017_b200", "models", "seer_b200.json"))
+    # the held-out split: same names / seed as tools/train_seer.py
+    import train_seer as ts
+    rows = ts.load(os.path.join(ROOT, "paper_2403_17017_b200", "models", "corpus"))
+    _, test = dataset.split_train_test(rows, 2403, 0.8)
+    names = {r.name for r in (rows if a.split == "all" else test)}
+    specs = []
+    for fam, p in cc.corpus(False) + cc.large_tier():
+        nm = fam + "_" + "_".join(f"{k}{v}" for k, v in p.items())
+        if nm in names:
+            specs.append((nm, fam, p))
+            names.discard(nm)
+    specs = sorted({s[0]: s for s in specs}.values())
+    if a.limit:
+        specs = specs[: a.limit]
+    specs += [("C1", "config", {}), ("C2", "config", {}), ("C3", "config", {}), ("C4", "config", {})]
+    dev = torch.device("cuda", 0)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def ev():
+        return torch.cuda.Event(enable_timing=True)
+
+    def t_graph(fn, reps):
+        fn()
+        cs = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cs):
+            fn()
+        g.replay()
+        torch.cuda.synchronize()
+        ts_ = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = ev(), ev()
+            e0.record()
+            g.replay()
+            e1.record()
+            e1.synchronize()
+            ts_.append(e0.elapsed_time(e1) * 1e-3)
+        del g
+        return statistics.median(ts_)
+
+    results = []
+    for nm, fam, p in specs:
+        m = gen.config(nm, device=dev) if fam == "config" else cc.build(fam, p, dev)
+        dt = torch.float64 if nm == "C4" else torch.float32
+        A = m.to_device_csr(dt, device=dev)
+        del m
+        x = (torch.rand(A.n_cols, device=dev, dtype=torch.float64) * 2 - 1).to(dt)
+        y = torch.empty(A.n_rows, device=dev, dtype=dt)
+        rec = {"name": nm, "rows": A.n_rows, "nnz": A.nnz, "k": {}}
+        # host restatement of the same trees on the device features: selection agreement
+        g = features.decode_outcome(features.gather_outcome(A))
+        single = {}
+        for kk in range(len(kernels.KERNELS)):
+            P = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
+            kernels.spmv(A, x, kk, y=y, prepared=P)
+            flush.zero_()
+            e0, e1 = ev(), ev()
+            e0.record()
+            kernels.spmv(A, x, kk, y=y, prepared=P)
+            e1.record()
+            e1.synchronize()
+            single[kk] = e0.elapsed_time(e1) * 1e-3
+            del P
+        for k in iters:
+            plan = seer.SeerPlan(model, A, x, y, k)
+            t_seer = t_graph(plan.launch, a.reps)
+            o = plan.outcome()
+            hk, hp = model.predict_host(A.n_rows, A.n_cols, A.nnz, k, [g.max_d, g.min_d, g.mean_d, g.var_d])
+            fixed = {}
+            for kk in range(len(kernels.KERNELS)):
+                if single[kk] * k * 1e3 > a.cap_ms * max(1, k) and single[kk] * 1e3 > a.cap_ms:
+                    fixed[kk] = single[kk] * (k + 1)  # slow kernel: extrapolated (never the best)
+                    continue
+
+                def step(kk=kk):
+                    P = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
+                    for _ in range(k):
+                        kernels.spmv(A, x, kk, y=y, prepared=P)
+                fixed[kk] = t_graph(step, a.reps)
+            rec["k"][str(k)] = {"seer_s": t_seer, "kernel": kernels.KERNELS[int(o.kernel)], "path": int(o.path),
+                                "host_kernel": kernels.KERNELS[hk], "host_path": hp,
+                                "fixed_s": {kernels.KERNELS[kk]: v for kk, v in fixed.items()}}
+            plan.close()
+        print(nm, {k: (v["kernel"], round(v["seer_s"] * 1e6, 1), round(min(v["fixed_s"].values()) * 1e6, 1))
+                   for k, v in rec["k"].items()}, flush=True)
+        results.append(rec)
+        del A, x, y
+        torch.cuda.empty_cache()
+
+    summary = {}
+    for k in iters:
+        ks = str(k)
+        recs = [r for r in results if ks in r["k"]]
+        tot = {K: sum(r["k"][ks]["fixed_s"][K] for r in recs) for K in kernels.KERNELS}
+        best_fixed = min(tot, key=tot.get)
+        seer_tot = sum(r["k"][ks]["seer_s"] for r in recs)
+        oracle_tot = sum(min(r["k"][ks]["fixed_s"].values()) for r in recs)
+        per = [r["k"][ks]["fixed_s"][best_fixed] / r["k"][ks]["seer_s"] for r in recs]
+        geo_k = [math.exp(sum(math.log(r["k"][ks]["fixed_s"][K] / r["k"][ks]["seer_s"]) for r in recs) / len(recs))
+                 for K in kernels.KERNELS]
+        agree = sum((r["k"][ks]["kernel"], r["k"][ks]["path"]) == (r["k"][ks]["host_kernel"], r["k"][ks]["host_path"])
+                    for r in recs)
+        summary[ks] = {
+            "matrices": len(recs), "best_fixed_kernel": best_fixed,
+            "per_matrix_geomean_vs_best_fixed": math.exp(sum(math.log(v) for v in per) / len(per)),
+            "aggregate_vs_best_fixed": tot[best_fixed] / seer_tot,
+            "geomean_over_kernels_of_aggregate_speedup": math.exp(sum(math.log(tot[K] / seer_tot) for K in kernels.KERNELS) / len(kernels.KERNELS)),
+            "geomean_over_kernels_of_per_matrix_geomean": math.exp(sum(math.log(v) for v in geo_k) / len(geo_k)),
+            "seer_over_oracle": seer_tot / oracle_tot,
+            "selection_agrees_with_host_restatement": f"{agree}/{len(recs)}",
+        }
+        print(ks, json.dumps(summary[ks]), flush=True)
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump({"split": a.split, "iters": iters, "summary": summary, "matrices": results}, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
