@@ -580,37 +580,44 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
     V carry = V(0);
     const int jb = lane * kIPT;
     int32_t tag = 0;
+    // software pipeline: unit u+1's (col, val) loads are issued as soon as unit u's row count
+    // fixes where they start, so their HBM latency overlaps unit u's gathers / scans
+    auto load_cv = [&](int64_t j0, int32_t (&c)[kIPT], V (&v)[kIPT]) {
+        if (j0 + kWarpTile <= nnz) {  // common case: unpredicated, immediate offsets
+            const int32_t *cp = col + j0 + lane;
+            const V *vp = val + j0 + lane;
+#pragma unroll
+            for (int t = 0; t < kIPT; ++t) {
+                c[t] = ld_stream(cp + t * 32);
+                v[t] = ld_stream(vp + t * 32);
+            }
+        } else {
+#pragma unroll
+            for (int t = 0; t < kIPT; ++t) {
+                const int64_t j = j0 + lane + t * 32;
+                c[t] = j < nnz ? ld_stream(col + j) : 0;
+                v[t] = j < nnz ? ld_stream(val + j) : V(0);
+            }
+        }
+    };
+    int32_t cn[kIPT];
+    V vn[kIPT];
+    if (u_begin < u_end) load_cv(u_begin * kWarpTile - r0, cn, vn);
     for (int64_t u = u_begin; u < u_end; ++u) {
         tag += 1 << 9;
         const int64_t d0 = u * kWarpTile;
         const int64_t d1 = d0 + kWarpTile < total ? d0 + kWarpTile : total;
         const int64_t j0 = d0 - r0;
-        // round 0 of the row-end probe + speculative nnz loads, all issued before use
+        // x gathers of this unit (loaded last iteration) + round 0 of the row-end probe
+        V p[kIPT];
+        V vv[kIPT];
+#pragma unroll
+        for (int t = 0; t < kIPT; ++t) {
+            vv[t] = vn[t];
+            p[t] = ld_x(x + cn[t]);
+        }
         int64_t rr = r0 + lane;
         int64_t re = rr < n_rows ? ldo(off + rr + 1) : INT64_MAX / 2;
-        V p[kIPT];
-        {
-            int32_t c[kIPT];
-            V v[kIPT];
-            if (j0 + kWarpTile <= nnz) {  // common case: unpredicated, immediate offsets
-                const int32_t *cp = col + j0 + lane;
-                const V *vp = val + j0 + lane;
-#pragma unroll
-                for (int t = 0; t < kIPT; ++t) {
-                    c[t] = ld_stream(cp + t * 32);
-                    v[t] = ld_stream(vp + t * 32);
-                }
-            } else {
-#pragma unroll
-                for (int t = 0; t < kIPT; ++t) {
-                    const int64_t j = j0 + lane + t * 32;
-                    c[t] = j < nnz ? ld_stream(col + j) : 0;
-                    v[t] = j < nnz ? ld_stream(val + j) : V(0);
-                }
-            }
-#pragma unroll
-            for (int t = 0; t < kIPT; ++t) p[t] = v[t] * ld_x(x + c[t]);
-        }
         // row ends inside the unit: q = re + rr < d1 (monotone in rr -> ballot + popc)
         int nr = 0;
         int64_t prev_re = row_start;  // end of the row before the probed one (off[rr])
@@ -618,8 +625,6 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
             const bool in = rr < n_rows && re + rr < d1;
             const unsigned m = __ballot_sync(0xffffffffu, in);
             const int cnt = __popc(m);
-            int64_t pre = __shfl_up_sync(0xffffffffu, re, 1);
-            if (lane == 0) pre = prev_re;
             if (in) {
                 const int k = nr + lane;  // row r0 + k; rows with elements here are overwritten by the scan
                 rowv[k] = k == 0 ? carry : V(0);
@@ -633,6 +638,9 @@ __global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
             re = rr < n_rows ? ldo(off + rr + 1) : INT64_MAX / 2;
         }
         const int nz = (int)((d1 - d0) - nr);
+        if (u + 1 < u_end) load_cv(d1 - (r0 + nr), cn, vn);
+#pragma unroll
+        for (int t = 0; t < kIPT; ++t) p[t] *= vv[t];
         if (nr == 0) {
             // the whole unit is one row's elements (long rows): no row ends, no marks, no
             // scans -- lane sums + a shuffle tree into the running carry (fixed order)
