@@ -200,7 +200,11 @@ class SeerPlan:
     launches).  ``launch()`` enqueues one graph launch on the current (or given) stream;
     ``outcome()`` reads the selection the last launch made."""
 
-    def __init__(self, model: SeerModel, A, x, y, k: int = 1, ell_cap: int | None = None):
+    def __init__(self, model: SeerModel, A, x, y, k: int = 1, ell_cap: int | None = None,
+                 force_gathered: bool = False):
+        """``force_gathered`` (measurement): replace the selector by a constant USE_GATHERED
+        leaf, so every launch runs the feature pass + gathered tree + SWITCH -- the realised
+        collection overhead the corpus charges to the gathered path."""
         import ctypes
         torch = _lib.require_cuda()
         from .device import as_device
@@ -219,6 +223,12 @@ class SeerPlan:
         self.red = torch.zeros(int(L.kp_reduce_workspace_bytes()), dtype=torch.uint8, device=dev)
         self.trees = model.device_trees(dev)
         sel, kn, ga = self.trees
+        if force_gathered:
+            import numpy as np
+            from .dtree import leaf_tree
+            raw = np.frombuffer(leaf_tree(USE_GATHERED, 2, 4).pack(), dtype=np.uint8).copy()
+            sel = torch.from_numpy(raw).to(dev)
+            self.trees = (sel, kn, ga)
         cap_stream = torch.cuda.Stream(device=dev)  # graph capture needs a created stream
         torch.cuda.synchronize(dev)
         handle = ctypes.c_void_p()

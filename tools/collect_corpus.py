@@ -5,8 +5,10 @@
 Writes the SPEC.md:246 artifact files into DIR:
   elapsed.csv     name + one column per kernel: seconds per SpMV iteration (median, L2 flushed)
   preprocess.csv  name + one column per kernel: seconds of one-time preprocessing (0 if none)
-  metadata.csv    name, max/min/mean/var density, collection_time (device time of the fused
-                  feature pass, kp_gather_features)
+  metadata.csv    name, max/min/mean/var density, collection_time = the realised overhead of
+                  the gathered path in the Seer plan (forced-gathered plan minus the same body
+                  as a plain graph: feature pass + tree + device SWITCH), or with --model ''
+                  the bare kp_gather_features time
   known.csv       name, rows, cols, nnz
 Times are CUDA-event device times on the launching stream (PAPER.md:331 uses 10 warm-ups +
 mean of 10; we use 2 warm-ups + median of 5, enough for ranking).  A kernel slower than
@@ -138,6 +140,48 @@ def build(fam, p, dev):
     raise ValueError(fam)
 
 
+def _plan_overhead(model, A, x, y, flush, ev, reps: int = 5):
+    """Realised cost of the gathered path inside the Seer plan: time of a plan forced onto
+    the gathered path (K1 feature pass + gathered tree + device SWITCH) minus the time of
+    the same chosen body (prep + 1 SpMV) as a plain graph.  This, not the bare feature
+    kernel, is what the selector must weigh against the known path."""
+    from paper_2403_17017_b200 import seer
+    plan = seer.SeerPlan(model, A, x, y, 1, force_gathered=True)
+    plan.launch()
+    torch.cuda.synchronize()
+    kern = int(plan.outcome().kernel)
+
+    def med(fn):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = ev(), ev()
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1) * 1e-3)
+        return statistics.median(ts)
+
+    t_plan = med(plan.launch)
+    plan.close()
+
+    def body():
+        P = kernels.prepare(A, kern, cache=False) if kern in kernels.NEEDS_PREP else None
+        kernels.spmv(A, x, kern, y=y, prepared=P)
+    body()
+    cs = torch.cuda.Stream()
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=cs):
+        body()
+    t_body = med(g.replay)
+    del g
+    return max(t_plan - t_body, 1e-6)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
@@ -146,12 +190,18 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--cap-ms", type=float, default=40.0)
     ap.add_argument("--only-large", action="store_true", help="only the large tier (append to a corpus)")
+    ap.add_argument("--model", default=os.path.join(ROOT, "paper_2403_17017_b200", "models", "seer_b200.json"),
+                    help="bundle whose gathered tree drives the plan-overhead measurement ('' = bare K1 time)")
     a = ap.parse_args()
     os.makedirs(a.out, exist_ok=True)
     dev = torch.device("cuda", 0)
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
     rows_el, rows_pp, rows_md, rows_kn = [], [], [], []
+    model = None
+    if a.model and os.path.exists(a.model):
+        from paper_2403_17017_b200 import seer
+        model = seer.SeerModel.load(a.model)
     t_start = time.time()
     for fam, p in (large_tier() if a.only_large else corpus(a.quick, a.extra)):
         m = build(fam, p, dev)
@@ -173,7 +223,10 @@ def main():
             e1.synchronize()
             cts.append(e0.elapsed_time(e1) * 1e-3)
         o = features.decode_outcome(buf)
-        rows_md.append([name, o.max_d, o.min_d, o.mean_d, o.var_d, statistics.median(cts)])
+        coll = statistics.median(cts)
+        if model is not None:
+            coll = _plan_overhead(model, A, x, y, flush, ev) or coll
+        rows_md.append([name, o.max_d, o.min_d, o.mean_d, o.var_d, coll])
         rows_kn.append([name, A.n_rows, A.n_cols, A.nnz])
         el, pp = [], []
         for k in range(len(kernels.KERNELS)):
