@@ -348,6 +348,7 @@ def run_ours(a):
             "metric": "Seer-selected SpMV GB/s (% HBM roofline) and geomean speedup vs best fixed kernel",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(total / a.steps * 1e3, 4), "higher_is_better": True, "scaling": "weak",
+            "gflops": round(world * a.steps * k * 2 * Z / total / 1e9, 2),
             "vs_baseline": None, "dtype": "f32" if dtype == torch.float32 else "f64",
             "data": "synthetic (counter-hash generated on device)",
             "config": {"workload": a.workload, "desc": desc, "rows": R, "cols": C, "nnz": Z, "iterations": k,
@@ -622,6 +623,7 @@ def run_sharded(a):
             "metric": "Seer-selected SpMV GB/s (% HBM roofline) and geomean speedup vs best fixed kernel",
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(total / a.steps * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "gflops": round(a.steps * k * 2 * Z / total / 1e9, 2),
             "vs_baseline": None, "dtype": "f32" if dtype == torch.float32 else "f64",
             "data": "synthetic (counter-hash R-MAT generated on device)",
             "config": {"workload": "C5", "desc": desc, "rows": R, "cols": C, "nnz": Z, "iterations": k,
