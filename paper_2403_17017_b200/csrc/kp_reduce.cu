@@ -151,7 +151,59 @@ __device__ __forceinline__ void stats_accum(const O *__restrict__ off, int64_t n
     const int lane = threadIdx.x & 31;
     const int64_t gwarp = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    if constexpr (kVec) {
+    if constexpr (kVec && sizeof(O) == 4) {
+        // int32 offsets (nnz < 2^31): lengths in 32 bits, Σlen² via one IMAD.WIDE.U32 per
+        // row; kH independent accumulator sets so no chain serialises the 16 rows of a trip
+        const int64_t nvec = n_rows / 4;
+        constexpr int kH = 4;
+        uint32_t l32[kH], h32[kH];
+        uint64_t q[kH];
+#pragma unroll
+        for (int h = 0; h < kH; ++h) { l32[h] = 0xffffffffu; h32[h] = 0; q[h] = 0; }
+        for (int64_t base = gwarp * (32 * kH); base < nvec; base += nwarps * (32 * kH)) {
+            int4 e[kH];
+            int32_t nx[kH];
+#pragma unroll
+            for (int h = 0; h < kH; ++h) {
+                const int64_t v = base + h * 32 + lane;
+                e[h] = v < nvec ? ld_stream4(reinterpret_cast<const int4 *>(off) + v) : make_int4(0, 0, 0, 0);
+                nx[h] = (v < nvec && (lane == 31 || v + 1 >= nvec)) ? __ldg(reinterpret_cast<const int32_t *>(off) + (v + 1) * 4) : 0;
+            }
+#pragma unroll
+            for (int h = 0; h < kH; ++h) {
+                const int64_t v = base + h * 32 + lane;
+                int32_t nxt = __shfl_down_sync(0xffffffffu, e[h].x, 1);
+                if (lane == 31 || v + 1 >= nvec) nxt = nx[h];
+                if (v < nvec) {
+                    if (e[h].y >= e[h].x && e[h].z >= e[h].y && e[h].w >= e[h].z && nxt >= e[h].w) {
+                        // non-decreasing (every valid CSR): lengths are exact as uint32
+                        const uint32_t u0 = (uint32_t)e[h].y - (uint32_t)e[h].x, u1 = (uint32_t)e[h].z - (uint32_t)e[h].y,
+                                       u2 = (uint32_t)e[h].w - (uint32_t)e[h].z, u3 = (uint32_t)nxt - (uint32_t)e[h].w;
+                        l32[h] = min(min(l32[h], u0), min(min(u1, u2), u3));
+                        h32[h] = max(max(h32[h], u0), max(max(u1, u2), u3));
+                        q[h] += (uint64_t)u0 * u0 + (uint64_t)u1 * u1 + (uint64_t)u2 * u2 + (uint64_t)u3 * u3;
+                    } else {  // arbitrary int32 arrays (the C-ABI accepts them): signed 64-bit lengths
+                        acc_len(e[h].x, e[h].y, lo, hi, s2);
+                        acc_len(e[h].y, e[h].z, lo, hi, s2);
+                        acc_len(e[h].z, e[h].w, lo, hi, s2);
+                        acc_len(e[h].w, nxt, lo, hi, s2);
+                    }
+                }
+            }
+        }
+#pragma unroll
+        for (int h = 0; h < kH; ++h) {
+            if (l32[h] != 0xffffffffu || h32[h] != 0 || q[h] != 0) {
+                lo = (int64_t)l32[h] < lo ? (int64_t)l32[h] : lo;
+                hi = (int64_t)h32[h] > hi ? (int64_t)h32[h] : hi;
+            }
+            s2 += q[h];
+        }
+        // scalar tail rows [nvec*4, n_rows)
+        const int64_t t0 = nvec * 4;
+        const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+        if (gt < n_rows - t0) acc_len(ldo(off + t0 + gt), ldo(off + t0 + gt + 1), lo, hi, s2);
+    } else if constexpr (kVec) {
         constexpr int V = Vec16<O>::V;
         const int64_t nvec = n_rows / V;  // vector v covers rows v*V .. v*V+V-1
         // kH independent 16-byte vectors per lane per iteration, plus (lane 31 / the last
@@ -506,7 +558,7 @@ __global__ void k_tree_predict(const void *tree, const double *__restrict__ x, i
 // ------------------------------------------------------------------ launch helpers
 int grid_for(int64_t n_rows, int per_thread) {
     int64_t want = (n_rows + (int64_t)kRedThreads * per_thread - 1) / ((int64_t)kRedThreads * per_thread);
-    int cap = num_sms() * 2;  // fewer, fuller CTAs: per-CTA fixed cost (ticket, reduce) amortised
+    int cap = num_sms() * 8;  // full occupancy for large inputs (bytes in flight); small inputs use few CTAs
     if (cap > kMaxRedBlocks) cap = kMaxRedBlocks;
     if (want < 1) want = 1;
     return (int)(want < cap ? want : cap);
@@ -515,11 +567,11 @@ int grid_for(int64_t n_rows, int per_thread) {
 int launch_k1(K1Args a, int32_t off_type, cudaStream_t s) {
     const bool aligned = ((uintptr_t)a.off & 15) == 0;
     if (off_type == KP_I32) {
-        int g = grid_for(a.n_rows, 16);
+        int g = grid_for(a.n_rows, 64);
         if (aligned) k_row_stats<int32_t, true><<<g, kRedThreads, 0, s>>>(a);
         else k_row_stats<int32_t, false><<<g, kRedThreads, 0, s>>>(a);
     } else if (off_type == KP_I64) {
-        int g = grid_for(a.n_rows, 8);
+        int g = grid_for(a.n_rows, 32);
         if (aligned) k_row_stats<int64_t, true><<<g, kRedThreads, 0, s>>>(a);
         else k_row_stats<int64_t, false><<<g, kRedThreads, 0, s>>>(a);
     } else {
@@ -628,11 +680,11 @@ int launch_plan_select(const void *d_off, int32_t off_type, int64_t n_rows, int6
     const bool known = T.node[0][i].value == KP_USE_KNOWN;
     const bool aligned = ((uintptr_t)d_off & 15) == 0;
     if (off_type == KP_I32) {
-        const int g = known ? 1 : grid_for(n_rows, 16);
+        const int g = known ? 1 : grid_for(n_rows, 64);
         if (aligned) k_seer_plan_select<int32_t, true><<<g, kRedThreads, 0, s>>>(a, T, h);
         else k_seer_plan_select<int32_t, false><<<g, kRedThreads, 0, s>>>(a, T, h);
     } else if (off_type == KP_I64) {
-        const int g = known ? 1 : grid_for(n_rows, 8);
+        const int g = known ? 1 : grid_for(n_rows, 32);
         if (aligned) k_seer_plan_select<int64_t, true><<<g, kRedThreads, 0, s>>>(a, T, h);
         else k_seer_plan_select<int64_t, false><<<g, kRedThreads, 0, s>>>(a, T, h);
     } else {

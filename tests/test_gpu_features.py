@@ -80,3 +80,19 @@ def test_device_clock_runs():
     A = gen.config("C1").to_device_csr()
     g = features.gather_features(A, clock.CudaEventClock())
     assert g.collection_time > 0
+
+
+def test_length_stats_int32_nonmonotone_and_extremes(orc):
+    """int32 offsets through the 32-bit fast path and its signed fallback: decreasing
+    offsets (negative lengths) and the full int32 range, vs the int64 oracle."""
+    import numpy as np
+    import torch
+    from paper_2403_17017_b200 import _kernels
+    rng = np.random.default_rng(9)
+    cases = [np.array([-2**31, 2**31 - 1, -2**31, 0, 5, 5, 3], dtype=np.int64),
+             rng.integers(-2**31, 2**31 - 1, 10001),
+             np.cumsum(rng.integers(0, 3, 70001)).astype(np.int64),
+             np.concatenate([np.cumsum(rng.integers(0, 5, 50000)), [7], np.arange(10, 2000)]).astype(np.int64)]
+    for off in cases:
+        t = torch.from_numpy(off.astype(np.int32)).cuda()
+        assert _kernels.length_stats(t) == orc.length_stats_np(off)
