@@ -431,61 +431,65 @@ __global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__
     asm volatile("griddepcontrol.wait;" ::: "memory");
     const int64_t n_units = n_units_dev ? *n_units_dev : n_units_host;
     const int lane = threadIdx.x & 31;
-    const int64_t wbase = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32;
-    if (wbase >= n_units) return;
-    const int64_t u = wbase + lane;
-    const int32_t r = u < n_units ? crow[u] : -2;
-    const V v = (u < n_units && r >= 0) ? cval[u] : V(0);
-    int32_t prev = __shfl_up_sync(0xffffffffu, r, 1);
-    if (lane == 0) prev = wbase > 0 ? crow[wbase - 1] : -3;
-    const bool head = r != prev;
-    // inclusive segmented scan within the warp
-    SegPair<V> inc{head ? 1 : 0, v};
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-        SegPair<V> t{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
-        if (lane >= o) inc = seg_op(t, inc);
-    }
-    int32_t next = __shfl_down_sync(0xffffffffu, r, 1);
-    if (lane == 31) next = (u + 1 < n_units) ? crow[u + 1] : -4;
-    // does this lane's run start inside this warp?  (lane of the run head)
-    const unsigned heads = __ballot_sync(0xffffffffu, head);
-    const unsigned below = heads & ((lane == 31) ? 0xffffffffu : ((2u << lane) - 1u));
-    const bool started_here = below != 0;  // a head at or before this lane within the warp
-    const bool run_end_here = next != r;
-    if (r >= 0 && started_here && run_end_here) {
-        if constexpr (kB) dst.put(r, dst.y[dst.self][r] + inc.v);
-        else y[r] += inc.v;
-    }
-    // run open at the warp end that started in this warp: continue over later units
-    const bool cont = (lane == 31) && r >= 0 && started_here && !run_end_here;
-    if (__ballot_sync(0xffffffffu, cont)) {
-        const int32_t rho = __shfl_sync(0xffffffffu, r, 31);
-        V acc = 0;
-        // 8 batches of 32 units per trip, all loads issued first; rho never reappears after
-        // its run ends, so matches past the end of the run cannot occur
-        for (int64_t b = wbase + 32;; b += 256) {
-            int32_t rr[8];
-            V vv[8];
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const int64_t q = b + 32 * i + lane;
-                rr[i] = q < n_units ? crow[q] : -5;
-                vv[i] = q < n_units ? cval[q] : V(0);
-            }
-            bool open = true;
-#pragma unroll
-            for (int i = 0; i < 8; ++i) {
-                const bool in = rr[i] == rho;
-                if (in) acc += vv[i];
-                open = open && __ballot_sync(0xffffffffu, in) == 0xffffffffu;
-            }
-            if (!open) break;  // the run ended inside this trip
+    // grid-stride over groups of 32 units: the launch is sized for the work, not for a
+    // host-side upper bound of the (device-counted) unit number
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t wbase = (((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5) * 32; wbase < n_units;
+         wbase += nwarps * 32) {
+        const int64_t u = wbase + lane;
+        const int32_t r = u < n_units ? crow[u] : -2;
+        const V v = (u < n_units && r >= 0) ? cval[u] : V(0);
+        int32_t prev = __shfl_up_sync(0xffffffffu, r, 1);
+        if (lane == 0) prev = wbase > 0 ? crow[wbase - 1] : -3;
+        const bool head = r != prev;
+        // inclusive segmented scan within the warp
+        SegPair<V> inc{head ? 1 : 0, v};
+    #pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            SegPair<V> t{__shfl_up_sync(0xffffffffu, inc.f, o), __shfl_up_sync(0xffffffffu, inc.v, o)};
+            if (lane >= o) inc = seg_op(t, inc);
         }
-        acc = group_sum<32>(acc);
-        if (lane == 31) {
-            if constexpr (kB) dst.put(rho, dst.y[dst.self][rho] + (inc.v + acc));
-            else y[rho] += inc.v + acc;
+        int32_t next = __shfl_down_sync(0xffffffffu, r, 1);
+        if (lane == 31) next = (u + 1 < n_units) ? crow[u + 1] : -4;
+        // does this lane's run start inside this warp?  (lane of the run head)
+        const unsigned heads = __ballot_sync(0xffffffffu, head);
+        const unsigned below = heads & ((lane == 31) ? 0xffffffffu : ((2u << lane) - 1u));
+        const bool started_here = below != 0;  // a head at or before this lane within the warp
+        const bool run_end_here = next != r;
+        if (r >= 0 && started_here && run_end_here) {
+            if constexpr (kB) dst.put(r, dst.y[dst.self][r] + inc.v);
+            else y[r] += inc.v;
+        }
+        // run open at the warp end that started in this warp: continue over later units
+        const bool cont = (lane == 31) && r >= 0 && started_here && !run_end_here;
+        if (__ballot_sync(0xffffffffu, cont)) {
+            const int32_t rho = __shfl_sync(0xffffffffu, r, 31);
+            V acc = 0;
+            // 8 batches of 32 units per trip, all loads issued first; rho never reappears after
+            // its run ends, so matches past the end of the run cannot occur
+            for (int64_t b = wbase + 32;; b += 256) {
+                int32_t rr[8];
+                V vv[8];
+    #pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int64_t q = b + 32 * i + lane;
+                    rr[i] = q < n_units ? crow[q] : -5;
+                    vv[i] = q < n_units ? cval[q] : V(0);
+                }
+                bool open = true;
+    #pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const bool in = rr[i] == rho;
+                    if (in) acc += vv[i];
+                    open = open && __ballot_sync(0xffffffffu, in) == 0xffffffffu;
+                }
+                if (!open) break;  // the run ended inside this trip
+            }
+            acc = group_sum<32>(acc);
+            if (lane == 31) {
+                if constexpr (kB) dst.put(rho, dst.y[dst.self][rho] + (inc.v + acc));
+                else y[rho] += inc.v + acc;
+            }
         }
     }
 }
@@ -1537,7 +1541,8 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
                 reinterpret_cast<const int32_t *>(b + L.b), U, crow, cval);
             KP_LAUNCHED();
             const int64_t umax = ad_units_max(A);
-            k_carry_fixup<V><<<(unsigned)((umax * 32 + 255) / 256), 256, 0, s>>>(crow, cval, U, 0, y);
+            const int64_t fg = (umax * 32 + 255) / 256 < (int64_t)sms * 16 ? (umax * 32 + 255) / 256 : (int64_t)sms * 16;
+            k_carry_fixup<V><<<(unsigned)fg, 256, 0, s>>>(crow, cval, U, 0, y);
             KP_LAUNCHED();
             return KP_OK;
         }
