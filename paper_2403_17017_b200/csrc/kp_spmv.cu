@@ -885,7 +885,8 @@ __global__ void __launch_bounds__(256) k_coo_wm(const int32_t *__restrict__ rid,
 // sharing an offset, i.e. the non-empty one), and a block max-scan seeded with the
 // row containing the window's first element fills every position.  Reads the
 // offsets once and writes each row id once (vectorised), no per-element search.
-constexpr int kCooPrepItems = 256 * kIPT;
+constexpr int kCooPrepIPT = 16;                      // row ids per thread
+constexpr int kCooPrepItems = 256 * kCooPrepIPT;  // 4096 nnz per CTA tile
 
 template <typename O>
 __device__ __forceinline__ int64_t upper_bound_off(const O *off, int64_t n_rows, int64_t v) {
@@ -915,28 +916,35 @@ __global__ void __launch_bounds__(256) k_prep_coo_starts(const O *__restrict__ o
 template <typename O>
 __global__ void __launch_bounds__(256) k_prep_coo(const O *__restrict__ off, int64_t n_rows, int64_t nnz,
                                                   const int32_t *__restrict__ c0s, int32_t *__restrict__ rid) {
-    __shared__ int32_t s_mark[kCooPrepItems];
+    constexpr int P = kCooPrepIPT;
+    // marks padded one slot per 32 so the blocked read (thread t: slots P*t .. P*t+P-1) is
+    // bank-conflict free
+    __shared__ int32_t s_mark[kCooPrepItems + kCooPrepItems / 32];
     __shared__ int32_t s_wmax[8];
     const int64_t j0 = (int64_t)blockIdx.x * kCooPrepItems;
     const int64_t j1 = j0 + kCooPrepItems < nnz ? j0 + kCooPrepItems : nnz;
     const int64_t nb = (nnz + kCooPrepItems - 1) / kCooPrepItems;
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    for (int k = tid; k < kCooPrepItems; k += 256) s_mark[k] = -1;
     const int64_t c0 = c0s[blockIdx.x];  // row containing j0
     const int64_t ra = c0 + 1;
     const int64_t rb = blockIdx.x + 1 < nb ? (int64_t)c0s[blockIdx.x + 1] + 1 : n_rows;
+    for (int k = tid; k < kCooPrepItems; k += 256) s_mark[k + (k >> 5)] = -1;
     __syncthreads();
     for (int64_t r = ra + tid; r < rb; r += 256) {
         const int64_t o = ldo(off + r);
-        if (o < j1) atomicMax(&s_mark[(int)(o - j0)], (int32_t)r);
+        if (o < j1) {
+            const int k = (int)(o - j0);
+            atomicMax(&s_mark[k + (k >> 5)], (int32_t)r);
+        }
     }
     __syncthreads();
-    // blocked max-scan: thread t owns positions 8t .. 8t+7
-    int32_t v[kIPT];
+    // blocked max-scan: thread t owns positions P*t .. P*t+P-1
+    int32_t v[P];
     int32_t m = -1;
 #pragma unroll
-    for (int i = 0; i < kIPT; ++i) {
-        const int32_t q = s_mark[tid * kIPT + i];
+    for (int i = 0; i < P; ++i) {
+        const int k = tid * P + i;
+        const int32_t q = s_mark[k + (k >> 5)];
         m = q > m ? q : m;
         v[i] = m;
     }
@@ -952,18 +960,17 @@ __global__ void __launch_bounds__(256) k_prep_coo(const O *__restrict__ off, int
     for (int i = 0; i < w; ++i) carry = s_wmax[i] > carry ? s_wmax[i] : carry;
     int32_t ex = __shfl_up_sync(0xffffffffu, inc, 1);
     if (lane > 0) carry = ex > carry ? ex : carry;
-    int32_t outv[kIPT];
 #pragma unroll
-    for (int i = 0; i < kIPT; ++i) outv[i] = v[i] > carry ? v[i] : carry;
-    const int64_t jb = j0 + tid * kIPT;
-    if (jb + kIPT <= j1) {
+    for (int i = 0; i < P; ++i) v[i] = v[i] > carry ? v[i] : carry;
+    const int64_t jb = j0 + tid * P;
+    if (jb + P <= j1) {
         int4 *dst = reinterpret_cast<int4 *>(rid + jb);
-        dst[0] = make_int4(outv[0], outv[1], outv[2], outv[3]);
-        dst[1] = make_int4(outv[4], outv[5], outv[6], outv[7]);
+#pragma unroll
+        for (int q = 0; q < P / 4; ++q) dst[q] = make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
     } else {
 #pragma unroll
-        for (int i = 0; i < kIPT; ++i)
-            if (jb + i < j1) rid[jb + i] = outv[i];
+        for (int i = 0; i < P; ++i)
+            if (jb + i < j1) rid[jb + i] = v[i];
     }
 }
 
