@@ -78,6 +78,7 @@ def main():
     ap.add_argument("--seed", type=int, default=2403)
     ap.add_argument("--weighting", default="cost-rel", choices=["none", "regret", "cost-log", "cost-rel"])
     ap.add_argument("--near-best", type=float, default=0.0, help="relabel within this fraction of the best")
+    ap.add_argument("--plots", default=None, help="emit SPEC eval plot data (CSV + SVG, test split) here")
     a = ap.parse_args()
     rows = load(a.corpus)
     train, test = dataset.split_train_test(rows, a.seed, 0.8)
@@ -93,6 +94,16 @@ def main():
            "test": evaluate(model, test, ITERS), "all": evaluate(model, rows, ITERS),
            "tree_nodes": {"known": model.known_tree.n_nodes, "gathered": model.gathered_tree.n_nodes,
                           "selector": model.selector_tree.n_nodes}}
+    from paper_2403_17017_b200 import evaluate as ev
+    rep["eval_report_test"] = {}
+    for k in ITERS:
+        er = ev.evaluate(model, test, k)
+        rep["eval_report_test"][str(k)] = {
+            name: {"total_realized_cost_s": p.total_realized_cost, "accuracy": p.accuracy,
+                   "error_vs_oracle_s": p.error_vs_oracle} for name, p in er.predictors.items()}
+        rep["eval_report_test"][str(k)]["geomean_speedup"] = ev.geomean_speedup(er)
+        if a.plots:
+            ev.emit_plot_data(er, a.plots, per_matrix=False)
     if a.report:
         with open(a.report, "w") as f:
             json.dump(rep, f, indent=1)
