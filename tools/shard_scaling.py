@@ -1,0 +1,73 @@
+"""Strong-scaling projection of the row-sharded C5 SpMV on ONE GPU (this round has 1 GPU):
+for P = 1, 2, 4, 8 the matrix is cut exactly as `dist.shard_device` cuts it for P ranks,
+and every rank's local SpMV (the chosen kernel, rank-padded x) is timed in turn; the
+step time of P GPUs is bounded below by the slowest rank.  Reports per-P max / mean rank
+time, the compute-only speedup t(1) / max_p t_p(P), and the bytes each rank must push per
+iteration in the y exchange (fused into the SpMV epilogue over NVLink, kp_spmv_bcast).
+
+    python tools/shard_scaling.py [--kernel CSR,WO] [--parts 1,2,4,8] [--out profiles/shard_scaling_r01.json]
+"""
+import argparse
+import json
+import os
+import statistics
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch  # noqa: E402
+
+from paper_2403_17017_b200 import dist as kdist  # noqa: E402
+from paper_2403_17017_b200 import gen, kernels  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--kernel", default="CSR,WO")
+    ap.add_argument("--parts", default="1,2,4,8")
+    ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--out", default=None)
+    a = ap.parse_args()
+    kern = kernels.kernel_index(a.kernel)
+    m = gen.config("C5", device="cuda")
+    R, C, Z = m.n_rows, m.n_cols, m.nnz
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    res = {"matrix": "C5 R-MAT s26 ef16", "rows": R, "nnz": Z, "kernel": a.kernel, "parts": {}}
+    for P in [int(v) for v in a.parts.split(",")]:
+        times, nnzs = [], []
+        for rank in range(P):
+            A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, C, rank, P, torch.float32)
+            x = torch.rand(P * plan.r_max, device="cuda", dtype=torch.float32)
+            y = torch.empty(plan.local_rows, device="cuda", dtype=torch.float32)
+            Pp = kernels.prepare(A, kern) if kern in kernels.NEEDS_PREP else None
+            kernels.spmv(A, x, kern, y=y, prepared=Pp)
+            ts = []
+            for _ in range(a.reps):
+                flush.zero_()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                kernels.spmv(A, x, kern, y=y, prepared=Pp)
+                e1.record()
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1) * 1e-3)
+            times.append(statistics.median(ts))
+            nnzs.append(A.nnz)
+            del A, x, y, Pp
+            torch.cuda.empty_cache()
+        rec = {"max_rank_ms": max(times) * 1e3, "mean_rank_ms": statistics.mean(times) * 1e3,
+               "rank_ms": [t * 1e3 for t in times], "rank_nnz": nnzs,
+               "exchange_bytes_per_rank_per_iter": int(4 * (R // P) * (P - 1))}
+        res["parts"][str(P)] = rec
+        print(P, json.dumps({k: v for k, v in rec.items() if k not in ("rank_ms", "rank_nnz")}), flush=True)
+    t1 = res["parts"]["1"]["max_rank_ms"] if "1" in res["parts"] else None
+    if t1:
+        for P, rec in res["parts"].items():
+            rec["compute_speedup_vs_1"] = t1 / rec["max_rank_ms"]
+    print(json.dumps({P: round(r.get("compute_speedup_vs_1", 0), 2) for P, r in res["parts"].items()}))
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
