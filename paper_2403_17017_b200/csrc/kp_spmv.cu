@@ -83,8 +83,11 @@ struct YDst {
     V *y[KP_MAX_PEERS];
     int32_t n, self;
     __device__ __forceinline__ void put(int64_t i, V v) const {
-#pragma unroll 1
-        for (int p = 0; p < n; ++p) y[p][i] = v;
+        // fully unrolled with a predicate: a dynamic index into this by-value parameter
+        // struct would force a local-memory copy of it
+#pragma unroll
+        for (int p = 0; p < KP_MAX_PEERS; ++p)
+            if (p < n) y[p][i] = v;
     }
 };
 

@@ -27,7 +27,11 @@ def main():
     ap.add_argument("--parts", default="1,2,4,8")
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--bcast", action="store_true", help="only measure the fused-exchange epilogue cost")
     a = ap.parse_args()
+    if a.bcast:
+        bcast_overhead()
+        return
     kern = kernels.kernel_index(a.kernel)
     m = gen.config("C5", device="cuda")
     R, C, Z = m.n_rows, m.n_cols, m.nnz
@@ -67,6 +71,37 @@ def main():
     if a.out:
         with open(a.out, "w") as f:
             json.dump(res, f, indent=1)
+
+
+
+def bcast_overhead(P: int = 8, reps: int = 5):
+    """Cost of the fused exchange epilogue itself on one GPU: rank 0's shard at P ranks,
+    kp_spmv vs kp_spmv_bcast writing its y slice into P distinct (local) next-x buffers."""
+    m = gen.config("C5", device="cuda")
+    A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, m.n_cols, 0, P, torch.float32)
+    del m
+    torch.cuda.empty_cache()
+    x = torch.rand(P * plan.r_max, device="cuda", dtype=torch.float32)
+    nxt = [torch.empty(P * plan.r_max, device="cuda", dtype=torch.float32) for _ in range(P)]
+    dests = [b[:plan.local_rows] for b in nxt]
+    y = torch.empty(plan.local_rows, device="cuda", dtype=torch.float32)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    out = {}
+    for name, fn in (("spmv", lambda: kernels.spmv(A, x, kernels.CSR_WO, y=y)),
+                     (f"spmv_bcast_{P}_dests", lambda: kernels.spmv_bcast(A, x, kernels.CSR_WO, dests, 0))):
+        fn()
+        ts = []
+        for _ in range(reps):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            ts.append(e0.elapsed_time(e1))
+        out[name + "_ms"] = statistics.median(ts)
+    print(json.dumps(out))
+    return out
 
 
 if __name__ == "__main__":
