@@ -314,7 +314,7 @@ def run_ours(a):
     traffic = _traffic_from_profiles(a.workload, kernels.KERNELS[kern])
 
     # ---------------------------------------------------------------- e2e through the public API
-    e2e = _e2e(a, A, x, dtype, dev, model, k, seer_step, stream)
+    e2e = _e2e(a, A, x, dtype, dev, model, k)
     clk = clocks.stop()
 
     # ---------------------------------------------------------------- per-kernel sweep
@@ -400,7 +400,7 @@ def _traffic_from_profiles(workload, kernel_label):
     return None
 
 
-def _e2e(a, A, x, dtype, dev, model, k, seer_step, stream):
+def _e2e(a, A, x, dtype, dev, model, k):
     """Public-API end to end: pinned host CSR + x -> H2D -> Seer plan -> y D2H, every step.
 
     Served as a two-deep pipeline, the way a serving loop would: step i+1's inputs stream
