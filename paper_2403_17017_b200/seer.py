@@ -322,10 +322,10 @@ def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int 
             wk.append(float(np.log1p(np.mean(regrets))) if regrets else 0.0)
     if not y:
         raise ValueError("no labelled examples")
-    if weighting in ("cost-log", "cost-rel"):
+    if weighting in ("cost-log", "cost-rel", "cost-mix"):
         return _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, weighting)
     if weighting not in ("none", "regret"):
-        raise ValueError("weighting must be 'none', 'regret', 'cost-log' or 'cost-rel'")
+        raise ValueError("weighting must be 'none', 'regret', 'cost-log', 'cost-rel' or 'cost-mix'")
     w = None if weighting == "none" else np.asarray(wk) + 1e-3
     kt = train_tree(Xk, y, max_depth, min_samples_leaf, nk, KNOWN_SCHEMA, w)
     gt = train_tree(Xg, y, max_depth, min_samples_leaf, nk, GATHERED_SCHEMA, w)
@@ -343,11 +343,19 @@ def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int 
 
 
 def _loss(costs, kind: str, cap: float = 1e3):
+    """Per-example loss of predicting each class: cost-log = log(t / t_best) (per-matrix
+    geomean objective), cost-rel = t / t_best - 1, cost-mix = log(t / t_best) + (t - t_best)
+    / 1 ms (adds the aggregate-time objective, so large matrices are not out-voted by many
+    small ones).  Missing kernels (inf) are capped at cap x t_best."""
     c = np.asarray(costs, dtype=np.float64)
     b = np.min(c[np.isfinite(c)])
     r = np.where(np.isfinite(c), c / b, cap)
     r = np.minimum(r, cap)
-    return np.log(r) if kind == "cost-log" else r - 1.0
+    if kind == "cost-log":
+        return np.log(r)
+    if kind == "cost-mix":
+        return np.log(r) + (r - 1.0) * b / 1e-3
+    return r - 1.0
 
 
 def _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, kind) -> SeerModel:

@@ -76,7 +76,7 @@ def main():
     ap.add_argument("--report", default=None)
     ap.add_argument("--max-depth", type=int, default=5)
     ap.add_argument("--seed", type=int, default=2403)
-    ap.add_argument("--weighting", default="cost-log", choices=["none", "regret", "cost-log", "cost-rel"])
+    ap.add_argument("--weighting", default="cost-mix", choices=["none", "regret", "cost-log", "cost-rel", "cost-mix"])
     ap.add_argument("--near-best", type=float, default=0.0, help="relabel within this fraction of the best")
     ap.add_argument("--plots", default=None, help="emit SPEC eval plot data (CSV + SVG, test split) here")
     a = ap.parse_args()
