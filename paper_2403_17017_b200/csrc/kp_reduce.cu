@@ -119,15 +119,6 @@ __device__ void epilogue(int64_t lo, int64_t hi, int64_t s1, int64_t s2, int64_t
 template <typename O>
 struct Vec16;
 template <>
-struct Vec16<int32_t> {
-    static constexpr int V = 4;
-    using T = int4;
-    __device__ static void load(const int32_t *p, int64_t (&o)[4]) {
-        int4 v = ld_stream4(reinterpret_cast<const int4 *>(p));
-        o[0] = v.x; o[1] = v.y; o[2] = v.z; o[3] = v.w;
-    }
-};
-template <>
 struct Vec16<int64_t> {
     static constexpr int V = 2;
     __device__ static void load(const int64_t *p, int64_t (&o)[2]) {

@@ -44,7 +44,6 @@ static_assert(sizeof(PrepHeader) <= kAlign, "header");
 constexpr size_t kRedWsBytes = 40960;  // >= kp_reduce_workspace_bytes()
 
 // ---------------------------------------------------------------- tunables
-constexpr int kTile = 256;      // threads per CTA for the tile kernels
 constexpr int kIPT = 8;         // merge items / nnz per thread
 constexpr int kCooChunk = 32 * kIPT;      // 256 nnz per warp
 constexpr int kTmRows = 256;              // CSR,TM rows per CTA tile
