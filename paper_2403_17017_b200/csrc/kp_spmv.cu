@@ -543,6 +543,10 @@ __device__ __forceinline__ int64_t merge_search_warp(const O *off, int64_t n_row
 }
 
 constexpr int kWarpTile = 32 * kIPT;  // 256 merge items per unit
+// fp64: 3 CTAs (24 warps) per SM in 80 registers instead of 2 at its natural ~110
+// (band-27 fp64 476 -> 402 us, gather-bound inputs unchanged); fp32: 4 CTAs in 64
+template <typename V>
+constexpr int kMergeMinBlocks = sizeof(V) == 4 ? 4 : 3;
 constexpr int kMergeWarps = 8;        // warps per CTA
 
 // Persistent merge-path warps (Merrill & Garland, restructured for B200).  The merge of
@@ -562,7 +566,7 @@ constexpr int kMergeWarps = 8;        // warps per CTA
 // counter makes stale marks of earlier units lose, so nothing is cleared), a max-scan
 // gives every position its row, and a thread-local + warp segmented scan sums rows.
 template <typename V, typename O, bool kPrep, bool kB = false>
-__global__ void __launch_bounds__(kMergeWarps * 32) k_csr_merge(
+__global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_merge(
     const O *__restrict__ off, const int32_t *__restrict__ col, const V *__restrict__ val, const V *__restrict__ x,
     V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, int64_t upw, int64_t n_ranges,
     const int64_t *__restrict__ part, int32_t *__restrict__ crow, V *__restrict__ cval, YDst<V> dst = YDst<V>{}) {
@@ -765,8 +769,12 @@ __global__ void __launch_bounds__(256) k_prep_mp(const O *__restrict__ off, int6
 // chunk in a register, and only the row open at the RANGE end goes through k_carry_fixup.
 // Empty rows (gaps between consecutive row ids) are zero-filled by the element that
 // follows the gap, so y needs no memset.
+// fp32: 5 CTAs (40 warps) per SM in 48 registers without spills (C2 107 -> 95 us, band-27
+// 0.50 -> 0.70 of HBM); fp64 keeps 64 registers (48 spills and runs slower)
+template <typename V>
+constexpr int kCooMinBlocks = sizeof(V) == 4 ? 5 : 4;
 template <typename V, bool kVec>
-__global__ void __launch_bounds__(256) k_coo_wm(const int32_t *__restrict__ rid, const int32_t *__restrict__ col,
+__global__ void __launch_bounds__(256, kCooMinBlocks<V>) k_coo_wm(const int32_t *__restrict__ rid, const int32_t *__restrict__ col,
                                                 const V *__restrict__ val, const V *__restrict__ x,
                                                 V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_chunks,
                                                 int64_t cpw, int64_t n_ranges, int32_t *__restrict__ crow,

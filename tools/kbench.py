@@ -33,6 +33,10 @@ MATS = {
     "pl": lambda d: (gen.powerlaw_rows(4_000_000, 16.0, 1.5, device=d), torch.float32),
     "const32": lambda d: (gen.constant_rows(4_000_000, 32, device=d), torch.float32),
     "C5": lambda d: (gen.config("C5", device=d), torch.float32),
+    # fp64 variants (C4 is the only fp64 BASELINE config)
+    "C2d": lambda d: (gen.config("C2", device=d), torch.float64),
+    "band27d": lambda d: (gen.banded(4_000_000, 27, device=d), torch.float64),
+    "pld": lambda d: (gen.powerlaw_rows(4_000_000, 16.0, 1.5, device=d), torch.float64),
 }
 
 
