@@ -34,6 +34,10 @@ int num_sms() {
 namespace {
 
 constexpr int kRedThreads = 256;
+// int32 offsets: 4 CTAs/SM (64 registers; 67 M rows 67 -> 59 us); int64 keeps the
+// compiler's own allocation (0 = no minimum), which measured faster than any forced budget
+template <typename O>
+constexpr int kK1MinBlocks = sizeof(O) == 4 ? 4 : 0;
 constexpr int kMaxRedBlocks = 148 * 8;
 
 struct Partial {
@@ -318,7 +322,7 @@ __device__ __forceinline__ bool k1_pass(const K1Args &a, const O *off, int64_t &
 }
 
 template <typename O, bool kVec>
-__global__ void __launch_bounds__(kRedThreads) k_row_stats(K1Args a) {
+__global__ void __launch_bounds__(kRedThreads, kK1MinBlocks<O>) k_row_stats(K1Args a) {
     __shared__ SmemTree tree;
     __shared__ int s_path;
     const O *off = reinterpret_cast<const O *>(a.off);
@@ -399,7 +403,7 @@ __device__ __forceinline__ int32_t predict_param(const ParamTrees &T, int t, con
 }
 
 template <typename O, bool kVec>
-__global__ void __launch_bounds__(kRedThreads) k_seer_plan_select(K1Args a, const __grid_constant__ ParamTrees T,
+__global__ void __launch_bounds__(kRedThreads, kK1MinBlocks<O>) k_seer_plan_select(K1Args a, const __grid_constant__ ParamTrees T,
                                                                    cudaGraphConditionalHandle h) {
     const O *off = reinterpret_cast<const O *>(a.off);
     const double xk[4] = {(double)a.n_rows, (double)a.n_cols, (double)a.nnz, (double)a.iters};
