@@ -544,9 +544,12 @@ __device__ __forceinline__ int64_t merge_search_warp(const O *off, int64_t n_row
 
 constexpr int kWarpTile = 32 * kIPT;  // 256 merge items per unit
 // fp64: 3 CTAs (24 warps) per SM in 80 registers instead of 2 at its natural ~110
-// (band-27 fp64 476 -> 402 us, gather-bound inputs unchanged); fp32: 4 CTAs in 64
+// (band-27 fp64 476 -> 402 us, gather-bound inputs unchanged).  fp32 keeps the compiler's
+// allocation (0 = no minimum): 64 registers / 4 CTAs for the plain kernel; the fused-
+// exchange variant lands at ~112 / 2 CTAs, which measured faster on the DRAM-bound C5
+// shards (916 vs 877 GB/s with a forced 4 CTAs).
 template <typename V>
-constexpr int kMergeMinBlocks = sizeof(V) == 4 ? 4 : 3;
+constexpr int kMergeMinBlocks = sizeof(V) == 4 ? 0 : 3;
 constexpr int kMergeWarps = 8;        // warps per CTA
 
 // Persistent merge-path warps (Merrill & Garland, restructured for B200).  The merge of
