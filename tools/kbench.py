@@ -46,7 +46,12 @@ def main():
     ap.add_argument("--kernels", default="0,1,2,3,4,5,6,7")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--out", default=None)
+    ap.add_argument("--wave-warps", type=int, default=0,
+                    help="persistent-kernel wave size in warps (0 = occupancy-derived; experiments)")
     a = ap.parse_args()
+    if a.wave_warps:
+        from paper_2403_17017_b200 import _lib
+        _lib.load().kp_debug_set_wave_warps(a.wave_warps)
     try:
         peak = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]
     except Exception:
