@@ -271,7 +271,7 @@ def selector_label(row, known_pred: int, gathered_pred: int, k: int) -> int:
 
 def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int = 1,
                kernels=KERNELS, meta: dict | None = None, weighting: str = "none",
-               near_best: float = 0.0) -> SeerModel:
+               near_best: float = 0.0, selector_folds: int = 0) -> SeerModel:
     """labels = fastest_kernel per (matrix, k); known tree on the known
     schema, gathered tree on the full schema, selector on labels from the two
     sub-models' own predictions on the training rows.
@@ -323,7 +323,7 @@ def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int 
     if not y:
         raise ValueError("no labelled examples")
     if weighting in ("cost-log", "cost-rel", "cost-mix"):
-        return _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, weighting)
+        return _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, weighting, selector_folds)
     if weighting not in ("none", "regret"):
         raise ValueError("weighting must be 'none', 'regret', 'cost-log', 'cost-rel' or 'cost-mix'")
     w = None if weighting == "none" else np.asarray(wk) + 1e-3
@@ -358,20 +358,43 @@ def _loss(costs, kind: str, cap: float = 1e3):
     return r - 1.0
 
 
-def _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, kind) -> SeerModel:
+def _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, kind,
+                     selector_folds: int = 0) -> SeerModel:
     """Cost-sensitive trio (extension): kernel trees minimise the summed loss of the
     realised per-iteration-count cost (log or relative regret vs the example's best
     kernel), the selector minimises the loss of the realised known vs gathered path
-    (collection time charged, SPEC.md:367-375 costs)."""
+    (collection time charged, SPEC.md:367-375 costs).
+
+    selector_folds > 1 (extension): the selector's known / gathered path costs come from
+    OUT-OF-FOLD sub-model predictions (matrices split into that many folds; each fold
+    predicted by trees trained on the others).  In-sample predictions make the known tree
+    look right wherever it was fit, so the selector never learns where its blind spot
+    (skew the known features cannot see) lies; out-of-fold costs expose it."""
     from .dtree import train_cost_tree
     nk = len(kernels)
     Ck = np.stack([_loss([r.cost(j, k) for j in range(nk)], kind) for r, k in ex])
     kt = train_cost_tree(Xk, Ck, max_depth, min_samples_leaf, KNOWN_SCHEMA)
     gt = train_cost_tree(Xg, Ck, max_depth, min_samples_leaf, GATHERED_SCHEMA)
+    kpred = [kt.predict(xk) for xk in Xk]
+    gpred = [gt.predict(xg) for xg in Xg]
+    if selector_folds > 1:
+        names = sorted({r.name for r, _ in ex})
+        fold_of = {n: i % selector_folds for i, n in enumerate(names)}
+        fold = np.array([fold_of[r.name] for r, _ in ex])
+        Xk_a, Xg_a = np.asarray(Xk, dtype=np.float64), np.asarray(Xg, dtype=np.float64)
+        for f in range(selector_folds):
+            tr, te = np.nonzero(fold != f)[0], np.nonzero(fold == f)[0]
+            if len(te) == 0 or len(tr) == 0:
+                continue
+            kt_f = train_cost_tree(Xk_a[tr], Ck[tr], max_depth, min_samples_leaf, KNOWN_SCHEMA)
+            gt_f = train_cost_tree(Xg_a[tr], Ck[tr], max_depth, min_samples_leaf, GATHERED_SCHEMA)
+            for i in te:
+                kpred[i] = kt_f.predict(Xk[i])
+                gpred[i] = gt_f.predict(Xg[i])
     Cs = []
-    for (r, k), xk, xg in zip(ex, Xk, Xg):
-        ck = r.cost(kt.predict(xk), k)
-        cg = r.cost(gt.predict(xg), k) + r.collection_time
+    for (r, k), kp, gp in zip(ex, kpred, gpred):
+        ck = r.cost(kp, k)
+        cg = r.cost(gp, k) + r.collection_time
         Cs.append(_loss([ck, cg], kind))
     st = train_cost_tree(Xk, np.stack(Cs), max_depth, min_samples_leaf, KNOWN_SCHEMA)
     meta = dict(meta or {})

@@ -75,18 +75,24 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--report", default=None)
     ap.add_argument("--max-depth", type=int, default=5)
+    ap.add_argument("--min-leaf", type=int, default=4,
+                    help="min training examples per leaf (tools/cv_seer.py: 4 is robust, 1 overfits)")
     ap.add_argument("--seed", type=int, default=2403)
     ap.add_argument("--weighting", default="cost-mix", choices=["none", "regret", "cost-log", "cost-rel", "cost-mix"])
     ap.add_argument("--near-best", type=float, default=0.0, help="relabel within this fraction of the best")
     ap.add_argument("--plots", default=None, help="emit SPEC eval plot data (CSV + SVG, test split) here")
+    ap.add_argument("--selector-folds", type=int, default=0,
+                    help="out-of-fold sub-model predictions for the selector's labels (0 = in-sample)")
     a = ap.parse_args()
     rows = load(a.corpus)
     train, test = dataset.split_train_test(rows, a.seed, 0.8)
-    model = seer.train_seer(train, ITERS, a.max_depth, 1, kernels.KERNELS,
+    model = seer.train_seer(train, ITERS, a.max_depth, a.min_leaf, kernels.KERNELS,
                             {"source": "B200-measured corpus (tools/collect_corpus.py)", "corpus": os.path.relpath(a.corpus, ROOT),
-                             "iterations": list(ITERS), "max_depth": a.max_depth, "split_seed": a.seed,
-                             "n_train": len(train), "n_test": len(test), "near_best": a.near_best},
-                            weighting=a.weighting, near_best=a.near_best)
+                             "iterations": list(ITERS), "max_depth": a.max_depth, "min_samples_leaf": a.min_leaf,
+                             "split_seed": a.seed,
+                             "n_train": len(train), "n_test": len(test), "near_best": a.near_best,
+                             "selector_folds": a.selector_folds},
+                            weighting=a.weighting, near_best=a.near_best, selector_folds=a.selector_folds)
     model.save(a.out)
     plain = seer.train_seer(train, ITERS, a.max_depth, 1, kernels.KERNELS, weighting="none")
     rep = {"weighting": a.weighting, "n_train": len(train), "n_test": len(test),
