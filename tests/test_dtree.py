@@ -170,3 +170,24 @@ def test_cost_seer_training_runs_on_corpus_rows():
     for r in rows[:20]:
         cost, kern, path = seer.realized_cost(m, r, 1)
         assert 0 <= kern < 8 and path in (0, 1) and cost > 0
+
+
+def test_cost_seer_out_of_fold_selector():
+    """selector_folds > 1: same kernel trees as the in-sample training (they are fitted on
+    all rows either way), a valid selector, deterministic."""
+    import csv
+    import os
+    from paper_2403_17017_b200 import dataset, seer
+    root = os.path.join(os.path.dirname(os.path.dirname(__file__)), "paper_2403_17017_b200", "models", "corpus")
+    known = {r["name"]: (int(r["rows"]), int(r["cols"]), int(r["nnz"]))
+             for r in csv.DictReader(open(os.path.join(root, "known.csv")))}
+    rd = lambda f: open(os.path.join(root, f)).read()  # noqa: E731
+    rows = dataset.read_tables(rd("elapsed.csv"), rd("preprocess.csv"), rd("metadata.csv"), known)[:150]
+    a = seer.train_seer(rows, (1, 10), 4, 4, weighting="cost-mix")
+    b = seer.train_seer(rows, (1, 10), 4, 4, weighting="cost-mix", selector_folds=3)
+    c = seer.train_seer(rows, (1, 10), 4, 4, weighting="cost-mix", selector_folds=3)
+    assert a.known_tree.to_dict() == b.known_tree.to_dict()
+    assert a.gathered_tree.to_dict() == b.gathered_tree.to_dict()
+    assert b.selector_tree.to_dict() == c.selector_tree.to_dict()
+    for r in rows[:30]:
+        assert seer.realized_cost(b, r, 10)[2] in (0, 1)
