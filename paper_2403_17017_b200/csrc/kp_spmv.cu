@@ -1257,15 +1257,11 @@ int merge_warps_per_sm() {
     return warps_per_sm;
 }
 int64_t g_wave_warps = 0;  // kp_debug_set_wave_warps (0 = occupancy-derived)
-// Persistent-kernel wave: every resident warp, except when x cannot stay in L2 (> 64 MB):
-// then the gathers miss to DRAM and half the warps measured faster (C5 shard: merge
-// 10.47 -> 10.11 ms, COO 10.73 -> ~9.9 ms), while L2-resident x wants full occupancy
-// (C2: 91 -> 97 us at half).
-int64_t wave_target(const kp_csr *A, size_t val_bytes, int warps_per_sm) {
-    const int64_t full = (int64_t)num_sms() * warps_per_sm;
-    const bool x_in_dram = (double)A->n_cols * (double)val_bytes > 64.0 * (1 << 20);
-    return x_in_dram ? (full + 1) / 2 : full;
-}
+// Persistent-kernel wave: every resident warp.  (Halving it when x exceeds L2 helped
+// random gathers that miss to DRAM -- C5 merge 10.47 -> 10.12 ms -- but cost banded
+// matrices with a large x 35-50 % (band-4, 32 M rows: merge 466 -> 716 us), and the
+// gather locality is not known at launch; reverted.)
+int64_t wave_target(const kp_csr *, size_t, int warps_per_sm) { return (int64_t)num_sms() * warps_per_sm; }
 template <typename V, typename O>
 MergeGeom merge_geom(const kp_csr *A) {
     const int warps_per_sm = merge_warps_per_sm<V, O>();

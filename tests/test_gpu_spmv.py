@@ -147,3 +147,23 @@ def test_coo_misaligned_user_arrays(orc):
     off, col, val = A.to_host()
     yref, absy = orc.spmv_csr(off, col, val, x.cpu().numpy())
     assert orc.spmv_check(y.cpu().numpy(), yref, absy, 1e-5)[0]
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_wide_x_half_wave(dtype, orc):
+    """x larger than 64 MB: the persistent kernels (merge, COO) run half a wave of warps
+    (DRAM-bound gathers); every kernel still matches the oracle."""
+    R, C, Z = 200_000, 20_000_000, 6_000_000
+    g = torch.Generator().manual_seed(11)
+    rows = torch.randint(0, R, (Z,), generator=g)
+    cols = torch.randint(0, C, (Z,), generator=g)
+    m = gen.from_coo("wide_x", R, C, rows, cols, 5)
+    A = m.to_device_csr(dtype)
+    x = (torch.rand(C, generator=g, dtype=torch.float64) * 2 - 1).to(dtype).cuda()
+    off, col, val = A.to_host()
+    yref, absy = orc.spmv_csr(off, col, val, x.cpu().numpy())
+    for k in range(8):
+        y = torch.full((A.n_rows,), float("nan"), dtype=dtype, device="cuda")
+        kernels.spmv(A, x, k, y=y)
+        ok, r = orc.spmv_check(y.cpu().numpy(), yref, absy, TOL[dtype])
+        assert ok, (kernels.KERNELS[k], r)
