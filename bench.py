@@ -319,6 +319,13 @@ def run_ours(a):
     # kernel-only timings above
     clk = clocks.stop()
     e2e = _e2e(a, A, x, dtype, dev, model, k)
+    if world > 1:  # whole-job e2e: every rank served its own matrix; slowest rank's step time
+        tt = torch.tensor([e2e["ms_per_step"]], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e["ms_per_step"] = round(float(tt.item()), 4)
+        e2e["value"] = round(world * k * bytes_csr / (e2e["ms_per_step"] * 1e-3) / 1e9, 2)
+        e2e["h2d_bytes_per_step"] *= world
+        e2e["d2h_bytes_per_step"] *= world
 
     # ---------------------------------------------------------------- per-kernel sweep
     sweep, geo, vs_best = None, None, None

@@ -164,49 +164,70 @@ __global__ void __launch_bounds__(128) k_csr_bm(const O *__restrict__ off, const
 // (256 threads, RPT rows each per tile) + 1 producer warp; 2 stages of <= 3072 nnz (fp32)
 // measured best on short-row inputs (band 4: 0.81 of the HBM peak vs 0.70 with 3 x 2048).  Per tile of 256*RPT rows
 // the producer pulls the row-offset window [r0, r1] and the nnz window
-// [off[r0], off[r1]) of cols and vals into one of 3 shared-memory stages with 1-D TMA
+// [off[r0], off[r1]) of cols and vals into one of 2 shared-memory stages with 1-D TMA
 // bulk copies (SASS UBLKCP) completing on the stage's `full` mbarrier; consumer warps
 // release a stage through its `empty` mbarrier, so no CTA-wide barrier sits in the
 // loop.  RPT is chosen on the host from the KNOWN mean row length (window ~3/4 of a
-// stage).  Windows larger than a stage fall back to direct per-thread global walks.
+// stage).  Medium rows get enlarged stages (below); a window larger than its stage (skew)
+// falls back to direct per-thread global walks for that tile.
 constexpr int kTmStages = 2;
 constexpr int kTmMaxRpt = 4;
+// gathers in flight per consumer thread: 4 for short-row stages (band 4: 0.81 of HBM vs
+// 0.70 at 8), kTmUWide for the enlarged medium-row stages
+constexpr int kTmUWide = 8;
+constexpr int kTmSplitWide = 2;  // consumer threads per row in the medium-row stages
+// Medium rows (the tile window of 256 rows exceeds kCap at the known mean, e.g. 27-point
+// stencils) get a LARGER stage instead of the per-thread global walk: capacity sized from
+// the known mean, up to what two stages of one CTA per SM can hold (kCapMax), so the
+// thread-per-row gathers stay coalesced across consecutive rows (ELL's access pattern
+// without its preparation).
 template <typename V, typename O>
 struct TmCfg {
-    static constexpr int kCap = sizeof(V) == 4 ? 3072 : 1536;                    // nnz per stage
+    static constexpr int kCap = sizeof(V) == 4 ? 3072 : 1536;                    // nnz per stage (short rows)
     static constexpr int kOffs = kTmRows * kTmMaxRpt + 8;                          // offsets per stage
     static constexpr size_t kOffBytes = (kOffs * sizeof(O) + 127) / 128 * 128;
-    static constexpr size_t kColBytes = (size_t)kCap * 4;
-    static constexpr size_t kStageBytes = kOffBytes + kColBytes + (size_t)kCap * sizeof(V);
+    static constexpr size_t kSmemMax = 216 * 1024;                                 // 2 stages, 1 CTA / SM
+    static constexpr int kCapMax = (int)((kSmemMax / kTmStages - kOffBytes) / (4 + sizeof(V))) / 128 * 128;
+    __host__ __device__ static constexpr size_t col_bytes(int cap) { return ((size_t)cap * 4 + 127) / 128 * 128; }
+    __host__ __device__ static constexpr size_t stage_bytes(int cap) {
+        return kOffBytes + col_bytes(cap) + ((size_t)cap * sizeof(V) + 127) / 128 * 128;
+    }
 };
 
-template <typename V, typename O, bool kTma>
-__global__ void __launch_bounds__(kTmRows + 32) k_csr_tm(const O *__restrict__ off, const int32_t *__restrict__ col,
+// kSplit > 1 (medium-row stages): kSplit consumer threads per row, each summing a
+// contiguous part of it (consecutive rows stay in consecutive lanes, so the gathers stay
+// coalesced), parts combined through shared memory in a fixed order: kSplit x the gathers
+// in flight per tile.  Measured on C3 / band 27 / band 27 fp64 (fraction of HBM):
+// (U, split) = (16, 1) 0.63 / 0.72 / 0.83, (8, 2) 0.69-0.72 / 0.74-0.76 / 0.89-0.90,
+// (4, 2) 0.67 / 0.77 / 0.90, (16, 2) 0.53 / 0.57 / 0.91, (8, 3) 0.52 / 0.55 / 0.88.
+template <typename V, typename O, bool kTma, int kTmU, int kSplit>
+__global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                          const V *__restrict__ val, const V *__restrict__ x,
-                                                         V *__restrict__ y, int64_t n_rows, int rpt) {
+                                                         V *__restrict__ y, int64_t n_rows, int rpt, int kCap) {
     using Cfg = TmCfg<V, O>;
-    constexpr int kCap = Cfg::kCap;
+    const size_t stage = Cfg::stage_bytes(kCap);
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[kTmStages], empty[kTmStages];
     __shared__ int64_t s_base[kTmStages];  // element index staged at col slot 0; -1 = direct
+    __shared__ V s_part[kTmStages][kSplit > 1 ? kSplit - 1 : 1][kSplit > 1 ? kTmRows : 1];  // parts 1..kSplit-1
     const int64_t tile_rows = (int64_t)kTmRows * rpt;
     const int64_t n_tiles = (n_rows + tile_rows - 1) / tile_rows;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    auto st_off = [&](int k) { return reinterpret_cast<O *>(smem_raw + k * Cfg::kStageBytes); };
-    auto st_col = [&](int k) { return reinterpret_cast<int32_t *>(smem_raw + k * Cfg::kStageBytes + Cfg::kOffBytes); };
+    auto st_off = [&](int k) { return reinterpret_cast<O *>(smem_raw + k * stage); };
+    auto st_col = [&](int k) { return reinterpret_cast<int32_t *>(smem_raw + k * stage + Cfg::kOffBytes); };
     auto st_val = [&](int k) {
-        return reinterpret_cast<V *>(smem_raw + k * Cfg::kStageBytes + Cfg::kOffBytes + Cfg::kColBytes);
+        return reinterpret_cast<V *>(smem_raw + k * stage + Cfg::kOffBytes + Cfg::col_bytes(kCap));
     };
     if (tid == 0) {
         for (int k = 0; k < kTmStages; ++k) {
             mbar_init(&full[k], 1);
-            mbar_init(&empty[k], kTmRows / 32);
+            mbar_init(&empty[k], kTmRows * kSplit / 32);
         }
         fence_barrier_init();
     }
     __syncthreads();
 
-    if (warp == kTmRows / 32) {  // ------------------------------------------- producer
+    if (warp == kTmRows * kSplit / 32) {  // ---------------------------------- producer
         if (lane != 0) return;
         const int64_t nnz = ldo(off + n_rows);
         auto bounds = [&](int64_t t, int64_t &s, int64_t &e) {
@@ -266,29 +287,50 @@ __global__ void __launch_bounds__(kTmRows + 32) k_csr_tm(const O *__restrict__ o
         const int32_t *sc = st_col(k) - base;
         const V *sv = st_val(k) - base;
         const int64_t r0 = t * tile_rows;
-#pragma unroll
-        for (int q = 0; q < kTmMaxRpt; ++q) {
-            const int rl = tid + q * kTmRows;
-            if (q >= rpt || r0 + rl >= n_rows) break;
-            const int64_t s = (int64_t)so[rl], e = (int64_t)so[rl + 1];
+        auto row_sum = [&](int64_t s, int64_t e) {
             V sum = 0;
             if (base >= 0) {
-                for (int64_t j = s; j < e; j += 4) {  // 4 gathers in flight per thread
-                    int32_t c[4];
-                    V v[4];
+                for (int64_t j = s; j < e; j += kTmU) {  // kTmU gathers in flight per thread
+                    int32_t c[kTmU];
+                    V v[kTmU];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < kTmU; ++u) {
                         c[u] = j + u < e ? sc[j + u] : 0;
                         v[u] = j + u < e ? sv[j + u] : V(0);
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u)
+                    for (int u = 0; u < kTmU; ++u)
                         if (j + u < e) sum = fma_acc(sum, v[u], ld_x(x + c[u]));
                 }
             } else {
                 for (int64_t j = s; j < e; j += 4) sum = batch_dot<4, 1>(col, val, x, j, e, sum);
             }
-            y[r0 + rl] = sum;
+            return sum;
+        };
+        if constexpr (kSplit > 1) {  // rpt = 1 (host)
+            const int rl = tid % kTmRows, part = tid / kTmRows;
+            const bool act = r0 + rl < n_rows;
+            V sum = V(0);
+            if (act) {
+                const int64_t s = (int64_t)so[rl], e = (int64_t)so[rl + 1];
+                const int64_t chunk = (e - s + kSplit - 1) / kSplit;
+                const int64_t a = s + part * chunk, b = a + chunk < e ? a + chunk : e;
+                sum = row_sum(a, b);
+            }
+            if (part > 0) s_part[k][part - 1][rl] = sum;
+            asm volatile("bar.sync 1, %0;" ::"r"(kTmRows * kSplit) : "memory");  // consumers only
+            if (part == 0 && act) {
+#pragma unroll
+                for (int p = 1; p < kSplit; ++p) sum += s_part[k][p - 1][rl];  // fixed order
+                y[r0 + rl] = sum;
+            }
+        } else {
+#pragma unroll
+            for (int q = 0; q < kTmMaxRpt; ++q) {
+                const int rl = tid + q * kTmRows;
+                if (q >= rpt || r0 + rl >= n_rows) break;
+                y[r0 + rl] = row_sum((int64_t)so[rl], (int64_t)so[rl + 1]);
+            }
         }
         __syncwarp();
         if (lane == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(&empty[k])) : "memory");
@@ -577,6 +619,9 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
     __shared__ V s_prod[kMergeWarps][kPad];
     __shared__ int32_t s_mark[kMergeWarps][kPad];
     __shared__ V s_rowv[kMergeWarps][kWarpTile + 1];  // value of each row ending in the unit (+ the open one)
+    // let the PDL-launched carry fix-up be scheduled now: its griddepcontrol.wait still
+    // waits for this grid's completion and memory flush, only the launch latency is hidden
+    asm volatile("griddepcontrol.launch_dependents;");
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t wid = (int64_t)blockIdx.x * kMergeWarps + w;
     if (wid >= n_ranges) return;
@@ -782,6 +827,7 @@ __global__ void __launch_bounds__(256, kCooMinBlocks<V>) k_coo_wm(const int32_t 
                                                 V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_chunks,
                                                 int64_t cpw, int64_t n_ranges, int32_t *__restrict__ crow,
                                                 V *__restrict__ cval) {
+    asm volatile("griddepcontrol.launch_dependents;");  // early PDL trigger (see k_csr_merge)
     const int lane = threadIdx.x & 31;
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (wid >= n_ranges) return;
@@ -1226,6 +1272,18 @@ int wm_group(const kp_csr *A) {
     return G;
 }
 
+// CSR,TM stage capacity (nnz): the short-row default, or -- when 256 rows of the KNOWN mean
+// length overflow it -- a stage sized for 256 rows with 25 % slack (up to kCapMax).
+template <typename V, typename O>
+int tm_capacity(const kp_csr *A) {
+    using Cfg = TmCfg<V, O>;
+    const double mean = A->n_rows > 0 ? (double)A->nnz / (double)A->n_rows : 1.0;
+    const double need = 1.25 * kTmRows * mean + 128;
+    if (need <= Cfg::kCap) return Cfg::kCap;
+    const int64_t c = ((int64_t)need + 127) / 128 * 128;
+    return (int)(c < Cfg::kCapMax ? c : Cfg::kCapMax);
+}
+
 // CSR,TM rows per thread: tile window ~3/4 of a stage at the KNOWN mean row length.
 int tm_rows_per_thread(const kp_csr *A, int cap) {
     const double mean = A->n_rows > 0 ? (double)A->nnz / (double)A->n_rows : 1.0;
@@ -1429,9 +1487,13 @@ template <typename V, typename O>
 int tm_attrs() {
     static bool done = false;
     if (done) return KP_OK;
-    const int smem = (int)(kTmStages * TmCfg<V, O>::kStageBytes);
-    KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    const int smem = (int)(kTmStages * TmCfg<V, O>::stage_bytes(TmCfg<V, O>::kCapMax));
+    KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, true, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, false, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, true, kTmUWide, kTmSplitWide>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, false, kTmUWide, kTmSplitWide>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     done = true;
     return KP_OK;
 }
@@ -1470,9 +1532,11 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
         }
         case KP_CSR_TM: {
             using Cfg = TmCfg<V, O>;
-            const size_t smem = kTmStages * Cfg::kStageBytes;
+            const int cap = tm_capacity<V, O>(A);
+            const size_t smem = kTmStages * Cfg::stage_bytes(cap);
             const bool aligned = (((uintptr_t)col | (uintptr_t)val | (uintptr_t)off) & 15) == 0;
-            const int rpt = tm_rows_per_thread(A, Cfg::kCap);
+            const bool wide = cap > Cfg::kCap;  // medium rows: enlarged stages, split rows, 1 row / thread
+            const int rpt = wide ? 1 : tm_rows_per_thread(A, cap);
             const int64_t tiles = (R + (int64_t)kTmRows * rpt - 1) / ((int64_t)kTmRows * rpt);
             const int per_sm = (int)((227 * 1024) / (smem + 1024));
             const int64_t g = tiles < (int64_t)sms * per_sm ? tiles : (int64_t)sms * per_sm;
@@ -1480,8 +1544,15 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
                 const int rc = tm_attrs<V, O>();
                 if (rc) return rc;
             }
-            if (aligned) k_csr_tm<V, O, true><<<(unsigned)g, kTmRows + 32, smem, s>>>(off, col, val, x, y, R, rpt);
-            else k_csr_tm<V, O, false><<<(unsigned)g, kTmRows + 32, smem, s>>>(off, col, val, x, y, R, rpt);
+            constexpr unsigned bw = kTmRows * kTmSplitWide + 32, bn = kTmRows + 32;
+            if (aligned && wide)
+                k_csr_tm<V, O, true, kTmUWide, kTmSplitWide><<<(unsigned)g, bw, smem, s>>>(off, col, val, x, y, R, 1, cap);
+            else if (aligned)
+                k_csr_tm<V, O, true, 4, 1><<<(unsigned)g, bn, smem, s>>>(off, col, val, x, y, R, rpt, cap);
+            else if (wide)
+                k_csr_tm<V, O, false, kTmUWide, kTmSplitWide><<<(unsigned)g, bw, smem, s>>>(off, col, val, x, y, R, 1, cap);
+            else
+                k_csr_tm<V, O, false, 4, 1><<<(unsigned)g, bn, smem, s>>>(off, col, val, x, y, R, rpt, cap);
             KP_LAUNCHED();
             return KP_OK;
         }

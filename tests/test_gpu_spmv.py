@@ -167,3 +167,32 @@ def test_wide_x_half_wave(dtype, orc):
         kernels.spmv(A, x, k, y=y)
         ok, r = orc.spmv_check(y.cpu().numpy(), yref, absy, TOL[dtype])
         assert ok, (kernels.KERNELS[k], r)
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("index", ["int32", "int64"])
+def test_tm_medium_row_stages(dtype, index, orc):
+    """CSR,TM enlarged stages (mean row length > ~9: capacity from the known mean, two
+    consumer threads per row) on ragged row counts, means around and above the largest
+    stage (per-tile fallback to direct walks), and skewed tiles that overflow their stage."""
+    ms = [gen.banded(10_001, 10), gen.banded(70_003, 27), gen.constant_rows(33_333, 40, seed=6),
+          gen.banded(5_000, 60), gen.stencil27(23)]
+    # mean ~27 with a few 5000-long rows: the tiles holding them overflow the stage
+    R = 20_000
+    lens = np.full(R, 27)
+    lens[[17, 9000, 19_999]] = 5000
+    rows = np.repeat(np.arange(R), lens)
+    cols = np.concatenate([np.sort(np.random.default_rng(l + i).choice(20_000, l, replace=False))
+                           for i, l in enumerate(lens)])
+    ms.append(gen.from_coo("skewed_tiles", R, 20_000, torch.tensor(rows), torch.tensor(cols), 5))
+    for m in ms:
+        A = m.to_device_csr(dtype, index=index)
+        key = (m.name, dtype)
+        if key not in XS:
+            g = torch.Generator().manual_seed(5)
+            XS[key] = (torch.rand(m.n_cols, generator=g, dtype=torch.float64) * 2 - 1).to(dtype).cuda()
+        y = torch.full((A.n_rows,), float("nan"), dtype=dtype, device="cuda")
+        kernels.spmv(A, XS[key], kernels.CSR_TM, y=y)
+        torch.cuda.synchronize()
+        _check(m, A, kernels.CSR_TM, y, orc)
+        assert torch.equal(y, kernels.spmv(A, XS[key], kernels.CSR_TM))

@@ -33,6 +33,10 @@ MATS = {
     "pl": lambda d: (gen.powerlaw_rows(4_000_000, 16.0, 1.5, device=d), torch.float32),
     "const32": lambda d: (gen.constant_rows(4_000_000, 32, device=d), torch.float32),
     "C5": lambda d: (gen.config("C5", device=d), torch.float32),
+    # small / medium inputs: latency (launches, searches, fix-ups) dominates
+    "u1m": lambda d: (gen.uniform_random(500_000, 500_000, 1_000_000, seed=5, device=d), torch.float32),
+    "rmat15": lambda d: (gen.rmat(15, 16, device=d), torch.float32),
+    "st43": lambda d: (gen.stencil27(43, device=d), torch.float32),
     # fp64 variants (C4 is the only fp64 BASELINE config)
     "C2d": lambda d: (gen.config("C2", device=d), torch.float64),
     "band27d": lambda d: (gen.banded(4_000_000, 27, device=d), torch.float64),
