@@ -210,6 +210,8 @@ def _eager_costs(A, x, y, k, flush, ev, reps, cap_ms):
             ts.append(t)
         if t * 1e3 > cap_ms:
             break
+    if not ts:  # reps = 0 and under the cap: the one run is the sample
+        ts.append(t)
     return statistics.median(ts), tprep
 
 
