@@ -195,11 +195,14 @@ struct TmCfg {
 };
 
 // kSplit > 1 (medium-row stages): kSplit consumer threads per row, each summing a
-// contiguous part of it (consecutive rows stay in consecutive lanes, so the gathers stay
-// coalesced), parts combined through shared memory in a fixed order: kSplit x the gathers
-// in flight per tile.  Measured on C3 / band 27 / band 27 fp64 (fraction of HBM):
-// (U, split) = (16, 1) 0.63 / 0.72 / 0.83, (8, 2) 0.69-0.72 / 0.74-0.76 / 0.89-0.90,
-// (4, 2) 0.67 / 0.77 / 0.90, (16, 2) 0.53 / 0.57 / 0.91, (8, 3) 0.52 / 0.55 / 0.88.
+// contiguous part of it; a warp holds 32 / kSplit consecutive rows x kSplit parts
+// (consecutive rows in consecutive lanes, so the gathers stay coalesced) and combines the
+// parts with shuffles in a fixed order: kSplit x the gathers in flight per tile.
+// Measured on C3 / band 27 / band 27 fp64 (fraction of HBM), parts combined through
+// shared memory + a consumer barrier: (U, split) = (16, 1) 0.63 / 0.72 / 0.83, (8, 2)
+// 0.69-0.72 / 0.74-0.76 / 0.89-0.90, (4, 2) 0.67 / 0.77 / 0.90, (16, 2) 0.53 / 0.57 / 0.91,
+// (8, 3) 0.52 / 0.55 / 0.88; (8, 2) with the in-warp shuffle combine (no barrier, ncu
+// showed 17 % barrier stalls): 0.71 / 0.77 / 0.93.
 template <typename V, typename O, bool kTma, int kTmU, int kSplit>
 __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                          const V *__restrict__ val, const V *__restrict__ x,
@@ -209,7 +212,6 @@ __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__res
     extern __shared__ __align__(128) unsigned char smem_raw[];
     __shared__ __align__(8) uint64_t full[kTmStages], empty[kTmStages];
     __shared__ int64_t s_base[kTmStages];  // element index staged at col slot 0; -1 = direct
-    __shared__ V s_part[kTmStages][kSplit > 1 ? kSplit - 1 : 1][kSplit > 1 ? kTmRows : 1];  // parts 1..kSplit-1
     const int64_t tile_rows = (int64_t)kTmRows * rpt;
     const int64_t n_tiles = (n_rows + tile_rows - 1) / tile_rows;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -308,7 +310,10 @@ __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__res
             return sum;
         };
         if constexpr (kSplit > 1) {  // rpt = 1 (host)
-            const int rl = tid % kTmRows, part = tid / kTmRows;
+            // the kSplit parts of a row sit in the SAME warp (lane groups of 32 / kSplit
+            // consecutive rows), so the combine is a shuffle, not a CTA barrier
+            constexpr int kG = 32 / kSplit;
+            const int rl = warp * kG + (lane % kG), part = lane / kG;
             const bool act = r0 + rl < n_rows;
             V sum = V(0);
             if (act) {
@@ -317,13 +322,9 @@ __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__res
                 const int64_t a = s + part * chunk, b = a + chunk < e ? a + chunk : e;
                 sum = row_sum(a, b);
             }
-            if (part > 0) s_part[k][part - 1][rl] = sum;
-            asm volatile("bar.sync 1, %0;" ::"r"(kTmRows * kSplit) : "memory");  // consumers only
-            if (part == 0 && act) {
 #pragma unroll
-                for (int p = 1; p < kSplit; ++p) sum += s_part[k][p - 1][rl];  // fixed order
-                y[r0 + rl] = sum;
-            }
+            for (int o = kG * (kSplit / 2); o >= kG; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);  // fixed order
+            if (part == 0 && act) y[r0 + rl] = sum;
         } else {
 #pragma unroll
             for (int q = 0; q < kTmMaxRpt; ++q) {
