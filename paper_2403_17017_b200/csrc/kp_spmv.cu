@@ -562,10 +562,8 @@ __device__ __forceinline__ int64_t merge_search_global(const O *off, int64_t n_r
 
 // Warp-cooperative 32-ary version (5 rounds of 32 parallel probes for 2^25 items).
 template <typename O>
-__device__ __forceinline__ int64_t merge_search_warp(const O *off, int64_t n_rows, int64_t nnz, int64_t d) {
+__device__ __forceinline__ int64_t merge_search_warp_in(const O *off, int64_t d, int64_t lo, int64_t hi) {
     const int lane = threadIdx.x & 31;
-    int64_t lo = d - nnz > 0 ? d - nnz : 0;
-    int64_t hi = d < n_rows ? d : n_rows;
     while (hi - lo > 32) {
         const int64_t step = (hi - lo + 32) / 33;  // probes at lo + step*(lane+1) - 1
         int64_t p = lo + step * (lane + 1) - 1;
@@ -583,6 +581,41 @@ __device__ __forceinline__ int64_t merge_search_warp(const O *off, int64_t n_row
     const int64_t p = lo + lane;  // final <= 32 candidates: one probe per lane
     const bool gr = p < hi && ldo(off + p + 1) <= d - p - 1;
     return lo + __popc(__ballot_sync(0xffffffffu, gr));
+}
+template <typename O>
+__device__ __forceinline__ int64_t merge_search_warp(const O *off, int64_t n_rows, int64_t nnz, int64_t d) {
+    return merge_search_warp_in(off, d, d - nnz > 0 ? d - nnz : 0, d < n_rows ? d : n_rows);
+}
+
+// CTA-shared first round of the WO start search: the CTA's warps start at nearby diagonals,
+// so one 256-point grid of Q(p) = off[p+1] + p + 1 (strictly increasing; the merge
+// coordinate of diagonal d is #{p : Q(p) <= d}) over the union of their search intervals,
+// loaded once (one probe per thread), narrows every warp to one grid cell before its own
+// 32-ary search: one dependent round instead of log33(256) ~ 1.6 of the per-warp search.
+template <typename O>
+__device__ __forceinline__ int64_t merge_search_cta(const O *off, int64_t n_rows, int64_t nnz, int64_t d,
+                                                    int64_t d_first, int64_t d_last, int64_t *s_q) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t lo = d_first - nnz > 0 ? d_first - nnz : 0;
+    const int64_t hi = d_last < n_rows ? d_last : n_rows;
+    const int64_t step = (hi - lo + 256) / 257;
+    {
+        const int64_t p = lo + step * (tid + 1) - 1;
+        s_q[tid] = p < hi ? (int64_t)ldo(off + p + 1) + p + 1 : INT64_MAX;
+    }
+    __syncthreads();
+    int c = 0;
+#pragma unroll
+    for (int t = 0; t < 8; ++t) c += s_q[lane * 8 + t] <= d ? 1 : 0;
+    c = __reduce_add_sync(0xffffffffu, c);
+    int64_t l = c == 0 ? lo : lo + step * c;  // p_{c-1} + 1
+    int64_t h = c == 256 ? hi : lo + step * (c + 1) - 1;  // p_c
+    if (h > hi) h = hi;
+    const int64_t lo_d = d - nnz > 0 ? d - nnz : 0, hi_d = d < n_rows ? d : n_rows;
+    if (l < lo_d) l = lo_d;
+    if (h > hi_d) h = hi_d;
+    if (l > h) l = h;
+    return merge_search_warp_in(off, d, l, h);
 }
 
 constexpr int kWarpTile = 32 * kIPT;  // 256 merge items per unit
@@ -625,6 +658,19 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
     asm volatile("griddepcontrol.launch_dependents;");
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t wid = (int64_t)blockIdx.x * kMergeWarps + w;
+    int64_t r0 = 0;
+    // CSR,WO: in-kernel start search, first round shared by the CTA.  Graph A/B against the
+    // per-warp 32-ary search (per SpMV, same box): C4 fp64 149.5 -> 141.3 us, band 27
+    // 282.6 -> 272.4 us, C2 equal, small inputs +0.2..0.7 us per iteration (the CTA
+    // barrier); keeping both searches behind a size switch lost the large-input gain
+    // (code generation of the main loop), so WO always uses this one.
+    if constexpr (!kPrep) {
+        __shared__ int64_t s_q[kMergeWarps * 32];
+        const int64_t w0 = (int64_t)blockIdx.x * kMergeWarps;
+        const int64_t wl = w0 + kMergeWarps - 1 < n_ranges - 1 ? w0 + kMergeWarps - 1 : n_ranges - 1;
+        const int64_t wc = wid < n_ranges ? wid : wl;
+        r0 = merge_search_cta(off, n_rows, nnz, wc * upw * kWarpTile, w0 * upw * kWarpTile, wl * upw * kWarpTile, s_q);
+    }
     if (wid >= n_ranges) return;
     const int64_t total = n_rows + nnz;
     const int64_t u_begin = wid * upw;
@@ -633,9 +679,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
     int32_t *mark = s_mark[w];
     V *rowv = s_rowv[w];
     for (int t = lane; t < kPad; t += 32) mark[t] = 0;
-    int64_t r0;
     if (kPrep) r0 = part[wid];
-    else r0 = merge_search_warp(off, n_rows, nnz, u_begin * kWarpTile);
     int64_t row_start = ldo(off + r0);  // r0 < n_rows: the range starts before the last item
     V carry = V(0);
     const int jb = lane * kIPT;
