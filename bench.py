@@ -153,10 +153,18 @@ def run_ours(a):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    # one rank per GPU; KP_BENCH_DIST_BACKEND=gloo (test only) lets N ranks share the GPUs
+    # present so the multi-rank control flow can be exercised on a 1-GPU box
+    backend = os.environ.get("KP_BENCH_DIST_BACKEND", "nccl")
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     dev = torch.device("cuda", local)
     L = _lib.load()
 
