@@ -173,8 +173,8 @@ __global__ void __launch_bounds__(128) k_csr_bm(const O *__restrict__ off, const
 constexpr int kTmStages = 2;
 constexpr int kTmMaxRpt = 4;
 // gathers in flight per consumer thread: 4 for short-row stages (band 4: 0.81 of HBM vs
-// 0.70 at 8), kTmUWide for the enlarged medium-row stages
-constexpr int kTmUWide = 8;
+// 0.70 at 8) and for the enlarged medium-row stages (split rows, below)
+constexpr int kTmUWide = 4;
 constexpr int kTmSplitWide = 2;  // consumer threads per row in the medium-row stages
 // Medium rows (the tile window of 256 rows exceeds kCap at the known mean, e.g. 27-point
 // stencils) get a LARGER stage instead of the per-thread global walk: capacity sized from
@@ -202,7 +202,8 @@ struct TmCfg {
 // shared memory + a consumer barrier: (U, split) = (16, 1) 0.63 / 0.72 / 0.83, (8, 2)
 // 0.69-0.72 / 0.74-0.76 / 0.89-0.90, (4, 2) 0.67 / 0.77 / 0.90, (16, 2) 0.53 / 0.57 / 0.91,
 // (8, 3) 0.52 / 0.55 / 0.88; (8, 2) with the in-warp shuffle combine (no barrier, ncu
-// showed 17 % barrier stalls): 0.71 / 0.77 / 0.93.
+// showed 17 % barrier stalls): 0.71 / 0.77 / 0.93; then (4, 2): C3 195 -> 188 us, band 27
+// 184 -> 174 us, band 27 fp64 equal (graph A/B; (12, 2) 213 / 203 / 242 us).
 template <typename V, typename O, bool kTma, int kTmU, int kSplit>
 __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                          const V *__restrict__ val, const V *__restrict__ x,
