@@ -111,7 +111,9 @@ typedef struct kp_prepared {
 
 /* ------------------------------------------------------- drop-in backend (K1, K2) */
 /* Scratch for every reduction entry point; must be zeroed ONCE at allocation
- * (cudaMemset); the kernels leave it zeroed again after each call. */
+ * (cudaMemset); the kernels leave it zeroed again after each call, and every entry point
+ * below also re-zeroes its 16-byte ticket (async) before launching.  One workspace per
+ * stream: two passes that may overlap must not share one. */
 KP_API size_t kp_reduce_workspace_bytes(void);
 
 /* _kernels.length_stats (_core.pyx:15-33 / _pure.py:11-21):

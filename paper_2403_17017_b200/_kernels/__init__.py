@@ -43,8 +43,9 @@ def length_stats(row_offsets) -> tuple[int, int, int, int]:
     torch, t, off_type = _device_offsets(row_offsets)
     from ..device import reduce_workspace
     out = torch.empty(4, dtype=torch.int64, device=t.device)
-    rc = _lib.load().kp_length_stats(t.data_ptr(), off_type, t.numel(), out.data_ptr(),
-                                     reduce_workspace(t.device).data_ptr(), _lib.stream_handle())
+    with torch.cuda.device(t.device):
+        rc = _lib.load().kp_length_stats(t.data_ptr(), off_type, t.numel(), out.data_ptr(),
+                                         reduce_workspace(t.device).data_ptr(), _lib.stream_handle(None, t.device))
     _lib.check(rc, "kp_length_stats")
     lo, hi, s1, s2 = out.cpu().tolist()
     return int(lo), int(hi), int(s1), int(s2)
@@ -57,9 +58,10 @@ def wave_ceil_max_sum(row_offsets, divisor: int, wave_rows: int) -> int:
     torch, t, off_type = _device_offsets(row_offsets)
     from ..device import reduce_workspace
     out = torch.empty(1, dtype=torch.int64, device=t.device)
-    rc = _lib.load().kp_wave_ceil_max_sum(t.data_ptr(), off_type, t.numel(), int(divisor), int(wave_rows),
-                                          out.data_ptr(), reduce_workspace(t.device).data_ptr(),
-                                          _lib.stream_handle())
+    with torch.cuda.device(t.device):
+        rc = _lib.load().kp_wave_ceil_max_sum(t.data_ptr(), off_type, t.numel(), int(divisor), int(wave_rows),
+                                              out.data_ptr(), reduce_workspace(t.device).data_ptr(),
+                                              _lib.stream_handle(None, t.device))
     _lib.check(rc, "kp_wave_ceil_max_sum")
     return int(out.item())
 

@@ -146,7 +146,9 @@ def require_cuda():
     return torch
 
 
-def stream_handle(stream=None) -> int:
+def stream_handle(stream=None, device=None) -> int:
+    """cudaStream_t of ``stream``, else of ``device``'s (default: the current device's)
+    current torch stream."""
     import torch
-    s = stream if stream is not None else torch.cuda.current_stream()
+    s = stream if stream is not None else torch.cuda.current_stream(device)
     return int(s.cuda_stream)

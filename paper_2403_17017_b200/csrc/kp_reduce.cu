@@ -559,7 +559,16 @@ int grid_for(int64_t n_rows, int per_thread) {
     return (int)(want < cap ? want : cap);
 }
 
+// Defensive reset of the last-CTA ticket before every host-dispatched pass: the kernels
+// leave it zero, but a caller that shares one workspace between overlapping streams (or a
+// grid that died mid-way) would otherwise poison every later pass.  16 bytes, async.
+int reset_ticket(void *ws, cudaStream_t s) {
+    KP_CUDA_TRY(cudaMemsetAsync(ws, 0, 16, s));
+    return KP_OK;
+}
+
 int launch_k1(K1Args a, int32_t off_type, cudaStream_t s) {
+    if (reset_ticket(a.ws, s)) return KP_ECUDA;
     const bool aligned = ((uintptr_t)a.off & 15) == 0;
     if (off_type == KP_I32) {
         int g = grid_for(a.n_rows, 64);
@@ -742,6 +751,7 @@ int kp_wave_ceil_max_sum(const void *d_off, int32_t off_type, int64_t n_off, int
         return KP_OK;
     }
     RedWorkspace *ws = (RedWorkspace *)d_ws;
+    if (reset_ticket(ws, s)) return KP_ECUDA;
     if (off_type == KP_I32) return launch_wave((const int32_t *)d_off, n, divisor, wave_rows, d_out1, ws, s);
     if (off_type == KP_I64) return launch_wave((const int64_t *)d_off, n, divisor, wave_rows, d_out1, ws, s);
     return KP_EINVAL;

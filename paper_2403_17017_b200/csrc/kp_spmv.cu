@@ -1531,8 +1531,12 @@ int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, 
 // plan's graph capture so no attribute call happens inside a capture).
 template <typename V, typename O>
 int tm_attrs() {
-    static bool done = false;
-    if (done) return KP_OK;
+    // the attribute is per device context: one bit per device (a process may drive several)
+    static unsigned long long done = 0;
+    int dev = 0;
+    KP_CUDA_TRY(cudaGetDevice(&dev));
+    const unsigned long long bit = 1ull << (dev & 63);
+    if (done & bit) return KP_OK;
     const int smem = (int)(kTmStages * TmCfg<V, O>::stage_bytes(TmCfg<V, O>::kCapMax));
     KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, true, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, false, 4, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -1540,7 +1544,7 @@ int tm_attrs() {
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     KP_CUDA_TRY(cudaFuncSetAttribute(k_csr_tm<V, O, false, kTmUWide, kTmSplitWide>,
                                      cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    done = true;
+    done |= bit;
     return KP_OK;
 }
 

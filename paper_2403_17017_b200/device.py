@@ -22,15 +22,18 @@ _I32_MAX = 2**31 - 1
 _red_ws: dict = {}
 
 
-def reduce_workspace(device=None):
-    """Zeroed K1/K2 scratch for `device` (the kernels leave it zeroed)."""
+def reduce_workspace(device=None, stream=None):
+    """Zeroed K1/K2 scratch for (`device`, `stream`) -- the kernels leave it zeroed.  One
+    per stream: K1's last-CTA ticket counter must never see two grids at once, and launches
+    on different streams may overlap."""
     torch = _lib.require_cuda()
     dev = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
-    ws = _red_ws.get(dev)
+    key = (dev, _lib.stream_handle(stream, dev))
+    ws = _red_ws.get(key)
     if ws is None:
         n = int(_lib.load().kp_reduce_workspace_bytes())
         ws = torch.zeros(n, dtype=torch.uint8, device=dev)
-        _red_ws[dev] = ws
+        _red_ws[key] = ws
     return ws
 
 

@@ -27,6 +27,7 @@ class PredictorResult:
     accuracy: float
     error_vs_oracle: float
     rows: list = field(default_factory=list)  # (matrix, chosen kernel, overhead, cost)
+    substituted: int = 0  # fixed kernels only: missing entries replaced by the worst present one
 
 
 @dataclass
@@ -44,9 +45,13 @@ def oracle_choice(row, k: int) -> int:
     return dataset.fastest_kernel(row.timings(), k)
 
 
-def _cost(row, K, k):
+def _cost(row, K, k, fixed: bool = False):
+    """Realised cost of kernel K.  A missing kernel costs +inf, so a model
+    that predicts it is maximally penalised; only FIXED-kernel baselines substitute the
+    worst present kernel, so their totals (the geomean's numerators) stay
+    finite.  Such substitutions are counted in ``PredictorResult.substituted``."""
     c = row.cost(K, k)
-    if not np.isfinite(c):  # worst present kernel substitutes a missing entry
+    if fixed and not np.isfinite(c):
         c = max(row.cost(j, k) for j in range(len(row.timings())) if np.isfinite(row.cost(j, k)))
     return c
 
@@ -59,12 +64,13 @@ def evaluate(model: seer.SeerModel, rows, k: int) -> EvalReport:
     nk = len(model.kernels)
     preds = {}
 
-    def run(name, choose):
+    def run(name, choose, fixed=False):
         res = PredictorResult(0.0, 0.0, 0.0)
         hits = 0
         for r in rows:
             kern, over = choose(r)
-            cost = _cost(r, kern, k) + over
+            cost = _cost(r, kern, k, fixed) + over
+            res.substituted += int(fixed and not np.isfinite(r.cost(kern, k)))
             orc = oracle_choice(r, k)
             res.rows.append((r.name, kern, over, cost))
             res.total_realized_cost += cost
@@ -83,7 +89,7 @@ def evaluate(model: seer.SeerModel, rows, k: int) -> EvalReport:
         return kern, (r.collection_time if path == seer.USE_GATHERED else 0.0)
     run("selector", sel)
     for K in range(nk):
-        run(model.kernels[K], lambda r, K=K: (K, 0.0))
+        run(model.kernels[K], lambda r, K=K: (K, 0.0), fixed=True)
     return EvalReport(k, tuple(model.kernels), preds)
 
 

@@ -16,7 +16,6 @@ scope for the runtime path).
 
 from __future__ import annotations
 
-import ctypes
 from dataclasses import dataclass
 from typing import Callable
 
@@ -73,14 +72,25 @@ def gather_outcome(m, out=None, stream=None):
     t, off_type = _offsets_on_device(m)
     if out is None:
         out = torch.empty(_lib.OUTCOME_BYTES, dtype=torch.uint8, device=t.device)
-    rc = _lib.load().kp_gather_features(t.data_ptr(), off_type, int(m.n_rows), int(m.n_cols), out.data_ptr(),
-                                        reduce_workspace(t.device).data_ptr(), _lib.stream_handle(stream))
+    with torch.cuda.device(t.device):
+        rc = _lib.load().kp_gather_features(t.data_ptr(), off_type, int(m.n_rows), int(m.n_cols), out.data_ptr(),
+                                            reduce_workspace(t.device, stream).data_ptr(),
+                                            _lib.stream_handle(stream, t.device))
     _lib.check(rc, "kp_gather_features")
     return out
 
 
-def decode_outcome(buf) -> _lib.kp_outcome:
-    raw = bytes(buf.cpu().numpy().tobytes()) if hasattr(buf, "cpu") else bytes(buf)
+def decode_outcome(buf, stream=None) -> _lib.kp_outcome:
+    """Host copy of a device (or host) kp_outcome.  ``stream``: the stream the outcome was
+    written on -- the copy is ordered after it (the D2H itself runs on the buffer device's
+    current stream, which waits for ``stream`` first)."""
+    if hasattr(buf, "cpu"):
+        if stream is not None and buf.is_cuda:
+            import torch
+            torch.cuda.current_stream(buf.device).wait_stream(stream)
+        raw = bytes(buf.cpu().numpy().tobytes())
+    else:
+        raw = bytes(buf)
     return _lib.kp_outcome.from_buffer_copy(raw)
 
 
@@ -103,6 +113,3 @@ def gather_features(m, clock: Clock | None = None) -> GatheredFeatures:
     del torch
     return GatheredFeatures(o.max_d, o.min_d, o.mean_d, o.var_d, elapsed)
 
-
-def _outcome_struct_bytes() -> int:
-    return ctypes.sizeof(_lib.kp_outcome)

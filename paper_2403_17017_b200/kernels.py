@@ -75,8 +75,9 @@ def prepare(A, kernel, *, ell_cap: int | None = None, stream=None, cache: bool =
     _lib.check(L.kp_prepare_bytes(k, ctypes.byref(A.struct), cap, ctypes.byref(nbytes)), "kp_prepare_bytes")
     buf = torch.empty(max(int(nbytes.value), 256), dtype=torch.uint8, device=A.device)
     st = _lib.kp_prepared()
-    _lib.check(L.kp_prepare(k, ctypes.byref(A.struct), cap, buf.data_ptr(), buf.numel(), ctypes.byref(st),
-                            _lib.stream_handle(stream)), "kp_prepare")
+    with torch.cuda.device(A.device):
+        _lib.check(L.kp_prepare(k, ctypes.byref(A.struct), cap, buf.data_ptr(), buf.numel(), ctypes.byref(st),
+                                _lib.stream_handle(stream, A.device)), "kp_prepare")
     P = Prepared(k, buf, st, cap)
     if cache:
         A._prepared[k] = P
@@ -86,7 +87,9 @@ def prepare(A, kernel, *, ell_cap: int | None = None, stream=None, cache: bool =
 _ws_cache: dict = {}
 
 
-def spmv_workspace(A: DeviceCSR, kernel: int):
+def spmv_workspace(A: DeviceCSR, kernel: int, stream=None):
+    """Carry scratch of a split-row kernel, one per (device, kernel, stream): launches on
+    different streams may overlap and must not share carries.  Grows to the largest matrix."""
     torch = _lib.require_cuda()
     nbytes = ctypes.c_size_t(0)
     _lib.check(_lib.load().kp_spmv_workspace_bytes(kernel, ctypes.byref(A.struct), ctypes.byref(nbytes)),
@@ -94,7 +97,7 @@ def spmv_workspace(A: DeviceCSR, kernel: int):
     n = int(nbytes.value)
     if n == 0:
         return None
-    key = (A.device, kernel)  # one per device and kernel; grows to the largest matrix
+    key = (A.device, kernel, _lib.stream_handle(stream, A.device))
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < n:
         ws = torch.empty(n, dtype=torch.uint8, device=A.device)
@@ -107,20 +110,34 @@ def spmv(A, x, kernel, *, y=None, prepared: Prepared | None = None, stream=None)
     torch = _lib.require_cuda()
     A = as_device(A)
     k = kernel_index(kernel)
-    if x.dtype != A.values.dtype or not x.is_cuda or x.numel() != A.n_cols:
-        raise ValueError("x must be a CUDA tensor of n_cols elements with the matrix value dtype")
+    check_vector(x, A, A.n_cols, "x")
     x = x.contiguous()
     if y is None:
         y = torch.empty(A.n_rows, dtype=A.values.dtype, device=A.device)
+    else:
+        check_vector(y, A, A.n_rows, "y", out=True)
     if k in NEEDS_PREP and prepared is None:
         prepared = prepare(A, k, stream=stream)
-    ws = spmv_workspace(A, k)
+    ws = spmv_workspace(A, k, stream)
     P = ctypes.byref(prepared.struct) if prepared is not None else None
-    rc = _lib.load().kp_spmv(k, ctypes.byref(A.struct), P, x.data_ptr(), y.data_ptr(),
-                             0 if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
-                             _lib.stream_handle(stream))
+    with torch.cuda.device(A.device):
+        rc = _lib.load().kp_spmv(k, ctypes.byref(A.struct), P, x.data_ptr(), y.data_ptr(),
+                                 0 if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
+                                 _lib.stream_handle(stream, A.device))
     _lib.check(rc, f"kp_spmv[{KERNELS[k]}]")
     return y
+
+
+def check_vector(v, A, n: int, name: str, out: bool = False) -> None:
+    """x / y contract of the C-ABI: a CUDA tensor on A's device with A's value dtype and
+    at least ``n`` elements (exactly n for an input); outputs must also be contiguous,
+    since the kernels write n elements through the raw pointer."""
+    ok = (v.is_cuda and v.device == A.device and v.dtype == A.values.dtype and
+          (v.numel() >= n if out else v.numel() == n) and (v.is_contiguous() or not out))
+    if not ok:
+        raise ValueError(f"{name} must be a {'contiguous ' if out else ''}CUDA tensor on {A.device} with "
+                         f"{'>= ' if out else ''}{n} elements of {A.values.dtype} (got {tuple(v.shape)} "
+                         f"{v.dtype} on {v.device})")
 
 
 def spmv_bcast(A, x, kernel, dests, self_index: int, *, prepared: Prepared | None = None, stream=None):
@@ -134,17 +151,19 @@ def spmv_bcast(A, x, kernel, dests, self_index: int, *, prepared: Prepared | Non
         raise ValueError("fused exchange is implemented for the merge-path kernels (CSR,MP / CSR,WO)")
     if not 1 <= len(dests) <= _lib.KP_MAX_PEERS or not 0 <= self_index < len(dests):
         raise ValueError("1..8 destinations and a valid self index")
+    check_vector(x, A, A.n_cols, "x")
     for d in dests:
-        if d.dtype != A.values.dtype or d.numel() < A.n_rows:
-            raise ValueError("each destination needs n_rows elements of the matrix value dtype")
+        if d.dtype != A.values.dtype or d.numel() < A.n_rows or not d.is_contiguous() or not d.is_cuda:
+            raise ValueError("each destination needs n_rows contiguous elements of the matrix value dtype")
     if k in NEEDS_PREP and prepared is None:
         prepared = prepare(A, k, stream=stream)
     pe = _lib.kp_peers()
     for i, d in enumerate(dests):
         pe.y[i] = d.data_ptr()
     pe.n, pe.self = len(dests), int(self_index)
-    ws = spmv_workspace(A, k)
+    ws = spmv_workspace(A, k, stream)
     P = ctypes.byref(prepared.struct) if prepared is not None else None
-    _lib.check(_lib.load().kp_spmv_bcast(k, ctypes.byref(A.struct), P, x.data_ptr(), ctypes.byref(pe),
-                                         0 if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
-                                         _lib.stream_handle(stream)), f"kp_spmv_bcast[{KERNELS[k]}]")
+    with torch.cuda.device(A.device):
+        _lib.check(_lib.load().kp_spmv_bcast(k, ctypes.byref(A.struct), P, x.data_ptr(), ctypes.byref(pe),
+                                             0 if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
+                                             _lib.stream_handle(stream, A.device)), f"kp_spmv_bcast[{KERNELS[k]}]")

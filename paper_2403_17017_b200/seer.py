@@ -23,7 +23,7 @@ from dataclasses import dataclass
 import numpy as np
 
 from . import _lib
-from .dataset import fastest_kernel, total_cost
+from .dataset import fastest_kernel
 from .dtree import DecisionTree, leaf_tree, train_tree
 from .kernels import KERNELS, NEEDS_PREP, prepare, spmv
 
@@ -116,9 +116,11 @@ def select_async(model: SeerModel, A, k: int, out=None, stream=None):
     sel, kn, ga = model.device_trees(A.device)
     if out is None:
         out = torch.empty(_lib.OUTCOME_BYTES, dtype=torch.uint8, device=A.device)
-    rc = _lib.load().kp_seer_select(A.row_offsets.data_ptr(), A.off_type, A.n_rows, A.n_cols, A.nnz, int(k),
-                                    sel.data_ptr(), kn.data_ptr(), ga.data_ptr(), out.data_ptr(),
-                                    reduce_workspace(A.device).data_ptr(), _lib.stream_handle(stream))
+    with torch.cuda.device(A.device):
+        rc = _lib.load().kp_seer_select(A.row_offsets.data_ptr(), A.off_type, A.n_rows, A.n_cols, A.nnz, int(k),
+                                        sel.data_ptr(), kn.data_ptr(), ga.data_ptr(), out.data_ptr(),
+                                        reduce_workspace(A.device, stream).data_ptr(),
+                                        _lib.stream_handle(stream, A.device))
     _lib.check(rc, "kp_seer_select")
     return out
 
@@ -173,7 +175,7 @@ class SeerRunner:
         torch = _lib.require_cuda()
         from .features import decode_outcome
         buf = select_async(self.model, A, k, stream=stream)
-        o = decode_outcome(buf)
+        o = decode_outcome(buf, stream)  # ordered after the selection on `stream`
         kern = int(o.kernel)
         P = prepare(A, kern, stream=stream) if kern in NEEDS_PREP else None
         if y is None:
@@ -209,9 +211,13 @@ class SeerPlan:
         torch = _lib.require_cuda()
         from .device import as_device
         from .kernels import default_ell_cap
+        from .kernels import check_vector
         self.A = as_device(A)
-        if x.dtype != self.A.values.dtype or y.dtype != self.A.values.dtype:
-            raise ValueError("x / y must have the matrix value dtype")
+        # the graph binds raw pointers: x / y must stay valid, sized and on A's device
+        check_vector(x, self.A, self.A.n_cols, "x")
+        check_vector(y, self.A, self.A.n_rows, "y", out=True)
+        if not x.is_contiguous():
+            raise ValueError("x must be contiguous (the plan binds its pointer)")
         self.x, self.y, self.k = x, y, int(k)
         L = _lib.load()
         cap = int(ell_cap) if ell_cap else default_ell_cap(self.A)
@@ -232,17 +238,19 @@ class SeerPlan:
         cap_stream = torch.cuda.Stream(device=dev)  # graph capture needs a created stream
         torch.cuda.synchronize(dev)
         handle = ctypes.c_void_p()
-        rc = L.kp_seer_plan_create(ctypes.byref(self.A.struct), self.k, cap, sel.data_ptr(), kn.data_ptr(),
-                                   ga.data_ptr(), x.data_ptr(), y.data_ptr(), self.buf.data_ptr(), self.buf.numel(),
-                                   self.red.data_ptr(), self.out.data_ptr(), ctypes.byref(handle),
-                                   int(cap_stream.cuda_stream))
+        with torch.cuda.device(dev):
+            rc = L.kp_seer_plan_create(ctypes.byref(self.A.struct), self.k, cap, sel.data_ptr(), kn.data_ptr(),
+                                       ga.data_ptr(), x.data_ptr(), y.data_ptr(), self.buf.data_ptr(), self.buf.numel(),
+                                       self.red.data_ptr(), self.out.data_ptr(), ctypes.byref(handle),
+                                       int(cap_stream.cuda_stream))
         _lib.check(rc, "kp_seer_plan_create")
         torch.cuda.synchronize(dev)
         self._handle = handle
         self._L = L
 
     def launch(self, stream=None) -> None:
-        _lib.check(self._L.kp_seer_plan_launch(self._handle, _lib.stream_handle(stream)), "kp_seer_plan_launch")
+        _lib.check(self._L.kp_seer_plan_launch(self._handle, _lib.stream_handle(stream, self.A.device)),
+                   "kp_seer_plan_launch")
 
     def outcome(self):
         from .features import decode_outcome
@@ -414,24 +422,18 @@ def realized_cost(model: SeerModel, row, k: int) -> tuple[float, int, int]:
 
 
 def geomean_speedup(rows, model: SeerModel, k: int) -> dict:
-    """geomean over fixed kernels K of total(K) / total(selector),
-    totals summed over ``rows``; also the best-fixed-kernel aggregate ratio."""
-    sel = sum(realized_cost(model, r, k)[0] for r in rows)
-    nk = len(model.kernels)
-    fixed = []
-    for K in range(nk):
-        tot = 0.0
-        for r in rows:
-            c = r.cost(K, k)
-            if not np.isfinite(c):  # SPEC.md:495 fallback: worst present kernel
-                c = max(r.cost(j, k) for j in range(nk) if np.isfinite(r.cost(j, k)))
-            tot += c
-        fixed.append(tot)
-    ratios = [f / sel for f in fixed]
+    """geomean over fixed kernels K of total(K) / total(selector), totals
+    summed over ``rows``; also the best-fixed-kernel aggregate ratio.  Delegates to
+    ``evaluate.evaluate`` so the missing-kernel rules are the eval module's: +inf for the
+    selector's own choices, worst-present substitution only in the fixed-kernel totals."""
+    from . import evaluate as ev
+    rep = ev.evaluate(model, list(rows), k)
+    sel = rep.predictors["selector"].total_realized_cost
+    fixed = [rep.predictors[K].total_realized_cost for K in rep.kernels]
     return {"selector_total": sel, "fixed_totals": fixed,
-            "geomean_vs_fixed": float(np.exp(np.mean(np.log(ratios)))),
+            "geomean_vs_fixed": ev.geomean_speedup(rep),
             "vs_best_fixed": min(fixed) / sel,
-            "oracle_total": sum(min(r.cost(j, k) for j in range(nk)) for r in rows)}
+            "oracle_total": rep.predictors["oracle"].total_realized_cost}
 
 
 def bootstrap_model() -> SeerModel:
@@ -463,6 +465,3 @@ def bootstrap_model() -> SeerModel:
     st = leaf_tree(USE_GATHERED, 2, 4, KNOWN_SCHEMA)
     return SeerModel(kt, gt, st, KERNELS, {"source": "bootstrap rules (not B200-measured)"})
 
-
-def total_cost_of(row, kernel, k):
-    return total_cost(row.runtime[kernel], row.preprocess[kernel], k)
