@@ -2,24 +2,33 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload C2]
 
-One STEP = the Seer hot path over one matrix (T_seer): fused selection
-(selector tree -> gathered feature pass -> gathered/known tree, one kernel), the chosen
-kernel's preprocessing (not cached across steps: charged every step), then k SpMV
-iterations.  Default workload = BASELINE configs[1] (C2: R-MAT scale 20, edge factor 16,
-permuted, fp32, k = 1), generated on the device with a counter-based hash (synthetic).
+One STEP = the Seer hot path over one matrix (T_seer): selection (selector tree ->
+gathered feature pass + gathered tree, or the known tree), the chosen kernel's preprocessing
+(charged every step) and k SpMV iterations, launched as one CUDA graph (kp_seer_plan).
+
+N = 1 (default): workload C2 = BASELINE configs[1] (R-MAT scale 20, edge factor 16, permuted,
+fp32, k = 1), generated on the device with a counter-based hash (synthetic data).  The same
+line carries `per_config` (C1, C3 k = 100, C4 fp64: Seer vs every fixed kernel, roofline of
+the chosen kernel, e2e, CPU baseline) and `favourable` (every kernel on the input BASELINE
+names for it, by its own byte model).
+N > 1: workload C5 = BASELINE configs[4] (R-MAT scale 26, ~1.06 B nnz, 20 power iterations),
+row-sharded over the ranks (nnz-balanced), y exchanged every iteration; strong scaling.
+`python bench.py --gpus N` without torchrun spawns N local ranks itself (NCCL, one GPU per
+rank; with fewer GPUs than ranks the ranks share GPUs over gloo -- control-flow check only).
 
 value      = CSR algorithmic bytes x k / device time of the step   [GB/s]
-             (bytes = nnz*(4+4) + (R+1)*4 + C*4 + R*4, x counted once; inputs resident)
+             (bytes = nnz*(4+sv) + (R+1)*so + C*sv + R*sv, x counted once; inputs resident)
 e2e        = same metric through the public API with HOST buffers: pinned host CSR + x
-             copied H2D, the Seer pipeline, y copied D2H, all inside the timed region
+             copied H2D, the Seer plan, y copied D2H, all inside the timed region
 roofline   = the chosen SpMV op's own byte model / its CUDA-event duration vs the
              measured HBM copy bandwidth (MEASURED_PEAKS.json)
-sweep      = every fixed kernel's prep + k*SpMV on the same matrix; geomean and best-fixed
-             speedups of Seer against them (the paper's 6.5x / 2x metrics)
-cpu_baseline = the oracle port on this host (OpenMP CPU SpMV + compiled reference
-             length_stats + restated predict), bounded ~10 s sample, rank 0 only
-L2: the 141 MB matrix exceeds the 126 MB L2 and a 512 MB buffer is rewritten between
-steps (outside the timed events) -> config["l2"] = "flushed".
+sweep      = every fixed kernel's prep + k SpMV captured as a graph like the plan (total),
+             and its prep alone and its k SpMVs alone as separate graphs in the same cache
+             state (L2 flushed before each launch) -> prep_us, spmv_us
+cpu_baseline = the oracle port on this host: the faithful CPU Seer (selector, feature pass
+             through the compiled reference length_stats ONLY on the gathered path,
+             SPEC.md:388, known/gathered tree) + k OpenMP CPU SpMVs; bounded sample, rank 0
+L2: every timed launch is preceded by a 512 MB buffer rewrite (outside the events).
 """
 
 from __future__ import annotations
@@ -38,6 +47,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 FALLBACK_HBM_GBS = 6650.0  # /opt/skills/guides/B200_PROFILING.md fallback
+METRIC = "Seer-selected SpMV GB/s (% HBM roofline) and geomean speedup vs best fixed kernel"
 
 
 def _peak_hbm():
@@ -55,14 +65,22 @@ def _args():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--workload", default=None, choices=["C1", "C2", "C3", "C4", "C5"],
+                    help="default: C2 at one GPU, C5 (row-sharded) at N > 1")
     ap.add_argument("--iters", type=int, default=None, help="SpMV iterations k (default per config)")
+    ap.add_argument("--scale", type=int, default=26, help="C5 R-MAT scale (26 = BASELINE configs[4])")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip per_config (C1, C3, C4) and favourable")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--exchange", default="auto", choices=["auto", "fused", "nccl"],
-                    help="C5: y exchange (fused epilogue stores over NVLink, or NCCL all-gather)")
-    return ap.parse_args()
+    ap.add_argument("--config-cpu-seconds", type=float, default=4.0)
+    ap.add_argument("--exchange", default="auto", choices=["auto", "fused", "nccl", "host"],
+                    help="C5: y exchange (fused epilogue stores over NVLink, NCCL all-gather, or host staging)")
+    ap.add_argument("--watchdog-s", type=float, default=300.0, help="NCCL watchdog timeout (multi-rank)")
+    a = ap.parse_args()
+    if a.workload is None:
+        a.workload = "C5" if a.gpus > 1 else "C2"
+    return a
 
 
 CFG = {  # BASELINE.json configs -> (k, dtype, description)
@@ -71,7 +89,20 @@ CFG = {  # BASELINE.json configs -> (k, dtype, description)
     "C3": (100, "float32", "27-point stencil 159^3 (R=4,019,679, 107.2M nnz), fp32, k=100"),
     "C4": (1, "float64", "skewed 2M rows: Poisson(8) + 4 rows x 1M nnz, fp64, k=1"),
     "C5": (20, "float32", "R-MAT s26 ef16 row-stochastic (64M rows, ~1.0B nnz), fp32, 20 power iterations, "
-                          "row-sharded over the ranks with an NCCL all-gather of y per iteration"),
+                          "row-sharded over the ranks, y exchanged every iteration"),
+}
+
+# BASELINE-declared favourable input per kernel (configs[2] ELL, configs[3] merge path) and,
+# for the other schedules, the regular input their schedule is built for
+FAVOURABLE = {
+    "Adaptive-CSR": ("band2k", "band 65,536 x 2048 (long regular rows)"),
+    "CSR,BM": ("band2k", "band 65,536 x 2048 (one CTA per long row)"),
+    "CSR,MP": ("C4", "BASELINE configs[3] (merge-path-favourable), fp64"),
+    "CSR,WM": ("band2k", "band 65,536 x 2048 (32 lanes per long row)"),
+    "CSR,WO": ("C4", "BASELINE configs[3] (merge-path-favourable), fp64"),
+    "CSR,TM": ("band27", "band 4M x 27 (thread per short regular row)"),
+    "COO,WM": ("band4", "band 32M x 4 (row-sorted COO, short rows)"),
+    "ELL,TM": ("C3", "BASELINE configs[2] (ELL-favourable 27-point stencil)"),
 }
 
 
@@ -138,260 +169,317 @@ def _load_model():
     return seer.bootstrap_model(), "bootstrap rules (no B200 bundle yet)"
 
 
-def _make_matrix(name, device):
+def _make_matrix(name, device, scale=26):
     from paper_2403_17017_b200 import gen
-    return gen.config(name, device=device)
+    if name == "C5" and scale != 26:
+        return gen.rmat(scale, 16, seed=42, device=device, values="stochastic")
+    if name in CFG:
+        return gen.config(name, device=device)
+    return {"band2k": lambda: gen.banded(65_536, 2048, device=device),
+            "band27": lambda: gen.banded(4_000_000, 27, device=device),
+            "band4": lambda: gen.banded(32_000_000, 4, device=device)}[name]()
 
 
-# ------------------------------------------------------------------------ our arm
-def run_ours(a):
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+class Timer:
+    """CUDA-event timing on the current stream with an L2 flush before every launch."""
+
+    def __init__(self, dev):
+        import torch
+        self.torch = torch
+        self.flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def ev(self):
+        return self.torch.cuda.Event(enable_timing=True)
+
+    def direct(self, fn, reps):
+        """fn enqueues work (e.g. a plan graph launch); seconds per call, each timed alone."""
+        out = []
+        for _ in range(reps):
+            self.flush.zero_()
+            e0, e1 = self.ev(), self.ev()
+            e0.record()
+            fn()
+            e1.record()
+            e1.synchronize()
+            out.append(e0.elapsed_time(e1) * 1e-3)
+        return out
+
+    def graph(self, fn, reps, warm=1):
+        """fn captured once as a CUDA graph (like the Seer plan), replayed `reps` times."""
+        torch = self.torch
+        fn()
+        cs = torch.cuda.Stream()
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=cs):
+            fn()
+        for _ in range(warm):
+            g.replay()
+        torch.cuda.synchronize()
+        out = self.direct(g.replay, reps)
+        del g
+        return out
+
+
+# ------------------------------------------------------------------------ one workload, one GPU
+def measure(name, dev, model, a, *, steps, warmup, headline=False, sweep=True, e2e=True, cpu_seconds=0.0):
+    """The Seer plan on BASELINE config `name` (device-resident, L2 flushed), the chosen SpMV
+    alone (roofline), the per-kernel sweep and -- optionally -- e2e through host buffers and
+    the faithful CPU Seer on this host's cores.  Returns a dict of the line's fields."""
     import torch
-    import torch.distributed as dist
     from paper_2403_17017_b200 import _lib, kernels, seer
-    from paper_2403_17017_b200.features import decode_outcome
-    from paper_2403_17017_b200.device import DeviceCSR
-
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    rank = int(os.environ.get("RANK", "0"))
-    # one rank per GPU; KP_BENCH_DIST_BACKEND=gloo (test only) lets N ranks share the GPUs
-    # present so the multi-rank control flow can be exercised on a 1-GPU box
-    backend = os.environ.get("KP_BENCH_DIST_BACKEND", "nccl")
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    if backend != "nccl":
-        local %= torch.cuda.device_count()
-    torch.cuda.set_device(local)
-    if world > 1:
-        if backend == "nccl":
-            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-        else:
-            dist.init_process_group(backend)
-    dev = torch.device("cuda", local)
     L = _lib.load()
-
-    k_default, dt_name, desc = CFG[a.workload]
-    k = a.iters or k_default
+    k_default, dt_name, desc = CFG[name]
+    k = a.iters if (headline and a.iters) else k_default
     dtype = getattr(torch, dt_name)
-    m = _make_matrix(a.workload, dev)
+    m = _make_matrix(name, dev)
     A = m.to_device_csr(dtype, device=dev)
     del m
     R, C, Z = A.n_rows, A.n_cols, A.nnz
     sv, so = A.values.element_size(), A.row_offsets.element_size()
     bytes_csr = csr_bytes(R, C, Z, sv, so)
-    model, model_src = _load_model()
     g = torch.Generator(device=dev).manual_seed(1234)
     x = (torch.rand(C, device=dev, dtype=torch.float64, generator=g) * 2 - 1).to(dtype)
     y = torch.empty(R, device=dev, dtype=dtype)
-    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
-    obuf = torch.empty(_lib.OUTCOME_BYTES, dtype=torch.uint8, device=dev)
-    ohost = torch.empty(_lib.OUTCOME_BYTES, dtype=torch.uint8, pin_memory=True)
+    T = Timer(dev)
 
-    def read_outcome():
-        ohost.copy_(obuf, non_blocking=True)
-        stream.synchronize()
-        return decode_outcome(ohost)
-
-    ev = lambda: torch.cuda.Event(enable_timing=True)  # noqa: E731
-
-    def seer_step(AA, xx, yy, marks=None):
-        seer.select_async(model, AA, k, out=obuf)
-        o = read_outcome()
-        kern = int(o.kernel)
-        P = kernels.prepare(AA, kern, cache=False) if kern in kernels.NEEDS_PREP else None
-        if marks is not None:
-            marks[0].record()
-        for _ in range(k):
-            kernels.spmv(AA, xx, kern, y=yy, prepared=P)
-        if marks is not None:
-            marks[1].record()
-        return o, P
-
-    def fixed_step(kern, marks=None):
-        P = kernels.prepare(A, kern, cache=False) if kern in kernels.NEEDS_PREP else None
-        if marks is not None:
-            marks[0].record()
-        for _ in range(k):
-            kernels.spmv(A, x, kern, y=y, prepared=P)
-        if marks is not None:
-            marks[1].record()
-        return P
-
-    def timed(kk, steps, warm):
-        """Fixed kernel kk: prep + k SpMVs captured as one CUDA graph (launched like the
-        Seer plan), plus an eager pass with events around the SpMVs for the split."""
-        fixed_step(kk)
-        cs = torch.cuda.Stream()
-        torch.cuda.synchronize()
-        gr = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(gr, stream=cs):
-            fixed_step(kk)
-        for _ in range(warm):
-            gr.replay()
-            fixed_step(kk)
-        torch.cuda.synchronize()
-        tot, inner = [], []
-        for _ in range(steps):
-            flush.zero_()
-            e0, e1 = ev(), ev()
-            e0.record()
-            gr.replay()
-            e1.record()
-            e1.synchronize()
-            tot.append(e0.elapsed_time(e1) * 1e-3)
-            flush.zero_()
-            m0, m1 = ev(), ev()
-            fixed_step(kk, (m0, m1))
-            m1.synchronize()
-            inner.append(m0.elapsed_time(m1) * 1e-3)
-        del gr
-        return tot, inner
-
-    # ---------------------------------------------------------------- warmup + timed (value)
-    # The step runs as ONE CUDA graph (seer.SeerPlan): select -> device-side SWITCH on the
-    # chosen kernel -> its preprocessing -> k SpMVs; no host round trip inside the step.
     plan = seer.SeerPlan(model, A, x, y, k)
-    o_eager, _ = seer_step(A, x, y)
-    torch.cuda.synchronize()
-    # our kernels per graph step: the chosen body (prep + k SpMVs), + the selection kernel
-    # on a gathered-path plan (the known path is resolved at plan build, PAPER.md:141)
-    n0 = L.kp_launch_count()
-    fixed_step(int(o_eager.kernel))
-    torch.cuda.synchronize()
-    launches_per_step = (L.kp_launch_count() - n0) + (1 if o_eager.path else 0)
-    for _ in range(a.warmup):
+    for _ in range(warmup):
         plan.launch()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
-    clocks = ClockSampler(local)
-    clocks.start()
-    time.sleep(0.3)
-    step_t = []
-    for _ in range(a.steps):
-        flush.zero_()
-        e0, e1 = ev(), ev()
-        e0.record()
-        plan.launch()
-        e1.record()
-        e1.synchronize()
-        step_t.append(e0.elapsed_time(e1) * 1e-3)
-    launches = launches_per_step * a.steps
-    torch.cuda.synchronize()
-    total = sum(step_t)
-    if world > 1:
-        dist.barrier()
-        tt = torch.tensor([total], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total = float(tt.item())
+    clocks = ClockSampler(dev.index) if headline else None
+    if clocks:
+        clocks.start()
+        time.sleep(0.3)
+    step_t = T.direct(plan.launch, steps)
     outcome = plan.outcome()
     kern = int(outcome.kernel)
-    assert kern == int(o_eager.kernel), "graph and host-dispatched selection disagree"
-    value = world * a.steps * k * bytes_csr / total / 1e9
-    # host-dispatched variant (selection read back, then launches) for comparison
-    eager_t = []
-    for _ in range(max(3, a.steps // 2)):
-        flush.zero_()
-        e0, e1 = ev(), ev()
-        e0.record()
-        seer_step(A, x, y)
-        e1.record()
-        e1.synchronize()
-        eager_t.append(e0.elapsed_time(e1) * 1e-3)
-    # dominant kernel: the chosen SpMV op timed alone on this stream (CUDA events)
-    prepared = kernels.prepare(A, kern) if kern in kernels.NEEDS_PREP else None
-    spmv_t = []
-    for _ in range(a.steps):
-        flush.zero_()
-        m0, m1 = ev(), ev()
-        m0.record()
-        kernels.spmv(A, x, kern, y=y, prepared=prepared)
-        m1.record()
-        m1.synchronize()
-        spmv_t.append(m0.elapsed_time(m1) * 1e-3)
-
-    # ---------------------------------------------------------------- roofline of the chosen SpMV op
-    peak, peak_src = _peak_hbm()
+    # our kernels per step: the chosen body (prep + k SpMVs) + the selection kernel on a
+    # gathered-path plan (the known path is resolved at plan build, PAPER.md:141)
+    P = kernels.prepare(A, kern, cache=False) if kern in kernels.NEEDS_PREP else None
+    n0 = L.kp_launch_count()
+    P2 = kernels.prepare(A, kern, cache=False) if kern in kernels.NEEDS_PREP else None
+    for _ in range(k):
+        kernels.spmv(A, x, kern, y=y, prepared=P2)
+    torch.cuda.synchronize()
+    launches_per_step = (L.kp_launch_count() - n0) + (1 if outcome.path else 0)
+    del P2
+    # the dominant kernel: the chosen SpMV op alone on this stream (CUDA events)
+    spmv_t = T.direct(lambda: kernels.spmv(A, x, kern, y=y, prepared=P), max(steps, 5))
     ell_w = None
     if kern == kernels.ELL_TM:
-        hdr = prepared.buf[:64].cpu().view(torch.int64)
-        ell_w = int(min(int(hdr[3]), prepared.ell_cap))
+        ell_w = int(min(int(P.buf[:64].cpu().view(torch.int64)[3]), P.ell_cap))
     kbytes = A.byte_model(kern, ell_w)
     per_launch = statistics.mean(spmv_t)
+    peak, peak_src = _peak_hbm()
     achieved = kbytes / per_launch / 1e9
-    traffic = _traffic_from_profiles(a.workload, kernels.KERNELS[kern])
+    seer_mean = statistics.mean(step_t)
+    res = {
+        "workload": name, "desc": desc, "rows": R, "cols": C, "nnz": Z, "iterations": k,
+        "dtype": "f32" if dtype == torch.float32 else "f64",
+        "offsets": str(A.row_offsets.dtype).replace("torch.", ""),
+        "bytes_csr": bytes_csr, "step_t": step_t, "launches_per_step": launches_per_step,
+        "value": k * bytes_csr / seer_mean / 1e9,
+        "gflops": k * 2 * Z / seer_mean / 1e9,
+        "seer": {"kernel": kernels.KERNELS[kern], "path": "gathered" if outcome.path else "known",
+                 "features": [outcome.max_d, outcome.min_d, outcome.mean_d, outcome.var_d] if outcome.path else None,
+                 "step_us_mean": round(seer_mean * 1e6, 2),
+                 "step_us_median": round(statistics.median(step_t) * 1e6, 2),
+                 "spmv_us_mean": round(per_launch * 1e6, 2),
+                 "dispatch": ("one CUDA graph (kp_seer_plan): known path resolved on the device at plan build "
+                              "(PAPER.md:141 zero overhead), graph = chosen body" if not outcome.path else
+                              "one CUDA graph (kp_seer_plan): feature pass + gathered tree -> device-side SWITCH")},
+        "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": _traffic_from_profiles(name, kernels.KERNELS[kern]),
+                     "kernel": kernels.KERNELS[kern], "algorithmic_bytes_per_launch": kbytes,
+                     "peak_source": peak_src},
+    }
+    if headline:  # host-dispatched variant (selection read back, then launches) for comparison
+        obuf = torch.empty(_lib.OUTCOME_BYTES, dtype=torch.uint8, device=dev)
 
-    # ---------------------------------------------------------------- e2e through the public API
-    # stop polling nvidia-smi before the e2e leg: its driver queries stall the pinned-copy
-    # pipeline (measured 2.5 -> 2.9 ms/step); the samples cover the timed loop and the
-    # kernel-only timings above
-    clk = clocks.stop()
-    e2e = _e2e(a, A, x, dtype, dev, model, k)
-    if world > 1:  # whole-job e2e: every rank served its own matrix; slowest rank's step time
-        tt = torch.tensor([e2e["ms_per_step"]], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e["ms_per_step"] = round(float(tt.item()), 4)
-        e2e["value"] = round(world * k * bytes_csr / (e2e["ms_per_step"] * 1e-3) / 1e9, 2)
-        e2e["h2d_bytes_per_step"] *= world
-        e2e["d2h_bytes_per_step"] *= world
+        def host_step():
+            from paper_2403_17017_b200.features import decode_outcome
+            seer.select_async(model, A, k, out=obuf)
+            kk = int(decode_outcome(obuf).kernel)
+            PP = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
+            for _ in range(k):
+                kernels.spmv(A, x, kk, y=y, prepared=PP)
+        res["seer"]["host_dispatched_step_us_median"] = round(statistics.median(
+            T.direct(host_step, max(3, steps // 2))) * 1e6, 2)
+        # stop polling nvidia-smi before the e2e leg: its driver queries stall the pinned-copy
+        # pipeline (measured 2.5 -> 2.9 ms/step); the samples cover the timed loop and the
+        # kernel-only timings above
+        res["clocks"] = clocks.stop()
 
-    # ---------------------------------------------------------------- per-kernel sweep
-    sweep, geo, vs_best = None, None, None
-    if not a.no_sweep and rank == 0:
-        sweep = {}
-        seer_mean = total / a.steps if world == 1 else sum(step_t) / a.steps
+    if sweep:
+        sw = {}
+        reps = max(3, steps // 4)
         for kk in range(len(kernels.KERNELS)):
-            tot, inner = timed(kk, max(3, a.steps // 2), 2)
-            t_tot, t_sp = statistics.median(tot), statistics.median(inner) / k
+            Pk = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
+
+            def total(kk=kk):
+                PP = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
+                for _ in range(k):
+                    kernels.spmv(A, x, kk, y=y, prepared=PP)
+
+            def prep_only(kk=kk):
+                kernels.prepare(A, kk, cache=False)
+
+            def iters_only(kk=kk, Pk=Pk):
+                for _ in range(k):
+                    kernels.spmv(A, x, kk, y=y, prepared=Pk)
+            t_tot = statistics.median(T.graph(total, reps))
+            t_prep = statistics.median(T.graph(prep_only, reps)) if kk in kernels.NEEDS_PREP else 0.0
+            t_sp = statistics.median(T.graph(iters_only, reps)) / k
             w = None
             if kk == kernels.ELL_TM:
-                P = kernels.prepare(A, kk, cache=False)
-                w = int(min(int(P.buf[:64].cpu().view(torch.int64)[3]), P.ell_cap))
-            sweep[kernels.KERNELS[kk]] = {
-                "total_us": round(t_tot * 1e6, 2), "spmv_us": round(t_sp * 1e6, 2),
-                "prep_us": round((t_tot - t_sp * k) * 1e6, 2),
-                "spmv_gbs": round(A.byte_model(kk, w) / t_sp / 1e9, 1),
-                "spmv_frac_of_peak": round(A.byte_model(kk, w) / t_sp / 1e9 / peak, 3)}
-        ratios = [sweep[n]["total_us"] * 1e-6 / seer_mean for n in kernels.KERNELS]
-        geo = math.exp(sum(math.log(r) for r in ratios) / len(ratios))
-        vs_best = min(ratios)
+                w = int(min(int(Pk.buf[:64].cpu().view(torch.int64)[3]), Pk.ell_cap))
+            gbs = A.byte_model(kk, w) / t_sp / 1e9
+            sw[kernels.KERNELS[kk]] = {"total_us": round(t_tot * 1e6, 2), "prep_us": round(t_prep * 1e6, 2),
+                                       "spmv_us": round(t_sp * 1e6, 2), "spmv_gbs": round(gbs, 1),
+                                       "spmv_frac_of_peak": round(gbs / peak, 3)}
+            del Pk
+        ratios = {n: v["total_us"] * 1e-6 / seer_mean for n, v in sw.items()}
+        best = min(ratios, key=ratios.get)
+        res["sweep"] = sw
+        res["geomean_speedup_vs_fixed"] = round(math.exp(sum(math.log(r) for r in ratios.values()) / len(ratios)), 3)
+        res["speedup_vs_best_fixed"] = round(ratios[best], 3)
+        res["best_fixed_kernel"] = best
+        res["best_fixed_total_us"] = sw[best]["total_us"]
+    if e2e:
+        res["e2e"] = _e2e(a, A, x, dtype, dev, model, k, steps, warmup)
+    if cpu_seconds > 0:
+        res["cpu_baseline"] = _cpu_baseline(A, x, k, model, bytes_csr, cpu_seconds)
+    plan.close()
+    del plan, A, x, y, P, T
+    torch.cuda.empty_cache()
+    return res
 
-    # ---------------------------------------------------------------- CPU baseline (rank 0, N=1)
-    cpu = None
-    if rank == 0 and world == 1 and not a.no_cpu:
-        cpu = _cpu_baseline(A, x, k, model, bytes_csr, a.cpu_seconds)
 
+def measure_favourable(dev, a, peak):
+    """Every kernel's single SpMV on its favourable input (FAVOURABLE), CUDA events, L2
+    flushed, fraction of the HBM copy peak by the kernel's own byte model."""
+    import torch
+    from paper_2403_17017_b200 import kernels
+    out = {}
+    by_input = {}
+    for kname, (inp, why) in FAVOURABLE.items():
+        by_input.setdefault(inp, []).append((kname, why))
+    for inp, ks in by_input.items():
+        dtype = torch.float64 if inp == "C4" else torch.float32
+        m = _make_matrix(inp, dev)
+        A = m.to_device_csr(dtype, device=dev)
+        del m
+        x = (torch.rand(A.n_cols, device=dev, dtype=torch.float64) * 2 - 1).to(dtype)
+        y = torch.empty(A.n_rows, device=dev, dtype=dtype)
+        T = Timer(dev)
+        for kname, why in ks:
+            kk = kernels.kernel_index(kname)
+            P = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
+            kernels.spmv(A, x, kk, y=y, prepared=P)
+            ts = T.direct(lambda: kernels.spmv(A, x, kk, y=y, prepared=P), 10)
+            w = int(min(int(P.buf[:64].cpu().view(torch.int64)[3]), P.ell_cap)) if kk == kernels.ELL_TM else None
+            t = statistics.median(ts)
+            b = A.byte_model(kk, w)
+            out[kname] = {"input": inp, "why": why, "rows": A.n_rows, "nnz": A.nnz,
+                          "dtype": "f64" if dtype == torch.float64 else "f32", "us": round(t * 1e6, 2),
+                          "gbs": round(b / t / 1e9, 1), "frac": round(b / t / 1e9 / peak, 3),
+                          "algorithmic_bytes": b}
+            del P
+        del A, x, y, T
+        torch.cuda.empty_cache()
+    return out
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_2403_17017_b200 import _lib
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    backend = _backend(world)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(local)
+    if world > 1:  # replicas of the single-GPU workload (explicit --workload C1-C4 only)
+        dist.init_process_group(backend, **({"device_id": torch.device("cuda", local)} if backend == "nccl" else {}))
+    dev = torch.device("cuda", local)
+    _lib.load()
+    model, model_src = _load_model()
+    with_cpu = rank == 0 and world == 1 and not a.no_cpu
+    head = measure(a.workload, dev, model, a, steps=a.steps, warmup=a.warmup, headline=True,
+                   sweep=not a.no_sweep and rank == 0, e2e=True, cpu_seconds=a.cpu_seconds if with_cpu else 0.0)
+    total = sum(head["step_t"])
+    if world > 1:
+        dist.barrier()
+        tt = torch.tensor([total, head["e2e"]["ms_per_step"]], device=dev, dtype=torch.float64)
+        if backend == "nccl":
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        else:
+            tc = tt.cpu()
+            dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+            tt = tc
+        total = float(tt[0])
+        e2e = head["e2e"]  # whole-job e2e: every rank served its own matrix; slowest rank's step
+        e2e["ms_per_step"] = round(float(tt[1]), 4)
+        e2e["value"] = round(world * head["iterations"] * head["bytes_csr"] / (e2e["ms_per_step"] * 1e-3) / 1e9, 2)
+        e2e["h2d_bytes_per_step"] *= world
+        e2e["d2h_bytes_per_step"] *= world
+    per_config, favourable = None, None
+    if rank == 0 and world == 1 and not a.no_configs and a.workload == "C2":
+        per_config = {}
+        peak, _ = _peak_hbm()
+        for c in ("C1", "C3", "C4"):
+            r = measure(c, dev, model, a, steps=max(6, a.steps // 2), warmup=max(3, a.warmup),
+                        sweep=True, e2e=True, cpu_seconds=0.0 if a.no_cpu else a.config_cpu_seconds)
+            per_config[c] = {kk: r[kk] for kk in ("desc", "rows", "cols", "nnz", "iterations", "dtype", "seer",
+                                                  "roofline", "e2e", "speedup_vs_best_fixed", "best_fixed_kernel",
+                                                  "best_fixed_total_us", "geomean_speedup_vs_fixed", "sweep")
+                             if kk in r}
+            per_config[c]["value"] = round(r["value"], 2)
+            per_config[c]["unit"] = "GB/s"
+            per_config[c]["cpu_baseline"] = r.get("cpu_baseline")
+        favourable = measure_favourable(dev, a, peak)
     if rank == 0:
+        k = head["iterations"]
         line = {
-            "metric": "Seer-selected SpMV GB/s (% HBM roofline) and geomean speedup vs best fixed kernel",
-            "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
+            "metric": METRIC,
+            "value": round(world * a.steps * k * head["bytes_csr"] / total / 1e9, 2), "unit": "GB/s",
+            "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(total / a.steps * 1e3, 4), "higher_is_better": True, "scaling": "weak",
-            "gflops": round(world * a.steps * k * 2 * Z / total / 1e9, 2),
-            "vs_baseline": None, "dtype": "f32" if dtype == torch.float32 else "f64",
+            "gflops": round(world * a.steps * k * 2 * head["nnz"] / total / 1e9, 2),
+            "vs_baseline": None, "dtype": head["dtype"],
             "data": "synthetic (counter-hash generated on device)",
-            "config": {"workload": a.workload, "desc": desc, "rows": R, "cols": C, "nnz": Z, "iterations": k,
-                       "offsets": str(A.row_offsets.dtype).replace("torch.", ""), "l2": "flushed (512 MB write "
-                       "between steps; matrix > L2)", "parallelism": f"replicas x{world}" if world > 1 else "1 GPU",
-                       "model": model_src, "byte_model": "nnz*(4+sv)+(R+1)*so+C*sv+R*sv"},
-            "seer": {"kernel": kernels.KERNELS[kern], "path": "gathered" if outcome.path else "known",
-                     "features": [outcome.max_d, outcome.min_d, outcome.mean_d, outcome.var_d] if outcome.path else None,
-                     "step_us_median": round(statistics.median(step_t) * 1e6, 2),
-                     "dispatch": ("one CUDA graph (kp_seer_plan): known path resolved on the device at plan "
-                                  "build (PAPER.md:141 zero overhead), graph = chosen body" if not outcome.path else
-                                  "one CUDA graph (kp_seer_plan): feature pass + gathered tree -> device-side SWITCH"),
-                     "host_dispatched_step_us_median": round(statistics.median(eager_t) * 1e6, 2),
-                     "spmv_us_mean": round(per_launch * 1e6, 2)},
-            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
-                         "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": kernels.KERNELS[kern],
-                         "algorithmic_bytes_per_launch": kbytes, "peak_source": peak_src},
-            "e2e": e2e,
-            "gpu_launches": int(launches),
-            "geomean_speedup_vs_fixed": None if geo is None else round(geo, 3),
-            "speedup_vs_best_fixed": None if vs_best is None else round(vs_best, 3),
-            "sweep": sweep,
-            "cpu_baseline": cpu,
-            "clocks": clk,
+            "config": {"workload": a.workload, "desc": head["desc"], "rows": head["rows"], "cols": head["cols"],
+                       "nnz": head["nnz"], "iterations": k, "offsets": head["offsets"],
+                       "l2": "flushed (512 MB write before every timed launch; matrix > L2)",
+                       "parallelism": f"replicas x{world}" if world > 1 else "1 GPU", "model": model_src,
+                       "byte_model": "nnz*(4+sv)+(R+1)*so+C*sv+R*sv"},
+            "seer": head["seer"],
+            "roofline": head["roofline"],
+            "e2e": head["e2e"],
+            "gpu_launches": int(head["launches_per_step"] * a.steps),
+            "geomean_speedup_vs_fixed": head.get("geomean_speedup_vs_fixed"),
+            "speedup_vs_best_fixed": head.get("speedup_vs_best_fixed"),
+            "best_fixed_kernel": head.get("best_fixed_kernel"),
+            "sweep": head.get("sweep"),
+            "cpu_baseline": head.get("cpu_baseline"),
+            "clocks": head.get("clocks"),
+            "per_config": per_config,
+            "favourable": favourable,
         }
+        if per_config:
+            sp = [per_config[c]["speedup_vs_best_fixed"] for c in per_config] + [head.get("speedup_vs_best_fixed")]
+            line["seer_vs_best_fixed_geomean_C1_C4"] = round(math.exp(sum(math.log(v) for v in sp) / len(sp)), 3)
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
@@ -418,7 +506,7 @@ def _traffic_from_profiles(workload, kernel_label):
     return None
 
 
-def _e2e(a, A, x, dtype, dev, model, k):
+def _e2e(a, A, x, dtype, dev, model, k, steps, warmup):
     """Public-API end to end: pinned host CSR + x -> H2D -> Seer plan -> y D2H, every step.
 
     The step's inputs live in ONE pinned host buffer (offsets, cols, vals, x at 256-byte
@@ -469,19 +557,19 @@ def _e2e(a, A, x, dtype, dev, model, k):
         h_y[s].copy_(d_y, non_blocking=True)
         freed[s].record(comp)
 
-    for i in range(max(2, a.warmup)):
+    for i in range(max(2, warmup)):
         step(i)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    steps = max(4, a.steps // 2)
+    n = max(4, steps // 2)
     e0.record(comp)
     copy.wait_event(e0)
-    for i in range(steps):
+    for i in range(n):
         step(i)
     comp.wait_stream(copy)
     e1.record(comp)
     e1.synchronize()
-    t = e0.elapsed_time(e1) * 1e-3 / steps
+    t = e0.elapsed_time(e1) * 1e-3 / n
     bytes_csr = csr_bytes(A.n_rows, A.n_cols, A.nnz, A.values.element_size(), A.row_offsets.element_size())
     for _, _, plan in sets:
         plan.close()
@@ -491,42 +579,62 @@ def _e2e(a, A, x, dtype, dev, model, k):
                    "seer.SeerPlan.launch (kp_seer_plan C-ABI) -> y to pinned host"}
 
 
+# ------------------------------------------------------------------------ CPU Seer (oracle port)
+def _cpu_seer_pipeline(model_dict, off64, off32, col, val, xh, R, C, Z, k, core, budget_s=None, t0=None):
+    """The reference's CPU path restated faithfully: the selector on the
+    known features; the row-offsets pass (compiled reference length_stats + the features.py
+    epilogue) ONLY when the selector demands gathered features; the chosen tree; then k CPU
+    SpMVs (the reference has no SpMV: OpenMP port).  Returns (kernel, path, iterations run);
+    with a budget, stops between iterations once it is spent."""
+    from oracle import oracle as orc
+    known = (float(R), float(C), float(Z), float(k))
+    path = orc.tree_predict(model_dict["selector"], known)
+    if path == 0:
+        kern = orc.tree_predict(model_dict["known"], known)
+    else:
+        lo, hi, s1, s2 = core.length_stats(off64) if core is not None else orc.length_stats(off64)
+        f = orc.features_epilogue(lo, hi, s1, s2, R, C)
+        kern = orc.tree_predict(model_dict["gathered"], known + tuple(f))
+    done = 0
+    for _ in range(k):
+        orc.spmv_native(off32, col, val, xh)
+        done += 1
+        if budget_s is not None and time.perf_counter() - t0 >= budget_s:
+            break
+    return kern, path, done
+
+
+def _model_dict(model):
+    return {n: t.to_dict() for n, t in (("selector", model.selector_tree), ("known", model.known_tree),
+                                         ("gathered", model.gathered_tree))}
+
+
 def _cpu_baseline(A, x, k, model, bytes_csr, seconds):
-    """Oracle port on this host: compiled reference length_stats (oracle/_ref) +
-    restated epilogue/predict + OpenMP CPU SpMV, looped for ~``seconds``."""
+    """Oracle port on this host, looped for ~``seconds`` (whole pipelines; a pipeline longer
+    than the budget is cut between SpMV iterations and counted by the iterations it ran)."""
     import numpy as np
     from oracle import oracle as orc
     off32, col, val = A.to_host()
     xh = x.cpu().numpy()
     off64 = off32.astype(np.int64)
     core = orc.ref_core()
-    mdict = {n: t.to_dict() for n, t in (("selector", model.selector_tree), ("known", model.known_tree),
-                                          ("gathered", model.gathered_tree))}
-
-    def one():
-        if core is not None:
-            lo, hi, s1, s2 = core.length_stats(off64)
-        else:
-            lo, hi, s1, s2 = orc.length_stats(off64)
-        f = orc.features_epilogue(lo, hi, s1, s2, A.n_rows, A.n_cols)
-        kern, _ = orc.infer(mdict, A.n_rows, A.n_cols, A.nnz, k, f)
-        for _ in range(k):
-            orc.spmv_native(off32, col, val, xh)
-        return kern
-
-    one()
+    md = _model_dict(model)
+    _cpu_seer_pipeline(md, off64, off32, col, val, xh, A.n_rows, A.n_cols, A.nnz, min(k, 2), core)  # warm
     t0 = time.perf_counter()
-    reps = 0
+    pipes, iters, path = 0, 0, 0
     while True:
-        one()
-        reps += 1
+        _, path, done = _cpu_seer_pipeline(md, off64, off32, col, val, xh, A.n_rows, A.n_cols, A.nnz, k, core,
+                                           seconds, t0)
+        pipes += 1
+        iters += done
         el = time.perf_counter() - t0
-        if el >= seconds or reps >= 10000:
+        if el >= seconds or pipes >= 10000:
             break
-    return {"value": round(reps * k * bytes_csr / el / 1e9, 3), "unit": "GB/s", "cores": orc.threads(),
-            "kind": "port", "sample": f"{reps} full pipelines (features via "
-            f"{'compiled reference _core' if core else 'oracle C'} + predict + {k} OpenMP SpMV) on the same matrix, "
-            f"{el:.1f} s", "ms_per_step": round(el / reps * 1e3, 3)}
+    return {"value": round(iters * bytes_csr / el / 1e9, 3), "unit": "GB/s", "cores": orc.threads(),
+            "kind": "port", "sample": f"{pipes} CPU Seer pipelines ({iters} SpMV iterations of k={k}; "
+            f"{'gathered path: features via ' + ('compiled reference _core' if core else 'oracle C') if path else 'known path: no feature pass (SPEC.md:388)'}"
+            f" + restated predict + OpenMP SpMV) on the same matrix, {el:.1f} s",
+            "ms_per_iteration": round(el / max(iters, 1) * 1e3, 3)}
 
 
 # ------------------------------------------------------------------------ reference arm
@@ -535,12 +643,13 @@ def run_reference(a):
     if rank != 0:
         return
     import torch
-    k_default, dt_name, desc = CFG[a.workload]
-    k = a.iters or k_default
-    dev = "cuda" if torch.cuda.is_available() else "cpu"
-    m = _make_matrix(a.workload, dev)  # generation only (torch); nothing of ours computes below
     import numpy as np
     from oracle import oracle as orc
+    name = a.workload if a.workload != "C5" else "C2"  # the CPU arm times one host; C5 is the multi-GPU config
+    k_default, dt_name, desc = CFG[name]
+    k = a.iters or k_default
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    m = _make_matrix(name, dev)  # generation only (torch); nothing of ours computes below
     off64, col64, val64 = m.numpy()
     dtype = np.float32 if dt_name == "float32" else np.float64
     off32 = off64.astype(np.int32) if m.nnz < 2**31 - 1 else off64
@@ -549,89 +658,98 @@ def run_reference(a):
     sv = np.dtype(dtype).itemsize
     bytes_csr = csr_bytes(m.n_rows, m.n_cols, m.nnz, sv, off32.itemsize)
     model, _ = _load_model()
-    mdict = {n: t.to_dict() for n, t in (("selector", model.selector_tree), ("known", model.known_tree),
-                                          ("gathered", model.gathered_tree))}
+    md = _model_dict(model)
     core = orc.ref_core()
-
-    def step():
-        lo, hi, s1, s2 = (core.length_stats(off64) if core is not None else orc.length_stats(off64))
-        f = orc.features_epilogue(lo, hi, s1, s2, m.n_rows, m.n_cols)
-        orc.infer(mdict, m.n_rows, m.n_cols, m.nnz, k, f)
-        for _ in range(k):
-            orc.spmv_native(off32, col, val, xh)
-
+    path = 0
     for _ in range(a.warmup):
-        step()
+        _cpu_seer_pipeline(md, off64, off32, col, val, xh, m.n_rows, m.n_cols, m.nnz, k, core)
     t0 = time.perf_counter()
     for _ in range(a.steps):
-        step()
+        _, path, _ = _cpu_seer_pipeline(md, off64, off32, col, val, xh, m.n_rows, m.n_cols, m.nnz, k, core)
     el = time.perf_counter() - t0
     v = a.steps * k * bytes_csr / el / 1e9
     print(json.dumps({
-        "impl": "reference",
-        "metric": "Seer-selected SpMV GB/s (% HBM roofline) and geomean speedup vs best fixed kernel",
+        "impl": "reference", "metric": METRIC,
         "value": round(v, 3), "unit": "GB/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": round(el / a.steps * 1e3, 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32" if dtype == np.float32 else "f64",
         "data": "synthetic (counter-hash generated)",
-        "config": {"workload": a.workload, "desc": desc, "rows": m.n_rows, "cols": m.n_cols, "nnz": m.nnz,
+        "config": {"workload": name, "desc": desc, "rows": m.n_rows, "cols": m.n_cols, "nnz": m.nnz,
                    "iterations": k},
         "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": orc.threads(), "kind": "port",
-                         "sample": f"{a.steps} full pipelines: features via "
-                                   f"{'compiled reference _core (oracle/_ref)' if core else 'oracle C restatement'}"
-                                   f", restated predict, {k} OpenMP CPU SpMV (the reference has no SpMV)"},
+                         "sample": f"{a.steps} faithful CPU Seer pipelines: selector -> "
+                                   + ("gathered path: features via " + ("compiled reference _core (oracle/_ref)"
+                                      if core else "oracle C restatement") if path else
+                                      "known path (no feature pass, SPEC.md:388)")
+                                   + f" -> restated predict -> {k} OpenMP CPU SpMV (the reference has no SpMV)"},
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
 
 # ------------------------------------------------------------------------ C5: row-sharded
+def _backend(world: int) -> str:
+    """NCCL, one GPU per rank; gloo (ranks sharing GPUs) when fewer GPUs than ranks or
+    KP_BENCH_DIST_BACKEND=gloo -- a control-flow check, never a performance number."""
+    import torch
+    b = os.environ.get("KP_BENCH_DIST_BACKEND")
+    if b:
+        return b
+    return "nccl" if world <= max(1, torch.cuda.device_count()) else "gloo"
+
+
 def run_sharded(a):
     """BASELINE configs[4]: the matrix is row-sharded over the ranks (nnz-balanced, K14),
-    x replicated in the rank-padded layout, y local; each iteration's y slices are
-    all-gathered in place over NVLink (NCCL) into the next x.  Selection = global
-    features from the ranks' K1 partials (one 32-byte all-gather).  One step = the
-    chosen kernel's preprocessing + k iterations; total work fixed as N grows (strong)."""
+    x replicated in the rank-padded layout, y local; each iteration's y slices reach every
+    rank (fused NVLink epilogue stores, or an in-place NCCL all-gather) as the next x.
+    Selection = global features from the ranks' K1 partials (one 32-byte all-gather).  One
+    step = the chosen kernel's preprocessing + k iterations; total work fixed (strong)."""
+    import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_2403_17017_b200 import _lib, dist as kdist, gen, kernels
+    from paper_2403_17017_b200 import _lib, dist as kdist, kernels
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    backend = _backend(world)
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:  # a 1-rank group so the fused exchange (symmetric memory) runs the N-rank code path
-        import socket
-        sk = socket.socket()
-        sk.bind(("127.0.0.1", 0))
-        port = sk.getsockname()[1]
-        sk.close()
-        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
-                                device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group(backend, **({"device_id": dev} if backend == "nccl" else {}))
+    else:  # a 1-rank group so the fused exchange (symmetric memory) runs the N-rank code path
+        dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{_free_port()}", rank=0, world_size=1,
+                                device_id=dev)
+        backend = "nccl"
     L = _lib.load()
+    wd = kdist.Watchdog.start(timeout_s=a.watchdog_s) if backend == "nccl" else None
     k_default, dt_name, desc = CFG["C5"]
     k = a.iters or k_default
     dtype = getattr(torch, dt_name)
     t0 = time.time()
-    m = gen.config("C5", device=dev)  # every rank generates the same global matrix (counter hash)
+    m = _make_matrix("C5", dev, a.scale)  # every rank generates the same global matrix (counter hash)
     R, C, Z = m.n_rows, m.n_cols, m.nnz
+    # sampled-row parity after the run: 1024 global rows' entries kept on the host
+    rs = np.sort(np.random.default_rng(2403).choice(R, size=min(1024, R), replace=False))
+    offh = m.row_offsets.cpu().numpy()
+    samp = [(int(r), m.col_indices[offh[r]:offh[r + 1]].cpu().numpy(), m.values[offh[r]:offh[r + 1]].cpu().numpy())
+            for r in rs]
     A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, C, rank, world, dtype)
     del m
     torch.cuda.empty_cache()
     t_gen = time.time() - t0
     model, model_src = _load_model()
-    run = kdist.ShardedSeer(model, A, plan, k, R, C, Z, exchange=a.exchange)
+    exchange = a.exchange if backend == "nccl" else "host"
+    run = kdist.ShardedSeer(model, A, plan, k, R, C, Z, exchange=exchange)
     kern = run.kernel
     x0 = torch.full((world * plan.r_max,), 1.0 / R, dtype=dtype, device=dev)
     sv, so = 4 if dtype == torch.float32 else 8, 4
     bytes_csr = csr_bytes(R, C, Z, sv, so)
     for _ in range(a.warmup):
         run.step(x0)
+        if wd:
+            wd.heartbeat()
     torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    dist.barrier()
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
@@ -641,15 +759,18 @@ def run_sharded(a):
     e0.record()
     for _ in range(a.steps):
         run.step(x0)
+        if wd:
+            wd.heartbeat()
     e1.record()
     e1.synchronize()
     launches = L.kp_launch_count() - n0
     total = e0.elapsed_time(e1) * 1e-3
-    if world > 1:
-        dist.barrier()
-        tt = torch.tensor([total], device=dev, dtype=torch.float64)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        total = float(tt.item())
+    dist.barrier()
+    tt = torch.tensor([total], dtype=torch.float64)
+    if backend == "nccl":
+        tt = tt.to(dev)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    total = float(tt.item())
     # this rank's SpMV alone (dominant kernel) for the roofline
     P = kernels.prepare(A, kern) if kern in kernels.NEEDS_PREP else None
     ys = torch.empty(plan.local_rows, dtype=dtype, device=dev)
@@ -662,28 +783,50 @@ def run_sharded(a):
         m1.synchronize()
         ts.append(m0.elapsed_time(m1) * 1e-3)
     clk = clocks.stop()
+    # sampled-row parity of one full iteration (SpMV + exchange) vs the fp64 oracle
+    x_in = torch.rand(world * plan.r_max, dtype=torch.float64, generator=torch.Generator().manual_seed(7))
+    x_in = x_in.to(dtype).to(dev)
+    x_out = run.step(x_in, iters=1).clone()
+    xg_in = plan.unpad(x_in).double().cpu().numpy()
+    xg_out = plan.unpad(x_out).double().cpu().numpy()
+    errs = []
+    for r, c, v in samp:
+        yr = float(np.dot(v.astype(dtype).astype(np.float64), xg_in[c]))
+        bound = 1e-5 * float(np.abs(v.astype(dtype).astype(np.float64) * xg_in[c]).sum()) + 1e-300
+        errs.append(abs(float(xg_out[r]) - yr) / bound)
+    parity_ok = bool(max(errs) <= 1.0)
+    if wd:
+        wstat = wd.stop()
     peak, peak_src = _peak_hbm()
     kb = A.byte_model(kern, None if kern != kernels.ELL_TM else int(min(int(P.buf[:64].cpu().view(torch.int64)[3]), P.ell_cap)))
     per = statistics.median(ts)
     value = a.steps * k * bytes_csr / total / 1e9
     if rank == 0:
         print(json.dumps({
-            "metric": "Seer-selected SpMV GB/s (% HBM roofline) and geomean speedup vs best fixed kernel",
+            "metric": METRIC,
             "value": round(value, 2), "unit": "GB/s", "n_gpus": world, "steps": a.steps, "warmup": a.warmup,
             "ms_per_step": round(total / a.steps * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "gflops": round(a.steps * k * 2 * Z / total / 1e9, 2),
             "vs_baseline": None, "dtype": "f32" if dtype == torch.float32 else "f64",
             "data": "synthetic (counter-hash R-MAT generated on device)",
-            "config": {"workload": "C5", "desc": desc, "rows": R, "cols": C, "nnz": Z, "iterations": k,
-                       "parallelism": f"row-sharded x{world} (nnz-balanced, NCCL all-gather of y)",
+            "config": {"workload": "C5", "desc": desc if a.scale == 26 else desc.replace("s26", f"s{a.scale}"),
+                       "rows": R, "cols": C, "nnz": Z, "iterations": k,
+                       "parallelism": f"row-sharded x{world} (nnz-balanced, y exchanged every iteration)",
                        "l2": "inputs larger than L2 (A: %.1f GB)" % (bytes_csr / 1e9), "model": model_src,
                        "byte_model": "nnz*(4+sv)+(R+1)*so+C*sv+R*sv per iteration, x counted once",
                        "generation_s": round(t_gen, 1)},
+            "comm": {"backend": backend, "nranks": dist.get_world_size(), "exchange": run.exchange,
+                     "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None,
+                     "watchdog": wstat if wd else None,
+                     "note": None if backend == "nccl" else "ranks share GPUs over gloo: control flow only"},
             "seer": {"kernel": kernels.KERNELS[kern], "path": "gathered" if run.outcome.path else "known",
                      "dispatch": "global selection from the ranks' K1 partials at setup (device)",
-                     "exchange": ("fused: SpMV epilogue stores y into every rank's next x over NVLink "
-                                  "(symmetric memory, kp_spmv_bcast) + device barrier" if run.exchange == "fused"
-                                  else "NCCL in-place all-gather of y after each SpMV")},
+                     "exchange": {"fused": "SpMV epilogue stores y into every rank's next x over NVLink "
+                                           "(symmetric memory, kp_spmv_bcast) + device barrier",
+                                  "nccl": "NCCL in-place all-gather of y after each SpMV",
+                                  "host": "y slices all-gathered through host staging (gloo)"}[run.exchange]},
+            "parity": {"sampled_rows": len(samp), "tol": 1e-5, "max_err_over_bound": round(max(errs), 4),
+                       "ok": parity_ok, "check": "one SpMV + exchange from a random x, rows vs fp64 oracle"},
             "roofline": {"bound": "hbm", "achieved": round(kb / per / 1e9, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(kb / per / 1e9 / peak, 4), "traffic": None, "kernel": kernels.KERNELS[kern],
                          "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
@@ -691,10 +834,29 @@ def run_sharded(a):
             "e2e": None, "gpu_launches": int(launches), "cpu_baseline": None, "clocks": clk,
         }), flush=True)
     dist.destroy_process_group()
+    if not parity_ok:
+        raise SystemExit(f"C5 sampled-row parity failed: max err/bound {max(errs)}")
+
+
+# ------------------------------------------------------------------------ local launcher
+def _spawn(a) -> int:
+    """`bench.py --gpus N` without torchrun: N local ranks (env rendezvous on 127.0.0.1)."""
+    port = _free_port()
+    procs = []
+    for r in range(a.gpus):
+        env = dict(os.environ, RANK=str(r), LOCAL_RANK=str(r), WORLD_SIZE=str(a.gpus),
+                   LOCAL_WORLD_SIZE=str(a.gpus), MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        procs.append(subprocess.Popen([sys.executable, os.path.abspath(__file__)] + sys.argv[1:], env=env))
+    rc = 0
+    for p in procs:
+        rc = max(rc, p.wait())
+    return rc
 
 
 def main():
     a = _args()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(a))
     if a.impl == "reference":
         run_reference(a)
     elif a.workload == "C5":

@@ -253,6 +253,22 @@ KP_API int kp_mm_parse(const char *buf, size_t len, int64_t *rows, int64_t *cols
 KP_API int kp_shard_partition(const void *d_off, int32_t off_type, int64_t n_rows, int32_t parts,
                        int64_t *d_cuts, void *stream);
 
+/* ------------------------------------------------------------ failure detection (multi-GPU) */
+/* Watchdog over an NCCL communicator (no reference counterpart): a native thread
+ * polls ncclCommGetAsyncError every poll_ms and the host heartbeat; on an NCCL error, or no
+ * heartbeat for timeout_ms (a hung collective or peer; 0 = no timeout), it calls
+ * ncclCommAbort so blocked collectives return.  `nccl_comm` is an ncclComm_t (e.g. torch's
+ * ProcessGroupNCCL._comm_ptr()); NCCL symbols come from the process's libnccl.so.2
+ * (KP_EUNSUPPORTED when absent).  heartbeat / status / stop return the state below. */
+#define KP_WD_OK 0
+#define KP_WD_NCCL_ERROR 1
+#define KP_WD_TIMEOUT 2
+typedef struct kp_watchdog kp_watchdog;
+KP_API int kp_watchdog_start(void *nccl_comm, int64_t timeout_ms, int64_t poll_ms, kp_watchdog **out);
+KP_API int kp_watchdog_heartbeat(kp_watchdog *w);
+KP_API int kp_watchdog_status(kp_watchdog *w, int32_t *nccl_result, char *msg, size_t msg_len);
+KP_API int kp_watchdog_stop(kp_watchdog *w);
+
 /* Library identification: "kpb200 <version> sm_100a". */
 KP_API const char *kp_version(void);
 /* Number of kernel launches issued by this library since load (instrumentation). */

@@ -27,7 +27,8 @@ EXPORTS = (
     "kp_spmv_workspace_bytes", "kp_spmv", "kp_seer_plan_bytes", "kp_seer_plan_create", "kp_seer_plan_launch",
     "kp_seer_plan_destroy", "kp_shard_partition", "kp_version", "kp_launch_count", "kp_debug_set_wave_warps",
     "kp_seer_select_partials", "kp_coo_workspace_bytes", "kp_csr_from_coo", "kp_spmv_bcast",
-    "kp_mm_header", "kp_mm_parse",
+    "kp_mm_header", "kp_mm_parse", "kp_watchdog_start", "kp_watchdog_heartbeat", "kp_watchdog_status",
+    "kp_watchdog_stop",
 )
 
 
@@ -60,6 +61,7 @@ class kp_prepared(ctypes.Structure):
 
 KP_MAX_PEERS = 8
 KP_EPARSE = -6
+KP_WD_OK, KP_WD_NCCL_ERROR, KP_WD_TIMEOUT = 0, 1, 2
 
 
 class kp_mm_info(ctypes.Structure):
@@ -115,6 +117,10 @@ def load(require: bool = True):
         "kp_spmv_bcast": (ctypes.c_int, [i32, P(kp_csr), P(kp_prepared), p, P(kp_peers), p, sz, p]),
         "kp_mm_header": (ctypes.c_int, [ctypes.c_char_p, sz, P(kp_mm_info)]),
         "kp_mm_parse": (ctypes.c_int, [ctypes.c_char_p, sz, p, p, p, i64, i32, P(kp_mm_info)]),
+        "kp_watchdog_start": (ctypes.c_int, [p, i64, i64, P(p)]),
+        "kp_watchdog_heartbeat": (ctypes.c_int, [p]),
+        "kp_watchdog_status": (ctypes.c_int, [p, P(i32), ctypes.c_char_p, sz]),
+        "kp_watchdog_stop": (ctypes.c_int, [p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

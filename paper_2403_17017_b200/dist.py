@@ -110,42 +110,77 @@ def _as_tensor(a, device):
     return torch.as_tensor(np.asarray(a), dtype=torch.int64, device=device)
 
 
-class ShardedSpMV:
-    """Iterative y = A x with x <- y across ranks (power iteration), GPU kernels + NCCL.
+def all_gather_slices(buf, plan: ShardPlan, group=None) -> None:
+    """The per-iteration y exchange: every rank's R_max slice of the rank-padded buffer
+    ``buf`` reaches every rank, in place.  NCCL: one in-place all_gather_into_tensor over
+    NVLink (send buffer = own slice of the receive buffer).  gloo (CPU tensors, or ranks
+    sharing GPUs for a control-flow check): through host staging."""
+    import torch.distributed as tdist
+    p = plan
+    if p.world == 1:
+        return
+    if buf.is_cuda and tdist.get_backend(group) == "nccl":
+        tdist.all_gather_into_tensor(buf, buf[p.rank * p.r_max:(p.rank + 1) * p.r_max], group=group)
+        return
+    host = buf.cpu() if buf.is_cuda else buf
+    tdist.all_gather_into_tensor(host, host[p.rank * p.r_max:(p.rank + 1) * p.r_max].clone(), group=group)
+    if buf.is_cuda:
+        buf.copy_(host)
 
-    ``run(x_full, k)``: x_pad[p] <- A_p . x_pad ; all_gather -> next x_pad ; k times."""
 
-    def __init__(self, A_full_host, kernel, group=None, dtype=None):
+class Watchdog:
+    """Failure detection for the NCCL path: ``kp_watchdog_*`` polls
+    ncclCommGetAsyncError on this rank's communicator and a heartbeat the host sends every
+    step; an NCCL error, or no heartbeat within ``timeout_s``, aborts the communicator
+    (ncclCommAbort) so blocked collectives return, and the next ``heartbeat()`` raises."""
+
+    def __init__(self, handle, timeout_s: float):
+        self._h, self.timeout_s = handle, timeout_s
+
+    @classmethod
+    def start(cls, timeout_s: float = 300.0, poll_s: float = 0.05, group=None) -> "Watchdog | None":
+        """Start on the NCCL communicator of ``group`` (default: WORLD); None when the
+        process group is not NCCL or exposes no communicator."""
+        import ctypes
         import torch
-        import torch.distributed as dist
-        from .device import DeviceCSR
-        self.dist = dist
-        self.group = group
-        rank, world = dist.get_rank(group), dist.get_world_size(group)
-        off, col, val = A_full_host
-        cuts = partition_cuts(off, world)
-        self.plan = ShardPlan(rank, world, cuts, int(np.asarray(off).size - 1))
-        loff, lc, lv = local_csr(np.asarray(off), np.asarray(col), np.asarray(val), self.plan)
-        dt = dtype or torch.float32
-        self.A = DeviceCSR.from_host(n_rows=self.plan.local_rows, n_cols=world * self.plan.r_max,
-                                     row_offsets=loff, col_indices=lc, values=lv, dtype=dt)
-        self.kernel = kernel
-        self.bufs = [torch.zeros(world * self.plan.r_max, dtype=dt, device=self.A.device) for _ in range(2)]
+        import torch.distributed as tdist
+        from . import _lib
+        pg = group or tdist.group.WORLD
+        if tdist.get_backend(pg) != "nccl":
+            return None
+        try:
+            comm = int(pg._get_backend(torch.device("cuda"))._comm_ptr())
+        except Exception:
+            return None
+        if not comm:
+            return None
+        h = ctypes.c_void_p()
+        rc = _lib.load().kp_watchdog_start(comm, int(timeout_s * 1000), max(1, int(poll_s * 1000)), ctypes.byref(h))
+        if rc != _lib.KP_OK:
+            return None
+        return cls(h, timeout_s)
 
-    def run(self, x_full, k: int):
-        from . import kernels
-        p = self.plan
-        cur = 0
-        self.bufs[cur].copy_(p.pad(x_full.to(self.bufs[0].device)))
-        P = kernels.prepare(self.A, self.kernel) if kernels.kernel_index(self.kernel) in kernels.NEEDS_PREP else None
-        for _ in range(k):
-            nxt = 1 - cur
-            mine = self.bufs[nxt][p.rank * p.r_max: p.rank * p.r_max + p.local_rows]
-            kernels.spmv(self.A, self.bufs[cur], self.kernel, y=mine, prepared=P)
-            self.dist.all_gather_into_tensor(self.bufs[nxt], self.bufs[nxt][p.rank * p.r_max:(p.rank + 1) * p.r_max],
-                                             group=self.group)
-            cur = nxt
-        return p.unpad(self.bufs[cur])
+    def status(self) -> tuple[int, int, str]:
+        import ctypes
+        from . import _lib
+        r = ctypes.c_int32(0)
+        msg = ctypes.create_string_buffer(256)
+        st = _lib.load().kp_watchdog_status(self._h, ctypes.byref(r), msg, 256)
+        return st, int(r.value), msg.value.decode()
+
+    def heartbeat(self) -> None:
+        from . import _lib
+        if _lib.load().kp_watchdog_heartbeat(self._h) != _lib.KP_WD_OK:
+            st, r, msg = self.status()
+            raise RuntimeError(f"NCCL watchdog: {msg} (state {st}, ncclResult {r})")
+
+    def stop(self) -> dict:
+        from . import _lib
+        st, r, msg = self.status()
+        _lib.load().kp_watchdog_stop(self._h)
+        self._h = None
+        return {"state": ["ok", "nccl_error", "timeout"][st], "nccl_result": r, "msg": msg,
+                "timeout_s": self.timeout_s}
 
 
 # ---------------------------------------------------------------------- device path (GPU)
@@ -202,8 +237,13 @@ def select_sharded(model, A, world: int, n_rows: int, n_cols: int, nnz: int, k: 
     from . import _lib
     part = _length_partials(A)
     if world > 1:
-        parts = torch.empty(4 * world, dtype=torch.int64, device=A.device)
-        tdist.all_gather_into_tensor(parts, part, group=group)
+        if tdist.get_backend(group) == "nccl":
+            parts = torch.empty(4 * world, dtype=torch.int64, device=A.device)
+            tdist.all_gather_into_tensor(parts, part, group=group)
+        else:  # gloo: host staging
+            hp = torch.empty(4 * world, dtype=torch.int64)
+            tdist.all_gather_into_tensor(hp, part.cpu(), group=group)
+            parts = hp.to(A.device)
     else:
         parts = part
     sel, kn, ga = model.device_trees(A.device)
@@ -239,9 +279,12 @@ class ShardedSeer:
         self._kernels = kernels
         # exchange: "fused" = the SpMV epilogue stores y into every rank's next-x buffer over
         # NVLink peer mappings of a symmetric allocation (kp_spmv_bcast) + a device-side
-        # barrier; "nccl" = local SpMV then an in-place all-gather.  "auto" = fused when the
-        # chosen kernel supports it and symmetric memory rendezvous works.
-        self.exchange = "nccl"
+        # barrier; "nccl" = local SpMV then an in-place all-gather; "host" = the all-gather
+        # through host staging (gloo: ranks sharing a GPU).  "auto" = fused when the chosen
+        # kernel supports it and symmetric memory rendezvous works.
+        if exchange not in ("auto", "fused", "nccl", "host"):
+            raise ValueError(f"unknown exchange {exchange!r}")
+        self.exchange = "host" if exchange == "host" else "nccl"
         if exchange in ("auto", "fused") and self.kernel in (kernels.CSR_MP, kernels.CSR_WO):
             try:
                 self._setup_fused(dt)
@@ -250,7 +293,7 @@ class ShardedSeer:
                 if exchange == "fused":
                     raise
                 self.fused_error = repr(exc)
-        if self.exchange == "nccl":
+        if self.exchange in ("nccl", "host"):
             self.bufs = [torch.zeros(plan.world * plan.r_max, dtype=dt, device=A.device) for _ in range(2)]
 
     def _setup_fused(self, dt):
@@ -275,11 +318,12 @@ class ShardedSeer:
         p = self.plan
         return buf[p.rank * p.r_max: p.rank * p.r_max + p.local_rows]
 
-    def step(self, x_pad=None):
-        """One timed unit: prep + k iterations; returns the final padded x buffer."""
-        import torch.distributed as tdist
+    def step(self, x_pad=None, iters: int | None = None):
+        """One timed unit: prep + k iterations (``iters`` overrides k); returns the final
+        padded x buffer."""
         K = self._kernels
         p = self.plan
+        k = self.k if iters is None else int(iters)
         if x_pad is not None:
             self.bufs[0].copy_(x_pad)
         P = K.prepare(self.A, self.kernel, cache=False) if self.kernel in K.NEEDS_PREP else None
@@ -287,7 +331,7 @@ class ShardedSeer:
         if self.exchange == "fused":
             if x_pad is not None:
                 self.hdl[0].barrier(channel=0)  # every rank's buffer 0 holds x before anyone reads
-            for _ in range(self.k):
+            for _ in range(k):
                 nxt = 1 - cur
                 # y -> every rank's next-x slice from the kernel epilogue; the barrier orders
                 # all ranks' stores before the next iteration's reads (and frees buffer cur)
@@ -295,11 +339,9 @@ class ShardedSeer:
                 self.hdl[nxt].barrier(channel=0)
                 cur = nxt
             return self.bufs[cur]
-        for _ in range(self.k):
+        for _ in range(k):
             nxt = 1 - cur
             K.spmv(self.A, self.bufs[cur], self.kernel, y=self._slice(self.bufs[nxt]), prepared=P)
-            if p.world > 1:
-                tdist.all_gather_into_tensor(self.bufs[nxt], self.bufs[nxt][p.rank * p.r_max:(p.rank + 1) * p.r_max],
-                                             group=self.group)
+            all_gather_slices(self.bufs[nxt], p, self.group)
             cur = nxt
         return self.bufs[cur]

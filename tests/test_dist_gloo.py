@@ -56,9 +56,9 @@ def _worker(rank, world, port, result_q):
     buf = torch.from_numpy(plan.pad(x).astype(np.float64))
     for _ in range(3):
         y, _ = orc.spmv_csr(loff, lc, lv, buf.numpy())
-        nxt = torch.zeros_like(buf)
+        nxt = torch.full_like(buf, float("nan"))
         nxt[rank * plan.r_max: rank * plan.r_max + plan.local_rows] = torch.from_numpy(y)
-        dist.all_gather_into_tensor(nxt, nxt[rank * plan.r_max:(rank + 1) * plan.r_max].clone())
+        kdist.all_gather_slices(nxt, plan)  # the exchange ShardedSeer runs (gloo: host path)
         buf = nxt
     out = plan.unpad(buf.numpy())
     # exact integer feature partials combine to the global ones

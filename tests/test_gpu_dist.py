@@ -146,3 +146,60 @@ def test_sharded_seer_fused_symmetric_memory_world1(orc):
         assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
     finally:
         tdist.destroy_process_group()
+
+
+def test_bench_gpus2_sharded_control_flow():
+    """`python bench.py --gpus 2` without torchrun: two local ranks (gloo when the box has
+    one GPU: ranks share it), row-sharded C5 family at a reduced scale, the host-staged y
+    exchange, global selection from partials and the sampled-row parity check."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--gpus", "2", "--scale", "16", "--steps", "2",
+                        "--warmup", "1", "--iters", "3", "--watchdog-s", "120"],
+                       capture_output=True, text=True, timeout=600, env=env, cwd=root)
+    assert p.returncode == 0, p.stderr[-3000:]
+    line = json.loads([ln for ln in p.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["config"]["parallelism"].startswith("row-sharded x2")
+    assert line["comm"]["nranks"] == 2 and line["parity"]["ok"]
+    assert line["scaling"] == "strong" and line["value"] > 0
+
+
+_WD_SCRIPT = r"""
+import socket, sys, time, torch, torch.distributed as dist
+sys.path.insert(0, sys.argv[1])
+from paper_2403_17017_b200 import dist as kdist
+s = socket.socket(); s.bind(("127.0.0.1", 0)); port = s.getsockname()[1]; s.close()
+dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                        device_id=torch.device("cuda", 0))
+wd = kdist.Watchdog.start(timeout_s=30.0)
+assert wd is not None, "no NCCL communicator exposed"
+t = torch.ones(8, device="cuda"); dist.all_reduce(t); torch.cuda.synchronize()
+wd.heartbeat()
+print("OK_STATE", wd.stop()["state"])
+wd = kdist.Watchdog.start(timeout_s=0.2)
+time.sleep(1.0)
+try:
+    wd.heartbeat()
+    print("NO_TIMEOUT")
+except RuntimeError as e:
+    print("TIMEOUT_RAISED", e)
+print("FINAL", wd.stop()["state"])
+sys.stdout.flush()
+import os; os._exit(0)  # the communicator was aborted: skip the process-group teardown
+"""
+
+
+def test_nccl_watchdog_heartbeat_and_timeout():
+    """kp_watchdog on a real NCCL communicator (world 1): healthy with heartbeats; with no
+    heartbeat inside the timeout it aborts the communicator and the next heartbeat raises."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, "-c", _WD_SCRIPT, root], capture_output=True, text=True, timeout=300)
+    assert "OK_STATE ok" in p.stdout, (p.stdout, p.stderr[-2000:])
+    assert "TIMEOUT_RAISED" in p.stdout and "FINAL timeout" in p.stdout, (p.stdout, p.stderr[-2000:])
