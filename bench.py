@@ -127,6 +127,12 @@ class ClockSampler:
             self.t.start()
         except Exception:
             self.proc = None
+            return
+        # nvidia-smi takes ~0.5-2 s to initialise: the timed region starts only once it
+        # is sampling, so short timed loops are still covered
+        t0 = time.time()
+        while not self.lines and time.time() - t0 < 8.0 and self.proc.poll() is None:
+            time.sleep(0.05)
 
     def _read(self):
         for ln in self.proc.stdout:
@@ -315,10 +321,6 @@ def measure(name, dev, model, a, *, steps, warmup, headline=False, sweep=True, e
                 kernels.spmv(A, x, kk, y=y, prepared=PP)
         res["seer"]["host_dispatched_step_us_median"] = round(statistics.median(
             T.direct(host_step, max(3, steps // 2))) * 1e6, 2)
-        # stop polling nvidia-smi before the e2e leg: its driver queries stall the pinned-copy
-        # pipeline (measured 2.5 -> 2.9 ms/step); the samples cover the timed loop and the
-        # kernel-only timings above
-        res["clocks"] = clocks.stop()
 
     if sweep:
         sw = {}
@@ -355,6 +357,11 @@ def measure(name, dev, model, a, *, steps, warmup, headline=False, sweep=True, e
         res["speedup_vs_best_fixed"] = round(ratios[best], 3)
         res["best_fixed_kernel"] = best
         res["best_fixed_total_us"] = sw[best]["total_us"]
+    if clocks:
+        # stop polling nvidia-smi before the e2e leg: its driver queries stall the pinned-copy
+        # pipeline (measured 2.5 -> 2.9 ms/step); the samples cover the timed loop and the
+        # kernel-only timings (chosen SpMV, sweep) above
+        res["clocks"] = clocks.stop()
     if e2e:
         res["e2e"] = _e2e(a, A, x, dtype, dev, model, k, steps, warmup)
     if cpu_seconds > 0:
@@ -570,11 +577,22 @@ def _e2e(a, A, x, dtype, dev, model, k, steps, warmup):
     e1.record(comp)
     e1.synchronize()
     t = e0.elapsed_time(e1) * 1e-3 / n
+    # the link floor on this box: the same pinned H2D alone (no compute, no D2H)
+    fl = []
+    for _ in range(3):
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(comp)
+        sets[0][0].copy_(h_in, non_blocking=True)
+        f1.record(comp)
+        f1.synchronize()
+        fl.append(f0.elapsed_time(f1) * 1e-3)
+    floor = min(fl)
     bytes_csr = csr_bytes(A.n_rows, A.n_cols, A.nnz, A.values.element_size(), A.row_offsets.element_size())
     for _, _, plan in sets:
         plan.close()
     return {"value": round(k * bytes_csr / t / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": bi,
             "d2h_bytes_per_step": int(bo), "ms_per_step": round(t * 1e3, 4),
+            "h2d_floor_ms": round(floor * 1e3, 4), "h2d_link_gbs": round(o / floor / 1e9, 1),
             "api": "pinned host CSR+x (one buffer) -> DeviceCSR staging views (copy stream, 2-deep) -> "
                    "seer.SeerPlan.launch (kp_seer_plan C-ABI) -> y to pinned host"}
 
@@ -790,9 +808,11 @@ def run_sharded(a):
     xg_in = plan.unpad(x_in).double().cpu().numpy()
     xg_out = plan.unpad(x_out).double().cpu().numpy()
     errs = []
+    npdt = np.float32 if dtype == torch.float32 else np.float64
     for r, c, v in samp:
-        yr = float(np.dot(v.astype(dtype).astype(np.float64), xg_in[c]))
-        bound = 1e-5 * float(np.abs(v.astype(dtype).astype(np.float64) * xg_in[c]).sum()) + 1e-300
+        vv = v.astype(npdt).astype(np.float64)
+        yr = float(np.dot(vv, xg_in[c]))
+        bound = 1e-5 * float(np.abs(vv * xg_in[c]).sum()) + 1e-300
         errs.append(abs(float(xg_out[r]) - yr) / bound)
     parity_ok = bool(max(errs) <= 1.0)
     if wd:
