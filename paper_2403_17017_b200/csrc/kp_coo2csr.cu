@@ -325,6 +325,7 @@ int kp_coo_workspace_bytes(int64_t n, int64_t n_rows, int64_t n_cols, size_t *by
 int kp_csr_from_coo(int64_t n_rows, int64_t n_cols, const int64_t *d_rows, const int64_t *d_cols,
                     const double *d_vals, int64_t n, int64_t *d_off, int32_t *d_col, double *d_val,
                     int64_t *d_out2, void *d_ws, size_t ws_bytes, void *stream) {
+    KP_NVTX("kp_csr_from_coo");
     if (n < 0 || n >= INT32_MAX || n_rows < 0 || n_rows >= INT32_MAX || n_cols < 0 || n_cols > INT32_MAX ||
         !d_off || !d_out2 || (n > 0 && (!d_rows || !d_cols || !d_vals || !d_col || !d_val)))
         return KP_EINVAL;

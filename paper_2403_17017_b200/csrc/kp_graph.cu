@@ -86,6 +86,7 @@ int kp_seer_plan_bytes(const kp_csr *A, int64_t ell_cap, size_t *bytes) {
 int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap, const void *d_selector,
                         const void *d_known, const void *d_gathered, const void *d_x, void *d_y, void *d_buf,
                         size_t bytes, void *d_red_ws, kp_outcome *d_out, kp_seer_plan **plan_out, void *stream) {
+    KP_NVTX("kp_seer_plan_create");
     if (!plan_out || !d_buf || !d_out || !d_red_ws || iterations < 1 || ell_cap < 1 || !d_y) return KP_EINVAL;
     if (((uintptr_t)d_buf & (kAl - 1)) != 0) return KP_EINVAL;
     PlanLayout L;
@@ -115,6 +116,7 @@ int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap, co
     };
     if (cudaGraphCreate(&P->graph, 0) != cudaSuccess) return fail(KP_ECUDA);
     void *ws = base + L.ws_off;
+    if (L.ws && cudaMemsetAsync(ws, 0, 16, s) != cudaSuccess) return fail(KP_ECUDA);  // kp_spmv's ticket
     // 0) Known-feature decisions depend only on the plan's static shape (rows, cols, nnz,
     //    iterations): "known at no additional runtime cost".  Evaluate
     //    the selector (and, on the known path, the known tree) on the device once, now.
@@ -201,6 +203,7 @@ int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap, co
 }
 
 int kp_seer_plan_launch(kp_seer_plan *plan, void *stream) {
+    KP_NVTX("kp_seer_plan_launch");
     if (!plan || !plan->exec) return KP_EINVAL;
     if (cudaGraphLaunch(plan->exec, (cudaStream_t)stream) != cudaSuccess) {
         cudaGetLastError();

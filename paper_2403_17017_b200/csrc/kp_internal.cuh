@@ -31,6 +31,17 @@ extern unsigned long long g_launches;  // kp_launch_count()
 
 int num_sms();
 
+// NVTX ranges around every C-ABI entry (domain "kernelpick"): a profiler (nsys, ncu
+// --nvtx) sees each Seer stage -- selection, feature pass, preparation, SpMV, plan
+// build/launch -- by name.  Header-only NVTX3; without an attached tool each range is a
+// null-pointer check.
+struct NvtxRange {
+    explicit NvtxRange(const char *name);
+    ~NvtxRange();
+};
+#define KP_NVTX(name) ::kp::NvtxRange _kp_nvtx_range(name)
+const char *kernel_label(int32_t kernel);
+
 // Trees by value for the plan's selection kernel (kp_reduce.cu, used by kp_graph.cu).
 constexpr int kParamTreeNodes = 127;  // depth <= 6
 struct ParamTrees {

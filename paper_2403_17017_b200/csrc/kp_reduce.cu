@@ -708,6 +708,7 @@ size_t kp_reduce_workspace_bytes(void) { return sizeof(RedWorkspace); }
 
 int kp_length_stats(const void *d_off, int32_t off_type, int64_t n_off, int64_t *d_out4, void *d_ws,
                     void *stream) {
+    KP_NVTX("kp_length_stats");
     if (!d_out4 || !d_ws || n_off < 0 || (n_off > 0 && !d_off)) return KP_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t n = n_off - 1;
@@ -722,6 +723,7 @@ int kp_length_stats(const void *d_off, int32_t off_type, int64_t n_off, int64_t 
 
 int kp_gather_features(const void *d_off, int32_t off_type, int64_t n_rows, int64_t n_cols,
                        kp_outcome *d_out, void *d_ws, void *stream) {
+    KP_NVTX("kp_gather_features");
     if (n_rows <= 0 || n_cols <= 0 || !d_off || !d_out || !d_ws) return KP_EINVAL;
     K1Args a = {};
     a.off = d_off; a.n_rows = n_rows; a.n_cols = n_cols; a.mode = kModeFeatures; a.out = d_out;
@@ -732,6 +734,7 @@ int kp_gather_features(const void *d_off, int32_t off_type, int64_t n_rows, int6
 int kp_seer_select(const void *d_off, int32_t off_type, int64_t n_rows, int64_t n_cols, int64_t nnz,
                    int64_t iterations, const void *d_selector, const void *d_known, const void *d_gathered,
                    kp_outcome *d_out, void *d_ws, void *stream) {
+    KP_NVTX("kp_seer_select");
     if (n_rows <= 0 || n_cols <= 0 || !d_off || !d_out || !d_ws || !d_selector || !d_known || !d_gathered)
         return KP_EINVAL;
     K1Args a = {};
@@ -743,6 +746,7 @@ int kp_seer_select(const void *d_off, int32_t off_type, int64_t n_rows, int64_t 
 
 int kp_wave_ceil_max_sum(const void *d_off, int32_t off_type, int64_t n_off, int64_t divisor,
                          int64_t wave_rows, int64_t *d_out1, void *d_ws, void *stream) {
+    KP_NVTX("kp_wave_ceil_max_sum");
     if (divisor <= 0 || wave_rows <= 0 || !d_out1 || !d_ws || n_off < 0) return KP_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t n = n_off - 1;
@@ -759,6 +763,7 @@ int kp_wave_ceil_max_sum(const void *d_off, int32_t off_type, int64_t n_off, int
 
 int kp_tree_predict(const void *d_tree, const double *d_x, int64_t n, int32_t n_feat, int32_t *d_out,
                     void *stream) {
+    KP_NVTX("kp_tree_predict");
     if (!d_tree || n < 0 || n_feat <= 0 || n_feat > 16) return KP_EINVAL;
     if (n == 0) return KP_OK;
     int64_t want = (n + 255) / 256;
@@ -771,6 +776,7 @@ int kp_tree_predict(const void *d_tree, const double *d_x, int64_t n, int32_t n_
 int kp_seer_select_partials(const int64_t *d_parts, int32_t n_parts, int64_t n_rows, int64_t n_cols, int64_t nnz,
                             int64_t iterations, const void *d_selector, const void *d_known, const void *d_gathered,
                             kp_outcome *d_out, void *stream) {
+    KP_NVTX("kp_seer_select_partials");
     if (n_parts < 1 || n_rows <= 0 || n_cols <= 0 || !d_parts || !d_out || !d_selector || !d_known || !d_gathered)
         return KP_EINVAL;
     k_seer_select_partials<<<1, 32, 0, (cudaStream_t)stream>>>(d_parts, n_parts, n_rows, n_cols, nnz, iterations,

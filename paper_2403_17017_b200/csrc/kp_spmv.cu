@@ -38,7 +38,10 @@ struct PrepHeader {
     int64_t n_units;   // device-written for adaptive
     int64_t stats[4];  // ELL: (lo, hi, s1, s2) of row lengths (K1)
     int64_t cap;       // ELL reserved width
-    int64_t pad[9];
+    int64_t n_tail;    // ELL: rows longer than the width (device-written by K12) ...
+    int64_t n_long;    // ... of which this many have > kEllLongTail elements past it
+    int64_t n_short;   // ... and this many not (list-fill counter)
+    int64_t pad[6];
 };
 static_assert(sizeof(PrepHeader) <= kAlign, "header");
 constexpr size_t kRedWsBytes = 40960;  // >= kp_reduce_workspace_bytes()
@@ -340,11 +343,14 @@ __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__res
 }
 
 // ================================================================= ELL,TM (K9 + K12)
+// Thread per row over the warp-sliced ELL (width W = min(max_len, cap)).  Rows longer than
+// W (listed by K12) keep their first W elements here; k_ell_tail adds the rest.
 template <typename V, typename O>
 __global__ void __launch_bounds__(256) k_ell_tm(const PrepHeader *__restrict__ hdr, const int32_t *__restrict__ ecol,
-                                                const V *__restrict__ evalv, const O *__restrict__ off,
-                                                const int32_t *__restrict__ col, const V *__restrict__ val,
-                                                const V *__restrict__ x, V *__restrict__ y, int64_t n_rows) {
+                                                const V *__restrict__ evalv, const V *__restrict__ x,
+                                                V *__restrict__ y, int64_t n_rows) {
+    // the PDL-launched tail kernel may be scheduled now (it waits for this grid's completion)
+    asm volatile("griddepcontrol.launch_dependents;");
     const int64_t row = (int64_t)blockIdx.x * 256 + threadIdx.x;
     if (row >= n_rows) return;
     const int64_t wmax = __ldg(&hdr->stats[1]);
@@ -385,11 +391,52 @@ __global__ void __launch_bounds__(256) k_ell_tm(const PrepHeader *__restrict__ h
         for (int i = 0; i < 8; ++i)
             if (k + i < W) sum = fma_acc(sum, v[i], ld_x(x + c[i]));
     }
-    if (wmax > cap) {  // hybrid tail: rows longer than the reserved width continue in CSR
-        const int64_t s = ldo(off + row), e = ldo(off + row + 1);
-        for (int64_t j = s + W; j < e; j += 4) sum = batch_dot<4, 1>(col, val, x, j, e, sum);
-    }
     y[row] = sum;
+}
+
+// Hybrid tail of ELL,TM: rows longer than the width W (K12's lists) get their elements
+// W.. added here, in a fixed order (y stays bit-identical run to run): rows with more than
+// kEllLongTail remaining elements by a whole CTA each (block reduction), the others by one
+// warp each (lane-strided batches + shuffle tree).  Launched with PDL right behind
+// k_ell_tm: it waits for the sweep's y stores, and exits at once when K12 listed no row
+// (W = max_len, the favourable case).  (The tail used to continue serially in the row's
+// own thread: C2 4.3 ms, C4 115 ms.)
+constexpr int64_t kEllLongTail = 4096;
+constexpr int kEllTailThreads = 512;
+template <typename V, typename O>
+__global__ void __launch_bounds__(kEllTailThreads) k_ell_tail(const PrepHeader *__restrict__ hdr,
+                                                              const int64_t *__restrict__ tail, int64_t tail_slots,
+                                                              const O *__restrict__ off, const int32_t *__restrict__ col,
+                                                              const V *__restrict__ val, const V *__restrict__ x,
+                                                              V *__restrict__ y) {
+    __shared__ V sred[32];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int64_t nt = hdr->n_tail, nl = hdr->n_long;
+    if (nt == 0) return;
+    const int64_t wmax = hdr->stats[1], cap = hdr->cap;
+    const int64_t W = wmax < cap ? wmax : cap;
+    // long rows (listed from the back of the buffer): one CTA each
+    for (int64_t t = blockIdx.x; t < nl; t += gridDim.x) {
+        const int64_t row = tail[tail_slots - 1 - t];
+        const int64_t s = ldo(off + row) + W, e = ldo(off + row + 1);
+        V sum = 0;
+        for (int64_t j = s + threadIdx.x; j < e; j += 4 * kEllTailThreads)
+            sum = batch_dot<4, kEllTailThreads>(col, val, x, j, e, sum);
+        const V tot = block_sum(sum, sred);
+        if (threadIdx.x == 0) y[row] += tot;
+        __syncthreads();  // sred is reused by the next row
+    }
+    // the other listed rows: one warp each
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < nt - nl; t += nw) {
+        const int64_t row = tail[t];
+        const int64_t s = ldo(off + row) + W, e = ldo(off + row + 1);
+        V sum = 0;
+        for (int64_t j = s + lane; j < e; j += 4 * 32) sum = batch_dot<4, 32>(col, val, x, j, e, sum);
+        sum = group_sum<32>(sum);
+        if (lane == 0) y[row] += sum;
+    }
 }
 
 __global__ void k_prep_hdr(PrepHeader *hdr, int64_t kernel, int64_t cap) {
@@ -400,23 +447,50 @@ __global__ void k_prep_hdr(PrepHeader *hdr, int64_t kernel, int64_t cap) {
 }
 
 // K12: CSR -> warp-sliced column-major ELL of width W = min(max_len, cap): slot (row, k)
-// at (row/32)*32*W + 32*k + row%32; padding = (col 0, val 0).
+// at (row/32)*32*W + 32*k + row%32; padding = (col 0, val 0).  Rows longer than W are
+// appended to the tail list (one global atomic per CTA; list order is irrelevant: every
+// listed row is summed whole by one warp).
 template <typename V, typename O>
-__global__ void __launch_bounds__(256) k_prep_ell(const PrepHeader *__restrict__ hdr, const O *__restrict__ off,
+__global__ void __launch_bounds__(256) k_prep_ell(PrepHeader *__restrict__ hdr, const O *__restrict__ off,
                                                   const int32_t *__restrict__ col, const V *__restrict__ val,
-                                                  int32_t *__restrict__ ecol, V *__restrict__ evalv, int64_t n_rows) {
+                                                  int32_t *__restrict__ ecol, V *__restrict__ evalv,
+                                                  int64_t *__restrict__ tail, int64_t tail_slots, int64_t n_rows) {
+    __shared__ int s_cnt, s_lcnt;
+    __shared__ int64_t s_base, s_lbase;
     const int64_t row = (int64_t)blockIdx.x * 256 + threadIdx.x;
-    if (row >= n_rows) return;
-    const int64_t wmax = __ldg(&hdr->stats[1]);
-    const int64_t cap = __ldg(&hdr->cap);
+    const int64_t wmax = hdr->stats[1];
+    const int64_t cap = hdr->cap;
     const int64_t W = wmax < cap ? wmax : cap;
-    const int64_t s = ldo(off + row), e = ldo(off + row + 1);
-    for (int64_t k = 0; k < W; ++k) {
-        const int64_t j = s + k;
-        const bool in = j < e;
-        const int64_t slot = (row >> 5) * 32 * W + k * 32 + (row & 31);
-        ecol[slot] = in ? __ldg(col + j) : 0;
-        evalv[slot] = in ? __ldg(val + j) : V(0);
+    if (threadIdx.x == 0) s_cnt = s_lcnt = 0;
+    __syncthreads();
+    int slot_in_cta = -1;
+    bool is_long = false;
+    if (row < n_rows) {
+        const int64_t s = ldo(off + row), e = ldo(off + row + 1);
+        for (int64_t k = 0; k < W; ++k) {
+            const int64_t j = s + k;
+            const bool in = j < e;
+            const int64_t slot = (row >> 5) * 32 * W + k * 32 + (row & 31);
+            ecol[slot] = in ? __ldg(col + j) : 0;
+            evalv[slot] = in ? __ldg(val + j) : V(0);
+        }
+        if (e - s > W) {
+            is_long = e - s - W > kEllLongTail;
+            slot_in_cta = atomicAdd(is_long ? &s_lcnt : &s_cnt, 1);
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        // n_tail counts every listed row; short rows fill the list from the front, long
+        // rows from the back (tail_slots >= every listed row: no overlap)
+        if (s_cnt + s_lcnt > 0) atomicAdd((unsigned long long *)&hdr->n_tail, (unsigned long long)(s_cnt + s_lcnt));
+        if (s_cnt > 0) s_base = (int64_t)atomicAdd((unsigned long long *)&hdr->n_short, (unsigned long long)s_cnt);
+        if (s_lcnt > 0) s_lbase = (int64_t)atomicAdd((unsigned long long *)&hdr->n_long, (unsigned long long)s_lcnt);
+    }
+    __syncthreads();
+    if (slot_in_cta >= 0) {
+        if (is_long) tail[tail_slots - 1 - (s_lbase + slot_in_cta)] = row;
+        else tail[s_base + slot_in_cta] = row;
     }
 }
 
@@ -628,6 +702,9 @@ constexpr int kWarpTile = 32 * kIPT;  // 256 merge items per unit
 template <typename V>
 constexpr int kMergeMinBlocks = sizeof(V) == 4 ? 0 : 3;
 constexpr int kMergeWarps = 8;        // warps per CTA
+// CSR,WO with at most this many warp ranges finishes its carries in the last CTA (one
+// launch; small matrices, where the separate fix-up launch was ~1/6 of the SpMV)
+constexpr int64_t kFuseMaxRanges = 1024;
 
 // Persistent merge-path warps (Merrill & Garland, restructured for B200).  The merge of
 // A = row ends off[1..R] with B = nnz indices 0..Z-1 (row r's end item sits at merge
@@ -645,11 +722,12 @@ constexpr int kMergeWarps = 8;        // warps per CTA
 // row end marks its relative end position (atomicMax of tag<<9 | k+1, the tag = unit
 // counter makes stale marks of earlier units lose, so nothing is cleared), a max-scan
 // gives every position its row, and a thread-local + warp segmented scan sums rows.
-template <typename V, typename O, bool kPrep, bool kB = false>
+template <typename V, typename O, bool kPrep, bool kB = false, bool kFuse = false>
 __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_merge(
     const O *__restrict__ off, const int32_t *__restrict__ col, const V *__restrict__ val, const V *__restrict__ x,
     V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, int64_t upw, int64_t n_ranges,
-    const int64_t *__restrict__ part, int32_t *__restrict__ crow, V *__restrict__ cval, YDst<V> dst = YDst<V>{}) {
+    const int64_t *__restrict__ part, int32_t *__restrict__ crow, V *__restrict__ cval, YDst<V> dst = YDst<V>{},
+    unsigned *__restrict__ ticket = nullptr) {
     constexpr int kPad = kWarpTile + kWarpTile / 32;
     __shared__ V s_prod[kMergeWarps][kPad];
     __shared__ int32_t s_mark[kMergeWarps][kPad];
@@ -672,6 +750,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
         const int64_t wc = wid < n_ranges ? wid : wl;
         r0 = merge_search_cta(off, n_rows, nnz, wc * upw * kWarpTile, w0 * upw * kWarpTile, wl * upw * kWarpTile, s_q);
     }
+    auto body = [&]() {
     if (wid >= n_ranges) return;
     const int64_t total = n_rows + nnz;
     const int64_t u_begin = wid * upw;
@@ -836,6 +915,30 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
         const bool open = r0 < n_rows;
         crow[wid] = open ? (int32_t)r0 : -1;
         cval[wid] = open ? carry : V(0);
+    }
+    };
+    body();
+    if constexpr (kFuse) {
+        // Small inputs (few ranges): the carry fix-up runs in the LAST CTA to finish instead
+        // of a second launch.  Threadfence-reduction pattern: every CTA publishes its carries
+        // and y stores, then takes a ticket; the CTA holding the last ticket sums each run
+        // of equal carry rows (one thread per run head, fixed order) into y and re-arms the
+        // ticket for the next launch (the workspace is zeroed once by its owner).
+        __shared__ bool s_last;
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+        __syncthreads();
+        if (!s_last) return;
+        __threadfence();
+        for (int64_t u = threadIdx.x; u < n_ranges; u += blockDim.x) {
+            const int32_t r = __ldcg(crow + u);
+            if (r < 0 || (u > 0 && __ldcg(crow + u - 1) == r)) continue;  // no carry / not a run head
+            V acc = __ldcg(cval + u);
+            for (int64_t v = u + 1; v < n_ranges && __ldcg(crow + v) == r; ++v) acc += __ldcg(cval + v);
+            y[r] = __ldcg(y + r) + acc;
+        }
+        if (threadIdx.x == 0) *ticket = 0;
     }
 }
 
@@ -1419,6 +1522,10 @@ struct Layout {
     size_t hdr = 0, red = 0, a = 0, b = 0, c = 0, total = 0;
 };
 
+// ELL tail list capacity: at most nnz / (cap + 1) rows are longer than W >= cap ... or,
+// when W = max_len < cap, none
+int64_t ell_tail_slots(const kp_csr *A, int64_t cap) { return A->nnz / (cap + 1) + 1; }
+
 Layout prep_layout(int32_t kernel, const kp_csr *A, int64_t cap) {
     Layout L;
     size_t o = align_up(sizeof(PrepHeader));
@@ -1428,6 +1535,8 @@ Layout prep_layout(int32_t kernel, const kp_csr *A, int64_t cap) {
             const size_t rpad = (size_t)((A->n_rows + 31) / 32 * 32);
             L.a = o; o += align_up((size_t)cap * rpad * sizeof(int32_t));
             L.b = o; o += align_up((size_t)cap * rpad * val_bytes(A));
+            // tail list: rows longer than W >= ... at most nnz / (cap + 1) of them
+            L.c = o; o += align_up((size_t)ell_tail_slots(A, cap) * sizeof(int64_t));
             break;
         }
         case KP_COO_WM:
@@ -1476,7 +1585,9 @@ int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, 
             if (g > 0) {
                 k_prep_ell<V, O><<<(unsigned)g, 256, 0, s>>>(hdr, off, A->col_indices, val,
                                                               reinterpret_cast<int32_t *>(buf + L.a),
-                                                              reinterpret_cast<V *>(buf + L.b), A->n_rows);
+                                                              reinterpret_cast<V *>(buf + L.b),
+                                                              reinterpret_cast<int64_t *>(buf + L.c),
+                                                              ell_tail_slots(A, cap), A->n_rows);
                 KP_LAUNCHED();
             }
             P->n_units = 0;
@@ -1556,9 +1667,12 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
     const V *val = reinterpret_cast<const V *>(A->values);
     const int64_t R = A->n_rows, Z = A->nnz;
     const int sms = num_sms();
-    // carries live in the workspace: [int32 rows | V vals]
+    // carries live in the workspace: [16-byte ticket | int32 rows | V vals]; the ticket (the
+    // fused CSR,WO fix-up's last-CTA counter) is zero when the owner hands the workspace
+    // over and is left zero by every launch
     const int64_t nu = spmv_units(kernel, A);
-    int32_t *crow = reinterpret_cast<int32_t *>(ws);
+    unsigned *ticket = reinterpret_cast<unsigned *>(ws);
+    int32_t *crow = reinterpret_cast<int32_t *>(ws + 16);
     V *cval = reinterpret_cast<V *>(ws + align_up((size_t)nu * sizeof(int32_t) + 16));
     switch (kernel) {
         case KP_CSR_WM: {
@@ -1611,9 +1725,16 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
             const Layout L = prep_layout(KP_ELL_TM, A, P->ell_cap);
             unsigned char *b = reinterpret_cast<unsigned char *>(P->buf);
             const int64_t g = (R + 255) / 256;
-            k_ell_tm<V, O><<<(unsigned)g, 256, 0, s>>>(reinterpret_cast<const PrepHeader *>(b),
-                                                       reinterpret_cast<const int32_t *>(b + L.a),
-                                                       reinterpret_cast<const V *>(b + L.b), off, col, val, x, y, R);
+            const PrepHeader *hdr = reinterpret_cast<const PrepHeader *>(b);
+            k_ell_tm<V, O><<<(unsigned)g, 256, 0, s>>>(hdr, reinterpret_cast<const int32_t *>(b + L.a),
+                                                       reinterpret_cast<const V *>(b + L.b), x, y, R);
+            KP_LAUNCHED();
+            // tail warps: enough for the longest rows to spread over every SM (at most
+            // nnz / (cap + 1) rows can be listed)
+            const int64_t slots = ell_tail_slots(A, P->ell_cap);
+            const int64_t tail_ctas = std::max<int64_t>(1, std::min<int64_t>((int64_t)sms * 2, (slots + 15) / 16));
+            KP_CUDA_TRY(launch_pdl(k_ell_tail<V, O>, (unsigned)tail_ctas, kEllTailThreads, s, hdr,
+                                   reinterpret_cast<const int64_t *>(b + L.c), slots, off, col, val, x, y));
             KP_LAUNCHED();
             return KP_OK;
         }
@@ -1739,6 +1860,7 @@ int kp_prepare_bytes(int32_t kernel, const kp_csr *A, int64_t ell_cap, size_t *b
 
 int kp_prepare(int32_t kernel, const kp_csr *A, int64_t ell_cap, void *d_buf, size_t bytes, kp_prepared *out,
                void *stream) {
+    KP_NVTX("kp_prepare");
     if (!valid_csr(A) || !out || kernel < 0 || kernel >= KP_NUM_KERNELS) return KP_EINVAL;
     if (kernel == KP_ELL_TM && ell_cap < 1) return KP_EINVAL;
     const Layout L = prep_layout(kernel, A, kernel == KP_ELL_TM ? ell_cap : 0);
@@ -1769,6 +1891,7 @@ int kp_spmv_workspace_bytes(int32_t kernel, const kp_csr *A, size_t *bytes) {
 
 int kp_spmv(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x, void *d_y, void *d_ws,
             size_t ws_bytes, void *stream) {
+    KP_NVTX(::kp::kernel_label(kernel));
     if (!valid_csr(A) || kernel < 0 || kernel >= KP_NUM_KERNELS || !d_y || (A->n_cols > 0 && !d_x)) return KP_EINVAL;
     size_t need = 0;
     kp_spmv_workspace_bytes(kernel, A, &need);
@@ -1798,6 +1921,7 @@ int64_t kp_debug_set_wave_warps(int64_t warps) {
 
 int kp_spmv_bcast(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x, const kp_peers *peers,
                   void *d_ws, size_t ws_bytes, void *stream) {
+    KP_NVTX("kp_spmv_bcast");
     if (!valid_csr(A) || !peers || peers->n < 1 || peers->n > KP_MAX_PEERS || peers->self < 0 ||
         peers->self >= peers->n || (kernel != KP_CSR_MP && kernel != KP_CSR_WO) || (A->n_cols > 0 && !d_x))
         return KP_EINVAL;
@@ -1824,6 +1948,7 @@ int kp_spmv_bcast(int32_t kernel, const kp_csr *A, const kp_prepared *P, const v
 
 int kp_shard_partition(const void *d_off, int32_t off_type, int64_t n_rows, int32_t parts, int64_t *d_cuts,
                        void *stream) {
+    KP_NVTX("kp_shard_partition");
     if (!d_off || !d_cuts || parts < 1 || n_rows < 0) return KP_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     const unsigned g = (unsigned)((parts + 1 + 255) / 256);

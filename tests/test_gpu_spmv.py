@@ -86,6 +86,35 @@ def test_ell_hybrid_tail_small_cap(orc):
     assert orc.spmv_check(y.cpu().numpy(), yref, absy, 1e-5)[0]
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("cap", [1, 3, 17, 4096])
+def test_ell_tail_lists(cap, dtype, orc):
+    """K12's tail lists: rows longer than the width W go to the warp list, rows with more
+    than kEllLongTail (4096) elements past W to the CTA list; the sweep keeps their first W
+    elements and k_ell_tail adds the rest.  Lengths straddle W and W + 4096 for each cap;
+    re-runs are bit-identical (the lists' order is atomic-dependent, the sums are not)."""
+    lens = [0, 1, 2, 3, 4, 5, 16, 17, 18, 40, 4096, 4097, 4099, 4100, 4113, 9000, 30000, 0, 7, 100000]
+    lens = lens * 3
+    rows = np.repeat(np.arange(len(lens)), lens)
+    cols = np.concatenate([(np.arange(l) * 7919) % 150000 for l in lens])
+    m = gen.from_coo("elltail", len(lens), 150000, torch.tensor(rows), torch.tensor(cols), 11)
+    A = m.to_device_csr(dtype)
+    P = kernels.prepare(A, kernels.ELL_TM, ell_cap=cap, cache=False)
+    x = (torch.rand(A.n_cols, dtype=torch.float64, generator=torch.Generator().manual_seed(5)) * 2 - 1).to(dtype).cuda()
+    y = torch.full((A.n_rows,), float("nan"), dtype=dtype, device="cuda")
+    kernels.spmv(A, x, kernels.ELL_TM, y=y, prepared=P)
+    off, col, val = A.to_host()
+    yref, absy = orc.spmv_csr(off, col, val, x.cpu().numpy())
+    ok, r = orc.spmv_check(y.cpu().numpy(), yref, absy, TOL[dtype])
+    assert ok, (cap, r)
+    hdr = P.buf[:128].cpu().view(torch.int64)
+    W = min(int(hdr[3]), cap)
+    assert int(hdr[7]) == sum(1 for v in lens if v > W)                    # n_tail
+    assert int(hdr[8]) == sum(1 for v in lens if v - W > 4096)             # n_long
+    for _ in range(2):
+        assert torch.equal(kernels.spmv(A, x, kernels.ELL_TM, prepared=P), y)
+
+
 def test_c2_full_size_every_kernel_agrees(orc):
     """Full-size C2 (R-MAT s20): every kernel vs the oracle (sampled-free full check)."""
     m = gen.config("C2", device="cuda")
