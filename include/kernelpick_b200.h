@@ -173,8 +173,7 @@ KP_API int kp_prepare(int32_t kernel, const kp_csr *A, int64_t ell_cap, void *d_
 KP_API int kp_spmv_workspace_bytes(int32_t kernel, const kp_csr *A, size_t *bytes);
 /* y = A . x with kernel `kernel` (KP_*).  d_x has n_cols entries, d_y n_rows, both of
  * A->val_type.  Deterministic: no floating-point atomics; repeated calls give
- * identical bits.  The first 16 bytes of d_ws must be zero when a workspace is first
- * handed over (a last-CTA ticket of small CSR,WO launches; every call leaves it zero). */
+ * identical bits. */
 KP_API int kp_spmv(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x,
             void *d_y, void *d_ws, size_t ws_bytes, void *stream);
 

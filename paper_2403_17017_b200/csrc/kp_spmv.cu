@@ -702,9 +702,6 @@ constexpr int kWarpTile = 32 * kIPT;  // 256 merge items per unit
 template <typename V>
 constexpr int kMergeMinBlocks = sizeof(V) == 4 ? 0 : 3;
 constexpr int kMergeWarps = 8;        // warps per CTA
-// CSR,WO with at most this many warp ranges finishes its carries in the last CTA (one
-// launch; small matrices, where the separate fix-up launch was ~1/6 of the SpMV)
-constexpr int64_t kFuseMaxRanges = 1024;
 
 // Persistent merge-path warps (Merrill & Garland, restructured for B200).  The merge of
 // A = row ends off[1..R] with B = nnz indices 0..Z-1 (row r's end item sits at merge
@@ -722,12 +719,11 @@ constexpr int64_t kFuseMaxRanges = 1024;
 // row end marks its relative end position (atomicMax of tag<<9 | k+1, the tag = unit
 // counter makes stale marks of earlier units lose, so nothing is cleared), a max-scan
 // gives every position its row, and a thread-local + warp segmented scan sums rows.
-template <typename V, typename O, bool kPrep, bool kB = false, bool kFuse = false>
+template <typename V, typename O, bool kPrep, bool kB = false>
 __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_merge(
     const O *__restrict__ off, const int32_t *__restrict__ col, const V *__restrict__ val, const V *__restrict__ x,
     V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, int64_t upw, int64_t n_ranges,
-    const int64_t *__restrict__ part, int32_t *__restrict__ crow, V *__restrict__ cval, YDst<V> dst = YDst<V>{},
-    unsigned *__restrict__ ticket = nullptr) {
+    const int64_t *__restrict__ part, int32_t *__restrict__ crow, V *__restrict__ cval, YDst<V> dst = YDst<V>{}) {
     constexpr int kPad = kWarpTile + kWarpTile / 32;
     __shared__ V s_prod[kMergeWarps][kPad];
     __shared__ int32_t s_mark[kMergeWarps][kPad];
@@ -750,7 +746,6 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
         const int64_t wc = wid < n_ranges ? wid : wl;
         r0 = merge_search_cta(off, n_rows, nnz, wc * upw * kWarpTile, w0 * upw * kWarpTile, wl * upw * kWarpTile, s_q);
     }
-    auto body = [&]() {
     if (wid >= n_ranges) return;
     const int64_t total = n_rows + nnz;
     const int64_t u_begin = wid * upw;
@@ -915,30 +910,6 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
         const bool open = r0 < n_rows;
         crow[wid] = open ? (int32_t)r0 : -1;
         cval[wid] = open ? carry : V(0);
-    }
-    };
-    body();
-    if constexpr (kFuse) {
-        // Small inputs (few ranges): the carry fix-up runs in the LAST CTA to finish instead
-        // of a second launch.  Threadfence-reduction pattern: every CTA publishes its carries
-        // and y stores, then takes a ticket; the CTA holding the last ticket sums each run
-        // of equal carry rows (one thread per run head, fixed order) into y and re-arms the
-        // ticket for the next launch (the workspace is zeroed once by its owner).
-        __shared__ bool s_last;
-        __threadfence();
-        __syncthreads();
-        if (threadIdx.x == 0) s_last = atomicAdd(ticket, 1u) == gridDim.x - 1;
-        __syncthreads();
-        if (!s_last) return;
-        __threadfence();
-        for (int64_t u = threadIdx.x; u < n_ranges; u += blockDim.x) {
-            const int32_t r = __ldcg(crow + u);
-            if (r < 0 || (u > 0 && __ldcg(crow + u - 1) == r)) continue;  // no carry / not a run head
-            V acc = __ldcg(cval + u);
-            for (int64_t v = u + 1; v < n_ranges && __ldcg(crow + v) == r; ++v) acc += __ldcg(cval + v);
-            y[r] = __ldcg(y + r) + acc;
-        }
-        if (threadIdx.x == 0) *ticket = 0;
     }
 }
 
@@ -1667,12 +1638,9 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
     const V *val = reinterpret_cast<const V *>(A->values);
     const int64_t R = A->n_rows, Z = A->nnz;
     const int sms = num_sms();
-    // carries live in the workspace: [16-byte ticket | int32 rows | V vals]; the ticket (the
-    // fused CSR,WO fix-up's last-CTA counter) is zero when the owner hands the workspace
-    // over and is left zero by every launch
+    // carries live in the workspace: [int32 rows | V vals]
     const int64_t nu = spmv_units(kernel, A);
-    unsigned *ticket = reinterpret_cast<unsigned *>(ws);
-    int32_t *crow = reinterpret_cast<int32_t *>(ws + 16);
+    int32_t *crow = reinterpret_cast<int32_t *>(ws);
     V *cval = reinterpret_cast<V *>(ws + align_up((size_t)nu * sizeof(int32_t) + 16));
     switch (kernel) {
         case KP_CSR_WM: {

@@ -100,7 +100,7 @@ def spmv_workspace(A: DeviceCSR, kernel: int, stream=None):
     key = (A.device, kernel, _lib.stream_handle(stream, A.device))
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < n:
-        ws = torch.zeros(n, dtype=torch.uint8, device=A.device)  # the fused fix-up's ticket starts at 0
+        ws = torch.empty(n, dtype=torch.uint8, device=A.device)
         _ws_cache[key] = ws
     return ws
 
