@@ -56,6 +56,7 @@ int launch_plan_select(const void *d_off, int32_t off_type, int64_t n_rows, int6
                        cudaGraphConditionalHandle h, cudaStream_t s);
 
 // ----------------------------------------------------------------- load helpers
+
 // Streamed (read-once) data: non-coherent path, do not allocate in L1 so the x
 // gathers keep the L1.
 __device__ __forceinline__ int32_t ld_stream(const int32_t *p) {

@@ -693,14 +693,26 @@ __device__ __forceinline__ int64_t merge_search_cta(const O *off, int64_t n_rows
     return merge_search_warp_in(off, d, l, h);
 }
 
-constexpr int kWarpTile = 32 * kIPT;  // 256 merge items per unit
+// merge items per lane: 8 (256-item units); fp64 may use 4 (128-item units) to halve the
+// per-lane arrays and raise the resident warps
+#ifndef KP_MERGE_IPT64
+#define KP_MERGE_IPT64 8
+#endif
+template <typename V>
+constexpr int kMergeIPT = sizeof(V) == 8 ? KP_MERGE_IPT64 : kIPT;
 // fp64: 3 CTAs (24 warps) per SM in 80 registers instead of 2 at its natural ~110
 // (band-27 fp64 476 -> 402 us, gather-bound inputs unchanged).  fp32 keeps the compiler's
 // allocation (0 = no minimum): 64 registers / 4 CTAs for the plain kernel; the fused-
 // exchange variant lands at ~112 / 2 CTAs, which measured faster on the DRAM-bound C5
 // shards (916 vs 877 GB/s with a forced 4 CTAs).
 template <typename V>
-constexpr int kMergeMinBlocks = sizeof(V) == 4 ? 0 : 3;
+#ifndef KP_MERGE_MINB_F32
+#define KP_MERGE_MINB_F32 0
+#endif
+#ifndef KP_MERGE_MINB_F64
+#define KP_MERGE_MINB_F64 3
+#endif
+constexpr int kMergeMinBlocks = sizeof(V) == 4 ? KP_MERGE_MINB_F32 : KP_MERGE_MINB_F64;
 constexpr int kMergeWarps = 8;        // warps per CTA
 
 // Persistent merge-path warps (Merrill & Garland, restructured for B200).  The merge of
@@ -724,10 +736,11 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
     const O *__restrict__ off, const int32_t *__restrict__ col, const V *__restrict__ val, const V *__restrict__ x,
     V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, int64_t upw, int64_t n_ranges,
     const int64_t *__restrict__ part, int32_t *__restrict__ crow, V *__restrict__ cval, YDst<V> dst = YDst<V>{}) {
-    constexpr int kPad = kWarpTile + kWarpTile / 32;
+    constexpr int kI = kMergeIPT<V>, kT = 32 * kI;  // items per lane / per unit
+    constexpr int kPad = kT + kT / 32;
     __shared__ V s_prod[kMergeWarps][kPad];
     __shared__ int32_t s_mark[kMergeWarps][kPad];
-    __shared__ V s_rowv[kMergeWarps][kWarpTile + 1];  // value of each row ending in the unit (+ the open one)
+    __shared__ V s_rowv[kMergeWarps][kT + 1];  // value of each row ending in the unit (+ the open one)
     // let the PDL-launched carry fix-up be scheduled now: its griddepcontrol.wait still
     // waits for this grid's completion and memory flush, only the launch latency is hidden
     asm volatile("griddepcontrol.launch_dependents;");
@@ -744,7 +757,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
         const int64_t w0 = (int64_t)blockIdx.x * kMergeWarps;
         const int64_t wl = w0 + kMergeWarps - 1 < n_ranges - 1 ? w0 + kMergeWarps - 1 : n_ranges - 1;
         const int64_t wc = wid < n_ranges ? wid : wl;
-        r0 = merge_search_cta(off, n_rows, nnz, wc * upw * kWarpTile, w0 * upw * kWarpTile, wl * upw * kWarpTile, s_q);
+        r0 = merge_search_cta(off, n_rows, nnz, wc * upw * kT, w0 * upw * kT, wl * upw * kT, s_q);
     }
     if (wid >= n_ranges) return;
     const int64_t total = n_rows + nnz;
@@ -757,41 +770,41 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
     if (kPrep) r0 = part[wid];
     int64_t row_start = ldo(off + r0);  // r0 < n_rows: the range starts before the last item
     V carry = V(0);
-    const int jb = lane * kIPT;
+    const int jb = lane * kI;
     int32_t tag = 0;
     // software pipeline: unit u+1's (col, val) loads are issued as soon as unit u's row count
     // fixes where they start, so their HBM latency overlaps unit u's gathers / scans
-    auto load_cv = [&](int64_t j0, int32_t (&c)[kIPT], V (&v)[kIPT]) {
-        if (j0 + kWarpTile <= nnz) {  // common case: unpredicated, immediate offsets
+    auto load_cv = [&](int64_t j0, int32_t (&c)[kI], V (&v)[kI]) {
+        if (j0 + kT <= nnz) {  // common case: unpredicated, immediate offsets
             const int32_t *cp = col + j0 + lane;
             const V *vp = val + j0 + lane;
 #pragma unroll
-            for (int t = 0; t < kIPT; ++t) {
+            for (int t = 0; t < kI; ++t) {
                 c[t] = ld_stream(cp + t * 32);
                 v[t] = ld_stream(vp + t * 32);
             }
         } else {
 #pragma unroll
-            for (int t = 0; t < kIPT; ++t) {
+            for (int t = 0; t < kI; ++t) {
                 const int64_t j = j0 + lane + t * 32;
                 c[t] = j < nnz ? ld_stream(col + j) : 0;
                 v[t] = j < nnz ? ld_stream(val + j) : V(0);
             }
         }
     };
-    int32_t cn[kIPT];
-    V vn[kIPT];
-    if (u_begin < u_end) load_cv(u_begin * kWarpTile - r0, cn, vn);
+    int32_t cn[kI];
+    V vn[kI];
+    if (u_begin < u_end) load_cv(u_begin * kT - r0, cn, vn);
     for (int64_t u = u_begin; u < u_end; ++u) {
         tag += 1 << 9;
-        const int64_t d0 = u * kWarpTile;
-        const int64_t d1 = d0 + kWarpTile < total ? d0 + kWarpTile : total;
+        const int64_t d0 = u * kT;
+        const int64_t d1 = d0 + kT < total ? d0 + kT : total;
         const int64_t j0 = d0 - r0;
         // x gathers of this unit (loaded last iteration) + round 0 of the row-end probe
-        V p[kIPT];
-        V vv[kIPT];
+        V p[kI];
+        V vv[kI];
 #pragma unroll
-        for (int t = 0; t < kIPT; ++t) {
+        for (int t = 0; t < kI; ++t) {
             vv[t] = vn[t];
             p[t] = ld_x(x + cn[t]);
         }
@@ -819,32 +832,32 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
         const int nz = (int)((d1 - d0) - nr);
         if (u + 1 < u_end) load_cv(d1 - (r0 + nr), cn, vn);
 #pragma unroll
-        for (int t = 0; t < kIPT; ++t) p[t] *= vv[t];
+        for (int t = 0; t < kI; ++t) p[t] *= vv[t];
         if (nr == 0) {
             // the whole unit is one row's elements (long rows): no row ends, no marks, no
             // scans -- lane sums + a shuffle tree into the running carry (fixed order)
             V sum = V(0);
 #pragma unroll
-            for (int t = 0; t < kIPT; ++t) sum += (lane + t * 32 < nz) ? p[t] : V(0);
+            for (int t = 0; t < kI; ++t) sum += (lane + t * 32 < nz) ? p[t] : V(0);
             carry += group_sum<32>(sum);
             continue;
         }
         if (lane == 0) rowv[nr] = V(0);  // open row: partial stays 0 unless it has elements here
         // stage products (positions >= nz belong to the next unit: zero)
 #pragma unroll
-        for (int t = 0; t < kIPT; ++t) {
+        for (int t = 0; t < kI; ++t) {
             const int k = lane + t * 32;
             prod[k + (k >> 5)] = k < nz ? p[t] : V(0);
         }
         __syncwarp();
         // blocked read-back: products and row index of every owned position
-        int ri[kIPT];
+        int ri[kI];
         {
             // max-scan of the RAW marks floored at `tag`: current marks (tag | k+1) beat
             // every stale one (smaller tag), so ri holds tag + row index without decoding
             int run = tag;
 #pragma unroll
-            for (int t = 0; t < kIPT; ++t) {
+            for (int t = 0; t < kI; ++t) {
                 const int q = jb + t + ((jb + t) >> 5);
                 p[t] = prod[q];
                 run = max(run, mark[q]);
@@ -859,23 +872,23 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
             int excl = __shfl_up_sync(0xffffffffu, incl, 1);
             if (lane == 0) excl = 0;
 #pragma unroll
-            for (int t = 0; t < kIPT; ++t) ri[t] = max(ri[t], excl);
+            for (int t = 0; t < kI; ++t) ri[t] = max(ri[t], excl);
         }
         // thread-local segmented scan
-        V acc[kIPT];
-        int first_head = kIPT;
-        const int prev_last = __shfl_up_sync(0xffffffffu, ri[kIPT - 1], 1);
+        V acc[kI];
+        int first_head = kI;
+        const int prev_last = __shfl_up_sync(0xffffffffu, ri[kI - 1], 1);
 #pragma unroll
-        for (int t = 0; t < kIPT; ++t) {
+        for (int t = 0; t < kI; ++t) {
             const bool head = t == 0 ? (lane == 0 || ri[0] != prev_last) : ri[t] != ri[t - 1];
-            if (head && first_head == kIPT) first_head = t;
+            if (head && first_head == kI) first_head = t;
             acc[t] = (head || t == 0) ? p[t] : acc[t - 1] + p[t];
         }
         // warp segmented scan of the lanes' last-segment sums; the head flags travel as
         // one ballot mask (lane l combines lane l-o unless a head lies in (l-o, l])
-        V inc = acc[kIPT - 1];
+        V inc = acc[kI - 1];
         {
-            const unsigned heads = __ballot_sync(0xffffffffu, first_head < kIPT);
+            const unsigned heads = __ballot_sync(0xffffffffu, first_head < kI);
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const V up = __shfl_up_sync(0xffffffffu, inc, o);
@@ -886,9 +899,9 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
         if (lane == 0) cin = V(0);
         const int next_first = __shfl_down_sync(0xffffffffu, ri[0], 1);
 #pragma unroll
-        for (int t = 0; t < kIPT; ++t) {
+        for (int t = 0; t < kI; ++t) {
             const int pos = jb + t;
-            const int rnext = (t + 1 < kIPT) ? ri[t + 1] : next_first;
+            const int rnext = (t + 1 < kI) ? ri[t + 1] : next_first;
             if (pos < nz && (pos == nz - 1 || rnext != ri[t])) {  // last element of its row in the unit
                 V vt = t < first_head ? acc[t] + cin : acc[t];
                 if (ri[t] == tag) vt += carry;  // row index 0: continued from earlier units
@@ -916,13 +929,13 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
 // K10: merge-path partition = the first coordinate of every warp range (one warp per
 // range, 32-ary search over the row ends; O(#ranges) ~ one wave of warps, independent
 // of the matrix size).  part[n_ranges] = n_rows.
-template <typename O>
+template <typename O, int kT>
 __global__ void __launch_bounds__(256) k_prep_mp(const O *__restrict__ off, int64_t n_rows, int64_t nnz,
                                                  int64_t upw, int64_t n_ranges, int64_t *__restrict__ part) {
     const int64_t wid = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     if (wid > n_ranges) return;
     const int64_t total = n_rows + nnz;
-    int64_t d = wid * upw * kWarpTile;
+    int64_t d = wid * upw * kT;
     if (d > total) d = total;
     const int64_t r = merge_search_warp(off, n_rows, nnz, d);
     if ((threadIdx.x & 31) == 0) part[wid] = wid == n_ranges ? n_rows : r;
@@ -1412,7 +1425,8 @@ int tm_rows_per_thread(const kp_csr *A, int cap) {
     return rpt;
 }
 
-int64_t merge_tiles(const kp_csr *A) { return (A->n_rows + A->nnz + kWarpTile - 1) / kWarpTile; }
+int64_t merge_tile_items(const kp_csr *A) { return 32 * (A->val_type == KP_F64 ? kMergeIPT<double> : kMergeIPT<float>); }
+int64_t merge_tiles(const kp_csr *A) { return (A->n_rows + A->nnz + merge_tile_items(A) - 1) / merge_tile_items(A); }
 // Persistent merge geometry: units of 256 merge items, `upw` consecutive units per warp so
 // that one wave of resident warps (occupancy API, cached per instantiation) covers the
 // matrix.  Used identically by the K10 partition and the SpMV launch.
@@ -1581,7 +1595,7 @@ int prepare_t(int32_t kernel, const kp_csr *A, int64_t cap, unsigned char *buf, 
         case KP_CSR_MP: {
             const MergeGeom G = merge_geom<V, O>(A);
             const int64_t g = ((G.n_ranges + 1) * 32 + 255) / 256;
-            k_prep_mp<O><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, G.upw, G.n_ranges,
+            k_prep_mp<O, 32 * kMergeIPT<V>><<<(unsigned)g, 256, 0, s>>>(off, A->n_rows, A->nnz, G.upw, G.n_ranges,
                                                       reinterpret_cast<int64_t *>(buf + L.a));
             KP_LAUNCHED();
             P->n_units = G.n_ranges;
