@@ -212,6 +212,26 @@ KP_API int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_
                                kp_outcome *d_out, kp_seer_plan **plan, void *stream);
 KP_API int kp_seer_plan_launch(kp_seer_plan *plan, void *stream);
 KP_API int kp_seer_plan_destroy(kp_seer_plan *plan);
+/* How a plan selects on each launch: KP_SELECT_STATIC (known path, resolved at creation:
+ * the graph is the chosen body alone), KP_SELECT_EMITTED (the bundle compiled in from
+ * include/kp_seer_trees.h, used when the plan's trees equal it byte for byte),
+ * KP_SELECT_PARAM (packed trees by value in the selection kernel's parameters) or
+ * KP_SELECT_TABLE (trees deeper than 127 nodes, walked in device memory). */
+#define KP_SELECT_STATIC 0
+#define KP_SELECT_EMITTED 1
+#define KP_SELECT_PARAM 2
+#define KP_SELECT_TABLE 3
+KP_API int kp_seer_plan_select_kind(const kp_seer_plan *plan);
+
+/* -------------------------------------------------------- emitted trees
+ * The frozen bundle's three trees compiled into the library as nested conditionals
+ * (include/kp_seer_trees.h, generated by tools/emit_trees.py from models/seer_b200.json).
+ * d_out[i] = tree(d_x[i*nf:]) for tree 0 = selector (nf 4), 1 = known (nf 4),
+ * 2 = gathered (nf 8); the same answers as kp_tree_predict on the packed bundle. */
+KP_API int kp_seer_emitted_predict(int32_t tree, const double *d_x, int64_t n, int32_t *d_out,
+                                   void *stream);
+/* KP_SEER_TREES_SHA256 of the compiled-in bundle (sha256 of the three packed trees). */
+KP_API const char *kp_seer_emitted_sha256(void);
 
 /* ------------------------------------------------------------ canonicalisation (COO -> CSR) */
 /* Scratch bytes kp_csr_from_coo needs for n triples (n < 2^31). */

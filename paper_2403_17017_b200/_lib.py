@@ -20,6 +20,7 @@ KP_OK, KP_EINVAL, KP_ECUDA, KP_ENOMEM, KP_EUNSUPPORTED, KP_ERANGE = 0, -1, -2, -
 KP_I32, KP_I64 = 0, 1
 KP_F32, KP_F64 = 0, 1
 KP_USE_KNOWN, KP_USE_GATHERED = 0, 1
+KP_SELECT_STATIC, KP_SELECT_EMITTED, KP_SELECT_PARAM, KP_SELECT_TABLE = 0, 1, 2, 3
 
 EXPORTS = (
     "kp_reduce_workspace_bytes", "kp_length_stats", "kp_wave_ceil_max_sum", "kp_gather_features",
@@ -28,7 +29,7 @@ EXPORTS = (
     "kp_seer_plan_destroy", "kp_shard_partition", "kp_version", "kp_launch_count", "kp_debug_set_wave_warps",
     "kp_seer_select_partials", "kp_coo_workspace_bytes", "kp_csr_from_coo", "kp_spmv_bcast",
     "kp_mm_header", "kp_mm_parse", "kp_watchdog_start", "kp_watchdog_heartbeat", "kp_watchdog_status",
-    "kp_watchdog_stop",
+    "kp_watchdog_stop", "kp_seer_plan_select_kind", "kp_seer_emitted_predict", "kp_seer_emitted_sha256",
 )
 
 
@@ -121,6 +122,9 @@ def load(require: bool = True):
         "kp_watchdog_heartbeat": (ctypes.c_int, [p]),
         "kp_watchdog_status": (ctypes.c_int, [p, P(i32), ctypes.c_char_p, sz]),
         "kp_watchdog_stop": (ctypes.c_int, [p]),
+        "kp_seer_plan_select_kind": (ctypes.c_int, [p]),
+        "kp_seer_emitted_predict": (ctypes.c_int, [i32, p, i64, p, p]),
+        "kp_seer_emitted_sha256": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

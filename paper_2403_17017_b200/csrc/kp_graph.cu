@@ -26,6 +26,7 @@ struct kp_seer_plan {
     cudaGraphExec_t exec = nullptr;
     cudaGraphConditionalHandle handle = 0;
     int32_t static_kernel = -1;  // >= 0: known-path plan (body only, no SWITCH)
+    int32_t select_kind = KP_SELECT_STATIC;
     kp_prepared prep[KP_NUM_KERNELS] = {};
 };
 
@@ -102,6 +103,10 @@ int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap, co
     ParamTrees *trees = new ParamTrees();
     const bool use_param_trees = plan_trees_load(d_selector, d_known, d_gathered, trees) == KP_OK;
     cudaGetLastError();
+    // the bundle compiled in from include/kp_seer_trees.h, when these are its trees
+    // (KP_NO_EMITTED_TREES=1 forces the interpreter, for A/B timing)
+    const char *no_emit = getenv("KP_NO_EMITTED_TREES");
+    const bool use_emitted = use_param_trees && !(no_emit && no_emit[0] == '1') && emitted_trees_match(*trees);
     struct TreesGuard {
         ParamTrees *t;
         ~TreesGuard() { delete t; }
@@ -152,11 +157,13 @@ int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap, co
         return fail(KP_ECUDA);
     if (use_param_trees) {
         // one kernel: selection with the trees in its parameter space, sets the SWITCH value
-        rc = launch_plan_select(A->row_offsets, A->off_type, A->n_rows, A->n_cols, A->nnz, iterations, *trees, d_out,
-                                d_red_ws, P->handle, s);
+        rc = launch_plan_select(A->row_offsets, A->off_type, A->n_rows, A->n_cols, A->nnz, iterations, *trees,
+                                use_emitted, d_out, d_red_ws, P->handle, s);
+        P->select_kind = use_emitted ? KP_SELECT_EMITTED : KP_SELECT_PARAM;
     } else {
         rc = kp_seer_select(A->row_offsets, A->off_type, A->n_rows, A->n_cols, A->nnz, iterations, d_selector,
                             d_known, d_gathered, d_out, d_red_ws, s);
+        P->select_kind = KP_SELECT_TABLE;
         if (rc == KP_OK) {
             k_set_switch<<<1, 1, 0, s>>>(P->handle, d_out);
             ++g_launches;
@@ -210,6 +217,8 @@ int kp_seer_plan_launch(kp_seer_plan *plan, void *stream) {
     }
     return KP_OK;
 }
+
+int kp_seer_plan_select_kind(const kp_seer_plan *plan) { return plan ? plan->select_kind : KP_EINVAL; }
 
 int kp_seer_plan_destroy(kp_seer_plan *plan) {
     if (!plan) return KP_EINVAL;

@@ -51,8 +51,10 @@ struct ParamTrees {
 };
 
 int plan_trees_load(const void *d_sel, const void *d_known, const void *d_gath, ParamTrees *T);
+// true iff T (loaded by plan_trees_load) equals the trees compiled in from include/kp_seer_trees.h
+bool emitted_trees_match(const ParamTrees &T);
 int launch_plan_select(const void *d_off, int32_t off_type, int64_t n_rows, int64_t n_cols, int64_t nnz,
-                       int64_t iters, const ParamTrees &T, kp_outcome *d_out, void *d_ws,
+                       int64_t iters, const ParamTrees &T, bool emitted, kp_outcome *d_out, void *d_ws,
                        cudaGraphConditionalHandle h, cudaStream_t s);
 
 // ----------------------------------------------------------------- load helpers

@@ -15,6 +15,9 @@
 // resets the ticket so the workspace is reusable without a memset.  Integer sums are
 // uint64 (wrap exactly like the reference's int64); sum = off[n] - off[0] telescopes.
 #include "kp_internal.cuh"
+#include "../../include/kp_seer_trees.h"
+
+#include <string.h>
 
 namespace kp {
 
@@ -402,15 +405,31 @@ __device__ __forceinline__ int32_t predict_param(const ParamTrees &T, int t, con
     return T.node[t][i].value;
 }
 
-template <typename O, bool kVec>
-__global__ void __launch_bounds__(kRedThreads, kK1MinBlocks<O>) k_seer_plan_select(K1Args a, const __grid_constant__ ParamTrees T,
-                                                                   cudaGraphConditionalHandle h) {
+// Tree evaluators for the plan's selection kernel: the packed trees by value (any bundle)
+// or the bundle's trees compiled in as nested conditionals (include/kp_seer_trees.h,
+// emitted by tools/emit_trees.py) -- used only when the plan's
+// trees equal the compiled ones byte for byte (emitted_trees_match).
+struct ParamPred {
+    const ParamTrees &T;
+    template <int NF>
+    __device__ __forceinline__ int32_t operator()(int t, const double (&x)[NF]) const { return predict_param(T, t, x); }
+};
+struct EmittedPred {
+    template <int NF>
+    __device__ __forceinline__ int32_t operator()(int t, const double (&x)[NF]) const {
+        if constexpr (NF == 4) return t == 0 ? seer_selector(x) : seer_known(x);
+        else return seer_gathered(x);
+    }
+};
+
+template <typename O, bool kVec, typename Pred>
+__device__ __forceinline__ void plan_select_body(const K1Args &a, const Pred &pred, cudaGraphConditionalHandle h) {
     const O *off = reinterpret_cast<const O *>(a.off);
     const double xk[4] = {(double)a.n_rows, (double)a.n_cols, (double)a.nnz, (double)a.iters};
-    if (predict_param(T, 0, xk) == KP_USE_KNOWN) {  // the matrix is never read
+    if (pred(0, xk) == KP_USE_KNOWN) {  // the matrix is never read
         if (blockIdx.x == 0 && threadIdx.x == 0) {
             kp_outcome o = {};
-            o.kernel = predict_param(T, 1, xk);
+            o.kernel = pred(1, xk);
             o.path = KP_USE_KNOWN;
             o.status = KP_OK;
             *a.out = o;
@@ -430,10 +449,37 @@ __global__ void __launch_bounds__(kRedThreads, kK1MinBlocks<O>) k_seer_plan_sele
         o.path = KP_USE_GATHERED;
         const double xg[8] = {(double)a.n_rows, (double)a.n_cols, (double)a.nnz, (double)a.iters,
                               o.max_d, o.min_d, o.mean_d, o.var_d};
-        o.kernel = predict_param(T, 2, xg);
+        o.kernel = pred(2, xg);
         *a.out = o;
         cudaGraphSetConditional(h, (o.kernel >= 0 && o.kernel < KP_NUM_KERNELS) ? (unsigned)o.kernel
                                                                                : (unsigned)KP_NUM_KERNELS);
+    }
+}
+
+template <typename O, bool kVec>
+__global__ void __launch_bounds__(kRedThreads, kK1MinBlocks<O>) k_seer_plan_select(K1Args a, const __grid_constant__ ParamTrees T,
+                                                                   cudaGraphConditionalHandle h) {
+    plan_select_body<O, kVec>(a, ParamPred{T}, h);
+}
+
+template <typename O, bool kVec>
+__global__ void __launch_bounds__(kRedThreads, kK1MinBlocks<O>) k_seer_plan_select_emitted(K1Args a,
+                                                                   cudaGraphConditionalHandle h) {
+    plan_select_body<O, kVec>(a, EmittedPred{}, h);
+}
+
+// batch evaluation of one compiled tree (tests: emitted == interpreted on 1e5 vectors)
+__global__ void k_emitted_predict(int32_t which, const double *__restrict__ x, int64_t n, int32_t *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (which == 2) {
+            double xv[8];
+            for (int f = 0; f < 8; ++f) xv[f] = x[i * 8 + f];
+            out[i] = seer_gathered(xv);
+        } else {
+            double xv[4];
+            for (int f = 0; f < 4; ++f) xv[f] = x[i * 4 + f];
+            out[i] = which == 0 ? seer_selector(xv) : seer_known(xv);
+        }
     }
 }
 
@@ -670,8 +716,22 @@ int plan_trees_load(const void *d_sel, const void *d_known, const void *d_gath, 
     return KP_OK;
 }
 
+bool emitted_trees_match(const ParamTrees &T) {
+    const unsigned char *packed[3] = {kp_seer_packed_selector, kp_seer_packed_known, kp_seer_packed_gathered};
+    const size_t bytes[3] = {sizeof(kp_seer_packed_selector), sizeof(kp_seer_packed_known),
+                             sizeof(kp_seer_packed_gathered)};
+    for (int t = 0; t < 3; ++t) {
+        kp_tree_header h;
+        memcpy(&h, packed[t], sizeof(h));
+        if (h.n_nodes != T.n[t] || bytes[t] != sizeof(h) + (size_t)h.n_nodes * sizeof(kp_tree_node) ||
+            memcmp(packed[t] + sizeof(h), T.node[t], (size_t)h.n_nodes * sizeof(kp_tree_node)) != 0)
+            return false;
+    }
+    return true;
+}
+
 int launch_plan_select(const void *d_off, int32_t off_type, int64_t n_rows, int64_t n_cols, int64_t nnz,
-                       int64_t iters, const ParamTrees &T, kp_outcome *d_out, void *d_ws,
+                       int64_t iters, const ParamTrees &T, bool emitted, kp_outcome *d_out, void *d_ws,
                        cudaGraphConditionalHandle h, cudaStream_t s) {
     K1Args a = {};
     a.off = d_off; a.n_rows = n_rows; a.n_cols = n_cols; a.nnz = nnz; a.iters = iters;
@@ -685,11 +745,17 @@ int launch_plan_select(const void *d_off, int32_t off_type, int64_t n_rows, int6
     const bool aligned = ((uintptr_t)d_off & 15) == 0;
     if (off_type == KP_I32) {
         const int g = known ? 1 : grid_for(n_rows, 64);
-        if (aligned) k_seer_plan_select<int32_t, true><<<g, kRedThreads, 0, s>>>(a, T, h);
+        if (emitted) {
+            if (aligned) k_seer_plan_select_emitted<int32_t, true><<<g, kRedThreads, 0, s>>>(a, h);
+            else k_seer_plan_select_emitted<int32_t, false><<<g, kRedThreads, 0, s>>>(a, h);
+        } else if (aligned) k_seer_plan_select<int32_t, true><<<g, kRedThreads, 0, s>>>(a, T, h);
         else k_seer_plan_select<int32_t, false><<<g, kRedThreads, 0, s>>>(a, T, h);
     } else if (off_type == KP_I64) {
         const int g = known ? 1 : grid_for(n_rows, 32);
-        if (aligned) k_seer_plan_select<int64_t, true><<<g, kRedThreads, 0, s>>>(a, T, h);
+        if (emitted) {
+            if (aligned) k_seer_plan_select_emitted<int64_t, true><<<g, kRedThreads, 0, s>>>(a, h);
+            else k_seer_plan_select_emitted<int64_t, false><<<g, kRedThreads, 0, s>>>(a, h);
+        } else if (aligned) k_seer_plan_select<int64_t, true><<<g, kRedThreads, 0, s>>>(a, T, h);
         else k_seer_plan_select<int64_t, false><<<g, kRedThreads, 0, s>>>(a, T, h);
     } else {
         return KP_EINVAL;
@@ -784,6 +850,19 @@ int kp_seer_select_partials(const int64_t *d_parts, int32_t n_parts, int64_t n_r
     KP_LAUNCHED();
     return KP_OK;
 }
+
+int kp_seer_emitted_predict(int32_t tree, const double *d_x, int64_t n, int32_t *d_out, void *stream) {
+    KP_NVTX("kp_seer_emitted_predict");
+    if (tree < 0 || tree > 2 || n < 0 || (n > 0 && (!d_x || !d_out))) return KP_EINVAL;
+    if (n == 0) return KP_OK;
+    int64_t want = (n + 255) / 256;
+    int g = (int)(want < num_sms() * 8 ? want : num_sms() * 8);
+    k_emitted_predict<<<g, 256, 0, (cudaStream_t)stream>>>(tree, d_x, n, d_out);
+    KP_LAUNCHED();
+    return KP_OK;
+}
+
+const char *kp_seer_emitted_sha256(void) { return KP_SEER_TREES_SHA256; }
 
 uint64_t kp_launch_count(void) { return (uint64_t)kp::g_launches; }
 const char *kp_version(void) { return "kpb200 0.1.0 sm_100a"; }

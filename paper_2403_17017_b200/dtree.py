@@ -217,10 +217,14 @@ class DecisionTree:
     # ------------------------------------------------------------------ source emission
     def emit_source(self, name: str, dialect: str = "cuda") -> str:
         """Nested conditionals equivalent to ``predict``.
-        dialect 'c' or 'cuda' (adds __host__ __device__); thresholds as exact hex floats."""
-        if dialect not in ("c", "cuda"):
-            raise ValueError("dialect must be 'c' or 'cuda'")
-        qual = "static inline __host__ __device__ int" if dialect == "cuda" else "static inline int"
+        dialect 'c', 'cuda' (adds __host__ __device__) or 'hd' (qualified by a KP_SEER_HD
+        macro the including header defines, so one text compiles as C and as CUDA);
+        thresholds as exact hex floats."""
+        quals = {"c": "static inline int", "cuda": "static inline __host__ __device__ int",
+                 "hd": "static inline KP_SEER_HD int"}
+        if dialect not in quals:
+            raise ValueError("dialect must be 'c', 'cuda' or 'hd'")
+        qual = quals[dialect]
         names = self.feature_names or [f"f{i}" for i in range(self.n_features)]
         lines = [f"/* {name}: features {', '.join(names)}; left iff x[f] <= threshold */",
                  f"{qual} {name}(const double *x) {{"]

@@ -107,6 +107,59 @@ class SeerModel:
             raise ValueError("selector demands gathered features but none were supplied")
         return self.gathered_tree.predict(kv + tuple(gathered)), USE_GATHERED
 
+    # ------------------------------------------------------------------ emitted header
+    def emit_header(self, source: str = "") -> str:
+        """SPEC.md:402 ("one source header containing all three emitted functions plus a
+        dispatch function mirroring infer's control flow") over SPEC.md:302-307 emit_source.
+        One text for C hosts and CUDA device code (KP_SEER_HD).  The packed trees it was
+        emitted from ride along, so a runtime can check a model it is handed against the
+        compiled functions byte for byte before trusting them (kp_seer_plan_create does)."""
+        import hashlib
+        packed = [("selector", self.selector_tree), ("known", self.known_tree), ("gathered", self.gathered_tree)]
+        sha = hashlib.sha256(b"".join(t.pack() for _, t in packed)).hexdigest()
+        out = [f"/* kp_seer_trees.h -- GENERATED by tools/emit_trees.py{(' from ' + source) if source else ''};",
+               " * do not edit.  Seer bundle " + SEER_FORMAT + ", kernels: " + ", ".join(
+                   f"{i}={k}" for i, k in enumerate(self.kernels)) + ".",
+               " * seer_selector / seer_known / seer_gathered: DecisionTree.emit_source (SPEC.md:302-307);",
+               " * seer_dispatch: infer's control flow (SPEC.md:376-384).  Left iff x[f] <= threshold. */",
+               "#ifndef KP_SEER_TREES_H", "#define KP_SEER_TREES_H", "",
+               "#ifdef __CUDACC__", "#define KP_SEER_HD __host__ __device__", "#else",
+               "#define KP_SEER_HD", "#endif", "",
+               f'#define KP_SEER_TREES_SHA256 "{sha}"  /* sha256 of the three packed trees below */', ""]
+        for name, t in packed:
+            b = t.pack()
+            out.append(f"/* dtree.pack() of the {name} tree ({len(b)} bytes): kp_tree_header + kp_tree_node[] */")
+            out.append(f"static const unsigned char kp_seer_packed_{name}[{len(b)}] = {{")
+            for i in range(0, len(b), 16):
+                out.append("    " + ", ".join(f"0x{v:02x}" for v in b[i:i + 16]) + ",")
+            out.append("};")
+        out.append("")
+        for name, t in packed:
+            out.append(t.emit_source(f"seer_{name}", "hd"))
+        out += ["/* infer (SPEC.md:376-384): the selector on the known features (rows, cols, nnz,",
+                " * iterations); USE_KNOWN (0) -> the known tree, never reading `gathered`",
+                " * (SPEC.md:388); USE_GATHERED (1) -> the gathered tree on known + (max, min, mean,",
+                " * var) density, or -1 when `gathered` is NULL (the caller must collect features",
+                " * first: seer_needs_gathered tells it so up front). */",
+                "static inline KP_SEER_HD int seer_needs_gathered(double rows, double cols, double nnz, "
+                "double iterations) {",
+                "    const double xk[4] = {rows, cols, nnz, iterations};",
+                "    return seer_selector(xk) != 0;",
+                "}",
+                "static inline KP_SEER_HD int seer_dispatch(double rows, double cols, double nnz, double iterations,",
+                "                                           const double *gathered, int *path) {",
+                "    const double xk[4] = {rows, cols, nnz, iterations};",
+                "    if (seer_selector(xk) == 0) {",
+                "        if (path) *path = 0;",
+                "        return seer_known(xk);",
+                "    }",
+                "    if (path) *path = 1;",
+                "    if (!gathered) return -1;",
+                "    const double xg[8] = {rows, cols, nnz, iterations, gathered[0], gathered[1], gathered[2], gathered[3]};",
+                "    return seer_gathered(xg);",
+                "}", "", "#endif  /* KP_SEER_TREES_H */", ""]
+        return "\n".join(out)
+
 
 # ---------------------------------------------------------------------- inference
 def select_async(model: SeerModel, A, k: int, out=None, stream=None):
@@ -255,6 +308,12 @@ class SeerPlan:
     def outcome(self):
         from .features import decode_outcome
         return decode_outcome(self.out)
+
+    def select_kind(self) -> str:
+        """How each launch selects: 'static' (known path resolved at creation), 'emitted'
+        (the bundle compiled in from include/kp_seer_trees.h), 'param' (packed trees by
+        value) or 'table' (trees in device memory)."""
+        return ("static", "emitted", "param", "table")[self._L.kp_seer_plan_select_kind(self._handle)]
 
     def close(self) -> None:
         if getattr(self, "_handle", None) is not None and self._handle.value:
