@@ -18,6 +18,8 @@
 // Determinism: no floating-point atomics anywhere.  Rows split across work units are
 // finished by k_carry_fixup, which sums the carries of a run of units in a fixed
 // (lane-strided + shuffle-tree) order, so y is bit-identical run to run.
+#include <stdlib.h>
+
 #include "kp_internal.cuh"
 
 namespace kp {
@@ -1437,6 +1439,13 @@ template <typename V, typename O>
 int merge_warps_per_sm() {
     static int warps_per_sm = 0;
     if (!warps_per_sm) {
+        if (const char *cv = getenv("KP_MERGE_CARVE")) {  // experiment: shared-memory carveout (percent)
+            const int pc = atoi(cv);
+            cudaFuncSetAttribute(k_csr_merge<V, O, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+            cudaFuncSetAttribute(k_csr_merge<V, O, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+            cudaFuncSetAttribute(k_csr_merge<V, O, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+            cudaFuncSetAttribute(k_csr_merge<V, O, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+        }
         int nb = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_csr_merge<V, O, true>, kMergeWarps * 32, 0) !=
                 cudaSuccess ||

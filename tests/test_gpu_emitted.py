@@ -48,7 +48,7 @@ def test_bundle_plan_uses_emitted_trees(dtype, index, orc):
     """C1 at k = 10 takes USE_GATHERED under the bundle's selector: the plan's selection
     kernel runs the compiled trees (feature pass -> seer_gathered -> SWITCH)."""
     model = _bundle()
-    for m, k in ((gen.config("C1"), 10), (gen.config("C2", small=True), 30)):
+    for m, k in ((gen.config("C1"), 10), (gen.config("C4", small=True), 10)):
         A = m.to_device_csr(dtype, index=index)
         x = _x(A.n_cols, dtype)
         y = torch.full((A.n_rows,), float("nan"), dtype=dtype, device="cuda")
