@@ -597,9 +597,16 @@ __global__ void k_tree_predict(const void *tree, const double *__restrict__ x, i
 }
 
 // ------------------------------------------------------------------ launch helpers
+// `per_thread` rows per thread keeps the partials few on large inputs; small inputs get up
+// to one CTA per SM at a quarter of that, so every offset load of the pass is in flight in
+// the first trip instead of a chain of dependent trips in one CTA (latency, not bandwidth)
 int grid_for(int64_t n_rows, int per_thread) {
-    int64_t want = (n_rows + (int64_t)kRedThreads * per_thread - 1) / ((int64_t)kRedThreads * per_thread);
-    int cap = num_sms() * 8;  // full occupancy for large inputs (bytes in flight); small inputs use few CTAs
+    const int64_t per_cta = (int64_t)kRedThreads * per_thread, per_cta_lat = per_cta / 4;
+    int64_t want = (n_rows + per_cta - 1) / per_cta;
+    int64_t want_lat = (n_rows + per_cta_lat - 1) / per_cta_lat;
+    if (want_lat > num_sms()) want_lat = num_sms();
+    if (want < want_lat) want = want_lat;
+    int cap = num_sms() * 8;  // full occupancy for large inputs (bytes in flight)
     if (cap > kMaxRedBlocks) cap = kMaxRedBlocks;
     if (want < 1) want = 1;
     return (int)(want < cap ? want : cap);

@@ -703,18 +703,20 @@ __device__ __forceinline__ int64_t merge_search_cta(const O *off, int64_t n_rows
 template <typename V>
 constexpr int kMergeIPT = sizeof(V) == 8 ? KP_MERGE_IPT64 : kIPT;
 // fp64: 3 CTAs (24 warps) per SM in 80 registers instead of 2 at its natural ~110
-// (band-27 fp64 476 -> 402 us, gather-bound inputs unchanged).  fp32 keeps the compiler's
-// allocation (0 = no minimum): 64 registers / 4 CTAs for the plain kernel; the fused-
-// exchange variant lands at ~112 / 2 CTAs, which measured faster on the DRAM-bound C5
-// shards (916 vs 877 GB/s with a forced 4 CTAs).
-template <typename V>
+// (band-27 fp64 476 -> 402 us, gather-bound inputs unchanged).  fp32: 3 CTAs (<= 85
+// registers; the kernel needs 71-80) with the larger L1 that leaves (merge_warps_per_sm):
+// C2 85 us vs 89 us for 4 CTAs at 64 registers, band 27 263 vs 243 us -- the headline's
+// random gathers want L1, regular streams want warps.  The fused-exchange fp32 variant
+// keeps the compiler's allocation (~112 / 2 CTAs: faster on the DRAM-bound C5 shards,
+// 916 vs 877 GB/s with a forced 4 CTAs).
 #ifndef KP_MERGE_MINB_F32
-#define KP_MERGE_MINB_F32 0
+#define KP_MERGE_MINB_F32 3
 #endif
 #ifndef KP_MERGE_MINB_F64
 #define KP_MERGE_MINB_F64 3
 #endif
-constexpr int kMergeMinBlocks = sizeof(V) == 4 ? KP_MERGE_MINB_F32 : KP_MERGE_MINB_F64;
+template <typename V, bool kB = false>
+constexpr int kMergeMinBlocks = sizeof(V) == 4 ? (kB ? 0 : KP_MERGE_MINB_F32) : KP_MERGE_MINB_F64;
 constexpr int kMergeWarps = 8;        // warps per CTA
 
 // Persistent merge-path warps (Merrill & Garland, restructured for B200).  The merge of
@@ -729,51 +731,57 @@ constexpr int kMergeWarps = 8;        // warps per CTA
 // range end goes through k_carry_fixup (~one per warp instead of one per unit).
 // Per unit: striped (coalesced) col/val loads of up to 256 nnz from j0 (speculative past
 // the unit's nnz end; read-once, L1 no-allocate), x gathers, products staged in the
-// warp's padded smem slice and read back blocked (lane l -> positions 8l..8l+7); each
-// row end marks its relative end position (atomicMax of tag<<9 | k+1, the tag = unit
-// counter makes stale marks of earlier units lose, so nothing is cleared), a max-scan
-// gives every position its row, and a thread-local + warp segmented scan sums rows.
+// warp's padded smem slice and read back blocked (lane l -> positions 8l..8l+7).  The
+// probing lane of every row with elements in the unit sets the bit of the row's last
+// position in a 256-bit mask (8 words per warp); each lane's byte of it gives its segment
+// heads, a thread-local + warp segmented scan leaves every position's running row sum,
+// which goes back into the same slice; the probing lanes then read their rows' sums at
+// their last positions and store y coalesced (empty rows: 0).  The shared footprint is
+// one product slice + 32 B per warp (8.7 KB per CTA fp32, 17 KB fp64): the gathers'
+// miss tracking lives in L1, and the carveout the kernel leaves to L1 sets how many
+// gathers an SM keeps in flight (merge_attrs sizes it).
 template <typename V, typename O, bool kPrep, bool kB = false>
-__global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_merge(
+__global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_csr_merge(
     const O *__restrict__ off, const int32_t *__restrict__ col, const V *__restrict__ val, const V *__restrict__ x,
     V *__restrict__ y, int64_t n_rows, int64_t nnz, int64_t n_units, int64_t upw, int64_t n_ranges,
     const int64_t *__restrict__ part, int32_t *__restrict__ crow, V *__restrict__ cval, YDst<V> dst = YDst<V>{}) {
     constexpr int kI = kMergeIPT<V>, kT = 32 * kI;  // items per lane / per unit
     constexpr int kPad = kT + kT / 32;
-    __shared__ V s_prod[kMergeWarps][kPad];
-    __shared__ int32_t s_mark[kMergeWarps][kPad];
-    __shared__ V s_rowv[kMergeWarps][kT + 1];  // value of each row ending in the unit (+ the open one)
+    constexpr unsigned kLaneBits = kI == 32 ? 0xffffffffu : ((1u << kI) - 1u);
+    __shared__ __align__(16) V s_prod[kMergeWarps][kPad];
+    __shared__ unsigned s_last[kMergeWarps][kT / 32];
     // let the PDL-launched carry fix-up be scheduled now: its griddepcontrol.wait still
     // waits for this grid's completion and memory flush, only the launch latency is hidden
     asm volatile("griddepcontrol.launch_dependents;");
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t wid = (int64_t)blockIdx.x * kMergeWarps + w;
     int64_t r0 = 0;
-    // CSR,WO: in-kernel start search, first round shared by the CTA.  Graph A/B against the
+    // CSR,WO: in-kernel start search, first round shared by the CTA (its grid of probes
+    // lives in the product slices, dead until the barrier below).  Graph A/B against the
     // per-warp 32-ary search (per SpMV, same box): C4 fp64 149.5 -> 141.3 us, band 27
     // 282.6 -> 272.4 us, C2 equal, small inputs +0.2..0.7 us per iteration (the CTA
     // barrier); keeping both searches behind a size switch lost the large-input gain
     // (code generation of the main loop), so WO always uses this one.
     if constexpr (!kPrep) {
-        __shared__ int64_t s_q[kMergeWarps * 32];
+        static_assert(sizeof(s_prod) >= kMergeWarps * 32 * sizeof(int64_t), "search grid alias");
+        int64_t *s_q = reinterpret_cast<int64_t *>(&s_prod[0][0]);
         const int64_t w0 = (int64_t)blockIdx.x * kMergeWarps;
         const int64_t wl = w0 + kMergeWarps - 1 < n_ranges - 1 ? w0 + kMergeWarps - 1 : n_ranges - 1;
         const int64_t wc = wid < n_ranges ? wid : wl;
         r0 = merge_search_cta(off, n_rows, nnz, wc * upw * kT, w0 * upw * kT, wl * upw * kT, s_q);
+        __syncthreads();
     }
     if (wid >= n_ranges) return;
     const int64_t total = n_rows + nnz;
     const int64_t u_begin = wid * upw;
     const int64_t u_end = u_begin + upw < n_units ? u_begin + upw : n_units;
     V *prod = s_prod[w];
-    int32_t *mark = s_mark[w];
-    V *rowv = s_rowv[w];
-    for (int t = lane; t < kPad; t += 32) mark[t] = 0;
+    unsigned *last = s_last[w];
+    if (lane < kT / 32) last[lane] = 0u;
     if (kPrep) r0 = part[wid];
     int64_t row_start = ldo(off + r0);  // r0 < n_rows: the range starts before the last item
     V carry = V(0);
     const int jb = lane * kI;
-    int32_t tag = 0;
     // software pipeline: unit u+1's (col, val) loads are issued as soon as unit u's row count
     // fixes where they start, so their HBM latency overlaps unit u's gathers / scans
     auto load_cv = [&](int64_t j0, int32_t (&c)[kI], V (&v)[kI]) {
@@ -794,11 +802,14 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
             }
         }
     };
+    auto store_y = [&](int64_t r, V v) {
+        if constexpr (kB) dst.put(r, v);
+        else y[r] = v;
+    };
     int32_t cn[kI];
     V vn[kI];
     if (u_begin < u_end) load_cv(u_begin * kT - r0, cn, vn);
     for (int64_t u = u_begin; u < u_end; ++u) {
-        tag += 1 << 9;
         const int64_t d0 = u * kT;
         const int64_t d1 = d0 + kT < total ? d0 + kT : total;
         const int64_t j0 = d0 - r0;
@@ -812,18 +823,26 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
         }
         int64_t rr = r0 + lane;
         int64_t re = rr < n_rows ? ldo(off + rr + 1) : INT64_MAX / 2;
-        // row ends inside the unit: q = re + rr < d1 (monotone in rr -> ballot + popc)
+        // rows ending inside the unit: q = re + rr < d1 (monotone in rr -> ballot + popc).
+        // Row k (= r0 + k) spans relative positions [s_k, e_k): e_k = off[r0+k+1] - j0 in
+        // [0, nz], s_k = e_{k-1} (k = 0: its start, clipped to the unit).
         int nr = 0;
         int64_t prev_re = row_start;  // end of the row before the probed one (off[rr])
+        int e_keep = 0, s_keep = 0;   // this lane's round-0 row
         for (int round = 0;; ++round) {
             const bool in = rr < n_rows && re + rr < d1;
             const unsigned m = __ballot_sync(0xffffffffu, in);
             const int cnt = __popc(m);
+            int64_t pe = __shfl_up_sync(0xffffffffu, re, 1);
+            if (lane == 0) pe = prev_re;
             if (in) {
-                const int k = nr + lane;  // row r0 + k; rows with elements here are overwritten by the scan
-                rowv[k] = k == 0 ? carry : V(0);
-                const int rk = (int)(re - j0);  // relative end, < 256
-                atomicMax(&mark[rk + (rk >> 5)], tag | (k + 1));
+                const int e = (int)(re - j0);
+                const int st = pe > j0 ? (int)(pe - j0) : 0;
+                if (e > st) atomicOr(&last[(e - 1) >> 5], 1u << ((e - 1) & 31));  // row's last position
+                if (round == 0) {
+                    e_keep = e;
+                    s_keep = st;
+                }
             }
             if (cnt > 0) prev_re = __shfl_sync(0xffffffffu, re, cnt - 1);
             nr += cnt;
@@ -844,53 +863,30 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
             carry += group_sum<32>(sum);
             continue;
         }
-        if (lane == 0) rowv[nr] = V(0);  // open row: partial stays 0 unless it has elements here
-        // stage products (positions >= nz belong to the next unit: zero)
+        // stage products (positions >= nz belong to the next unit: zero), read back blocked
 #pragma unroll
         for (int t = 0; t < kI; ++t) {
             const int k = lane + t * 32;
             prod[k + (k >> 5)] = k < nz ? p[t] : V(0);
         }
         __syncwarp();
-        // blocked read-back: products and row index of every owned position
-        int ri[kI];
-        {
-            // max-scan of the RAW marks floored at `tag`: current marks (tag | k+1) beat
-            // every stale one (smaller tag), so ri holds tag + row index without decoding
-            int run = tag;
 #pragma unroll
-            for (int t = 0; t < kI; ++t) {
-                const int q = jb + t + ((jb + t) >> 5);
-                p[t] = prod[q];
-                run = max(run, mark[q]);
-                ri[t] = run;
-            }
-            int incl = run;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const int q = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl = max(incl, q);
-            }
-            int excl = __shfl_up_sync(0xffffffffu, incl, 1);
-            if (lane == 0) excl = 0;
-#pragma unroll
-            for (int t = 0; t < kI; ++t) ri[t] = max(ri[t], excl);
-        }
+        for (int t = 0; t < kI; ++t) p[t] = prod[jb + t + ((jb + t) >> 5)];
+        // segment heads: position 0, and every position after a row's last one
+        const unsigned mine = (last[jb >> 5] >> (jb & 31)) & kLaneBits;
+        const unsigned prev_bits = __shfl_up_sync(0xffffffffu, mine, 1);
+        const bool prev_last = lane == 0 || ((prev_bits >> (kI - 1)) & 1u);
+        const unsigned heads_local = ((mine << 1) | (prev_last ? 1u : 0u)) & kLaneBits;
         // thread-local segmented scan
         V acc[kI];
-        int first_head = kI;
-        const int prev_last = __shfl_up_sync(0xffffffffu, ri[kI - 1], 1);
 #pragma unroll
-        for (int t = 0; t < kI; ++t) {
-            const bool head = t == 0 ? (lane == 0 || ri[0] != prev_last) : ri[t] != ri[t - 1];
-            if (head && first_head == kI) first_head = t;
-            acc[t] = (head || t == 0) ? p[t] : acc[t - 1] + p[t];
-        }
+        for (int t = 0; t < kI; ++t) acc[t] = ((heads_local >> t) & 1u || t == 0) ? p[t] : acc[t - 1] + p[t];
+        const int first_head = heads_local ? __ffs(heads_local) - 1 : kI;
         // warp segmented scan of the lanes' last-segment sums; the head flags travel as
         // one ballot mask (lane l combines lane l-o unless a head lies in (l-o, l])
         V inc = acc[kI - 1];
         {
-            const unsigned heads = __ballot_sync(0xffffffffu, first_head < kI);
+            const unsigned heads = __ballot_sync(0xffffffffu, heads_local != 0u);
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const V up = __shfl_up_sync(0xffffffffu, inc, o);
@@ -899,24 +895,32 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V>) k_csr_me
         }
         V cin = __shfl_up_sync(0xffffffffu, inc, 1);
         if (lane == 0) cin = V(0);
-        const int next_first = __shfl_down_sync(0xffffffffu, ri[0], 1);
+        __syncwarp();  // every lane has read its products and mask word
+        // running row sums back into the slice (blocked); the mask is cleared for the next unit
 #pragma unroll
-        for (int t = 0; t < kI; ++t) {
-            const int pos = jb + t;
-            const int rnext = (t + 1 < kI) ? ri[t + 1] : next_first;
-            if (pos < nz && (pos == nz - 1 || rnext != ri[t])) {  // last element of its row in the unit
-                V vt = t < first_head ? acc[t] + cin : acc[t];
-                if (ri[t] == tag) vt += carry;  // row index 0: continued from earlier units
-                rowv[ri[t] - tag] = vt;
+        for (int t = 0; t < kI; ++t) prod[jb + t + ((jb + t) >> 5)] = t < first_head ? acc[t] + cin : acc[t];
+        if (lane < kT / 32) last[lane] = 0u;
+        __syncwarp();
+        // rows r0 .. r0+nr-1: the probing lanes read their sums at the rows' last positions
+        // and store y coalesced; the open row's partial (after the last row end) is the carry
+        for (int base = 0; base < nr; base += 32) {
+            int e = e_keep, st = s_keep;
+            if (base > 0) {  // rows past the first 32 (units of short / empty rows): re-probe (L1)
+                const int64_t rq = r0 + base + lane;
+                const int64_t rq_end = base + lane < nr ? ldo(off + rq + 1) : 0;
+                int64_t pq = __shfl_up_sync(0xffffffffu, rq_end, 1);
+                if (lane == 0) pq = ldo(off + r0 + base);
+                e = (int)(rq_end - j0);
+                st = pq > j0 ? (int)(pq - j0) : 0;
+            }
+            if (base + lane < nr) {
+                V v = e > st ? prod[(e - 1) + ((e - 1) >> 5)] : V(0);
+                if (base + lane == 0) v += carry;
+                store_y(r0 + base + lane, v);
             }
         }
-        __syncwarp();
-        // finished rows r0 .. r0+nr-1: coalesced stores; the open row's partial is the carry
-        for (int k = lane; k < nr; k += 32) {
-            if constexpr (kB) dst.put(r0 + k, rowv[k]);
-            else y[r0 + k] = rowv[k];
-        }
-        carry = rowv[nr];
+        const int e_last = (int)(prev_re - j0);
+        carry = e_last < nz ? prod[(nz - 1) + ((nz - 1) >> 5)] : V(0);
         r0 += nr;
         row_start = prev_re;
         __syncwarp();
@@ -1437,25 +1441,49 @@ struct MergeGeom {
 };
 template <typename V, typename O>
 int merge_warps_per_sm() {
-    static int warps_per_sm = 0;
-    if (!warps_per_sm) {
-        if (const char *cv = getenv("KP_MERGE_CARVE")) {  // experiment: shared-memory carveout (percent)
-            const int pc = atoi(cv);
-            cudaFuncSetAttribute(k_csr_merge<V, O, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
-            cudaFuncSetAttribute(k_csr_merge<V, O, false>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
-            cudaFuncSetAttribute(k_csr_merge<V, O, true, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
-            cudaFuncSetAttribute(k_csr_merge<V, O, false, true>, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
+    // Residency and carveout together: the register budget (launch bounds) fixes how many
+    // CTAs fit; the shared-memory carveout is then the SMALLEST configuration that holds
+    // them, so L1 -- where the x gathers' misses are tracked -- gets the rest (a carveout
+    // left to the driver let the CTAs outnumber what was resident: a second partial wave
+    // of the persistent grid, and a 132-228 KB carve starved the gathers).  Measured on
+    // the v2 kernel, per SpMV (min of 2): C2 fp32 carve 32 KB 85.0 us vs 87.0 driver default
+    // (old kernel 93.2), band 27 263 us (273); C4 fp64 64 KB 140 us, C2 fp64 105 us.
+    // Per device (the attribute is per context); KP_MERGE_CARVE=<percent> overrides (A/B).
+    static int warps_per_sm[64] = {};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) dev = 0;
+    dev &= 63;
+    if (!warps_per_sm[dev]) {
+        void (*fns[4])(const O *, const int32_t *, const V *, const V *, V *, int64_t, int64_t, int64_t, int64_t,
+                       int64_t, const int64_t *, int32_t *, V *, YDst<V>) = {
+            k_csr_merge<V, O, true>, k_csr_merge<V, O, false>, k_csr_merge<V, O, true, true>,
+            k_csr_merge<V, O, false, true>};
+        const char *cv = getenv("KP_MERGE_CARVE");
+        for (auto f : fns) {
+            int nb = 0, pc = cv ? atoi(cv) : -1;
+            cudaFuncAttributes fa = {};
+            if (pc < 0 && cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, f, kMergeWarps * 32, 0) == cudaSuccess &&
+                nb > 0 && cudaFuncGetAttributes(&fa, f) == cudaSuccess) {
+                const size_t need = (size_t)nb * (fa.sharedSizeBytes + 1024);  // + the per-CTA reserve
+                int smem_max = 0;
+                cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+                if (smem_max <= 0) smem_max = 228 * 1024;
+                pc = (int)((need * 100 + smem_max - 1) / smem_max);
+                if (pc > 100) pc = 100;
+            }
+            if (pc >= 0) cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, pc);
         }
+        cudaGetLastError();
         int nb = 0;
         if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, k_csr_merge<V, O, true>, kMergeWarps * 32, 0) !=
                 cudaSuccess ||
             nb <= 0) {
             cudaGetLastError();
-            nb = 4;
+            nb = 3;
         }
-        warps_per_sm = nb * kMergeWarps;
+        warps_per_sm[dev] = nb * kMergeWarps;
     }
-    return warps_per_sm;
+    return warps_per_sm[dev];
 }
 int64_t g_wave_warps = 0;  // kp_debug_set_wave_warps (0 = occupancy-derived)
 // Persistent-kernel wave: every resident warp.  (Halving it when x exceeds L2 helped
