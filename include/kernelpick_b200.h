@@ -170,6 +170,9 @@ KP_API int kp_prepare(int32_t kernel, const kp_csr *A, int64_t ell_cap, void *d_
                kp_prepared *out, void *stream);
 
 /* ------------------------------------------------------------ SpMV */
+/* Scratch of kp_spmv / kp_spmv_bcast for this kernel and matrix (0 = none): carries of the
+ * split-row schedules, the long-row list of CSR,WM / CSR,TM.  Zero it ONCE at allocation
+ * (cudaMemset); the kernels leave it zeroed.  One workspace per stream. */
 KP_API int kp_spmv_workspace_bytes(int32_t kernel, const kp_csr *A, size_t *bytes);
 /* y = A . x with kernel `kernel` (KP_*).  d_x has n_cols entries, d_y n_rows, both of
  * A->val_type.  Deterministic: no floating-point atomics; repeated calls give

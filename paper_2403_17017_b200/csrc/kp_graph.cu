@@ -121,6 +121,9 @@ int kp_seer_plan_create(const kp_csr *A, int64_t iterations, int64_t ell_cap, co
     };
     if (cudaGraphCreate(&P->graph, 0) != cudaSuccess) return fail(KP_ECUDA);
     void *ws = base + L.ws_off;
+    // the SpMV workspace starts zeroed (the row-mapped schedules' long-row list counter;
+    // kernels leave it zeroed again) -- once, here, outside any capture
+    if (L.ws && cudaMemsetAsync(ws, 0, L.ws, s) != cudaSuccess) return fail(KP_ECUDA);
     // 0) Known-feature decisions depend only on the plan's static shape (rows, cols, nnz,
     //    iterations): "known at no additional runtime cost".  Evaluate
     //    the selector (and, on the known path, the known tree) on the device once, now.

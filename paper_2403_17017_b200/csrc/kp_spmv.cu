@@ -19,6 +19,9 @@
 // finished by k_carry_fixup, which sums the carries of a run of units in a fixed
 // (lane-strided + shuffle-tree) order, so y is bit-identical run to run.
 #include <stdlib.h>
+#include <cstddef>
+
+#include <cooperative_groups.h>
 
 #include "kp_internal.cuh"
 
@@ -95,6 +98,28 @@ struct YDst {
     }
 };
 
+// ================================================================= long-row deferral (WM, TM)
+// The row-mapped schedules (CSR,WM: a group of G lanes per row; CSR,TM: a thread per row)
+// walk each row with one lane group, so a row far longer than the schedule's mean becomes
+// a serial chain of dependent batches -- the 10-1000x pitfalls of PAPER.md Table II on
+// power-law inputs (C2: WM 1.36 ms, TM 2.9 ms against 85 us for WO).  Rows longer than the
+// schedule's threshold T are LISTED instead (one atomic per long row, in the SpMV
+// workspace) and finished by k_long_rows, launched with PDL right behind the sweep: a warp
+// per row up to kLongCta elements, a CTA per row beyond, each with a fixed reduction order
+// (y stays bit-identical run to run).  The workspace is zeroed once at allocation; the
+// tail's last CTA re-zeroes the counter.  No row can exceed n_cols elements, so T >= n_cols
+// disables the list and the tail launch altogether.
+struct DeferWs {
+    unsigned int count, n_huge, done, pad;
+    int64_t rows[1];  // [0, huge_at): rows up to kLongCta elements; [huge_at, ...): longer ones
+};
+constexpr int64_t kLongCta = 4096;
+constexpr int kLongThreads = 512;
+__device__ __forceinline__ void defer_row(DeferWs *dw, int64_t row, int64_t len, int64_t huge_at) {
+    if (len > kLongCta) dw->rows[huge_at + atomicAdd(&dw->n_huge, 1u)] = row;
+    else dw->rows[atomicAdd(&dw->count, 1u)] = row;
+}
+
 // ================================================================= CSR,WM (K4)
 // Predicated batch of U strided elements: all U (col, val) loads are issued before the
 // first x gather, so a lane keeps 2U + U requests in flight instead of one chain.
@@ -118,12 +143,17 @@ __device__ __forceinline__ V batch_dot(const int32_t *__restrict__ col, const V 
 template <typename V, typename O, int G>
 __global__ void __launch_bounds__(256) k_csr_wm(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                 const V *__restrict__ val, const V *__restrict__ x,
-                                                V *__restrict__ y, int64_t n_rows) {
+                                                V *__restrict__ y, int64_t n_rows, DeferWs *dw, int64_t long_t,
+                                                int64_t huge_at) {
     constexpr int U = 4;
     const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) / G;
     if (row >= n_rows) return;  // whole groups exit together (G divides 32)
     const int gl = threadIdx.x % G;
     const int64_t s = ldo(off + row), e = ldo(off + row + 1);
+    if (e - s > long_t) {  // listed for k_long_rows (the whole group leaves together)
+        if (gl == 0) defer_row(dw, row, e - s, huge_at);
+        return;
+    }
     V sum = 0;
     for (int64_t j = s + gl; j < e; j += (int64_t)U * G) sum = batch_dot<U, G>(col, val, x, j, e, sum);
     if constexpr (G > 1) {
@@ -212,7 +242,8 @@ struct TmCfg {
 template <typename V, typename O, bool kTma, int kTmU, int kSplit>
 __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                          const V *__restrict__ val, const V *__restrict__ x,
-                                                         V *__restrict__ y, int64_t n_rows, int rpt, int kCap) {
+                                                         V *__restrict__ y, int64_t n_rows, int rpt, int kCap,
+                                                         DeferWs *dw, int64_t long_t, int64_t huge_at) {
     using Cfg = TmCfg<V, O>;
     const size_t stage = Cfg::stage_bytes(kCap);
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -320,13 +351,18 @@ __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__res
             // consecutive rows), so the combine is a shuffle, not a CTA barrier
             constexpr int kG = 32 / kSplit;
             const int rl = warp * kG + (lane % kG), part = lane / kG;
-            const bool act = r0 + rl < n_rows;
+            bool act = r0 + rl < n_rows;
             V sum = V(0);
             if (act) {
                 const int64_t s = (int64_t)so[rl], e = (int64_t)so[rl + 1];
-                const int64_t chunk = (e - s + kSplit - 1) / kSplit;
-                const int64_t a = s + part * chunk, b = a + chunk < e ? a + chunk : e;
-                sum = row_sum(a, b);
+                if (e - s > long_t) {  // listed for k_long_rows
+                    act = false;
+                    if (part == 0) defer_row(dw, r0 + rl, e - s, huge_at);
+                } else {
+                    const int64_t chunk = (e - s + kSplit - 1) / kSplit;
+                    const int64_t a = s + part * chunk, b = a + chunk < e ? a + chunk : e;
+                    sum = row_sum(a, b);
+                }
             }
 #pragma unroll
             for (int o = kG * (kSplit / 2); o >= kG; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);  // fixed order
@@ -336,7 +372,9 @@ __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__res
             for (int q = 0; q < kTmMaxRpt; ++q) {
                 const int rl = tid + q * kTmRows;
                 if (q >= rpt || r0 + rl >= n_rows) break;
-                y[r0 + rl] = row_sum((int64_t)so[rl], (int64_t)so[rl + 1]);
+                const int64_t s = (int64_t)so[rl], e = (int64_t)so[rl + 1];
+                if (e - s > long_t) defer_row(dw, r0 + rl, e - s, huge_at);  // listed for k_long_rows
+                else y[r0 + rl] = row_sum(s, e);
             }
         }
         __syncwarp();
@@ -438,6 +476,74 @@ __global__ void __launch_bounds__(kEllTailThreads) k_ell_tail(const PrepHeader *
         for (int64_t j = s + lane; j < e; j += 4 * 32) sum = batch_dot<4, 32>(col, val, x, j, e, sum);
         sum = group_sum<32>(sum);
         if (lane == 0) y[row] += sum;
+    }
+}
+
+// Finishes the rows CSR,WM / CSR,TM listed (see DeferWs): whole rows, written once.
+// Rows past kLongCta elements take a thread-block CLUSTER of kLongCluster CTAs each (the
+// CTAs stride the row together, 8 x 512 x 4 gathers in flight; rank 0 folds the CTAs'
+// partials through distributed shared memory in rank order -- C4's 1 M-element rows in
+// one pass instead of one CTA walking them); the others a warp each.
+constexpr int kLongCluster = 8;
+template <typename V, typename O>
+__global__ void __launch_bounds__(kLongThreads) k_long_rows(DeferWs *__restrict__ dw, const O *__restrict__ off,
+                                                            const int32_t *__restrict__ col, const V *__restrict__ val,
+                                                            const V *__restrict__ x, V *__restrict__ y,
+                                                            int64_t huge_at) {
+    namespace cg = cooperative_groups;
+    cg::cluster_group cl = cg::this_cluster();
+    __shared__ V sred[32];
+    __shared__ V s_part;
+    __shared__ int64_t s_n, s_h;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x == 0) {
+        s_n = (int64_t)*reinterpret_cast<volatile unsigned int *>(&dw->count);
+        s_h = (int64_t)*reinterpret_cast<volatile unsigned int *>(&dw->n_huge);
+    }
+    __syncthreads();
+    const int64_t n = s_n, nh = s_h;
+    if (n == 0 && nh == 0) return;  // the common case: nothing listed, nothing to reset
+    const volatile int64_t *rows = dw->rows;
+    const unsigned cr = cl.block_rank();
+    const int64_t cid = blockIdx.x / kLongCluster, ncl = gridDim.x / kLongCluster;
+    for (int64_t t = cid; t < nh; t += ncl) {  // identical trip sequence in every CTA of a cluster
+        const int64_t row = rows[huge_at + t];
+        const int64_t s = ldo(off + row), e = ldo(off + row + 1);
+        V sum = 0;
+        constexpr int S = kLongThreads * kLongCluster;
+        for (int64_t j = s + (int64_t)cr * kLongThreads + threadIdx.x; j < e; j += 4 * (int64_t)S)
+            sum = batch_dot<4, S>(col, val, x, j, e, sum);
+        const V tot = block_sum(sum, sred);
+        if (threadIdx.x == 0) s_part = tot;
+        cl.sync();
+        if (cr == 0 && threadIdx.x == 0) {
+            V acc = 0;
+            for (int r = 0; r < kLongCluster; ++r) acc += *cl.map_shared_rank(&s_part, r);
+            y[row] = acc;
+        }
+        cl.sync();  // s_part / sred are reused by the next row
+    }
+    // the others: a warp each (lane-strided batches + shuffle tree)
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5; t < n; t += nw) {
+        const int64_t row = rows[t];
+        const int64_t s = ldo(off + row), e = ldo(off + row + 1);
+        V sum = 0;
+        for (int64_t j = s + lane; j < e; j += 4 * 32) sum = batch_dot<4, 32>(col, val, x, j, e, sum);
+        sum = group_sum<32>(sum);
+        if (lane == 0) y[row] = sum;
+    }
+    // every CTA has read the count: the last one re-zeroes the list for the next launch
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&dw->done, 1u) == gridDim.x - 1) {
+            dw->count = 0;
+            dw->n_huge = 0;
+            dw->done = 0;
+            __threadfence();
+        }
     }
 }
 
@@ -1579,6 +1685,34 @@ Layout prep_layout(int32_t kernel, const kp_csr *A, int64_t cap) {
     return L;
 }
 
+// Long-row threshold of the row-mapped schedules (DeferWs): WM lists rows longer than 64
+// lanes-worth of its group (16 batches of 4 per lane), TM rows longer than max(256, 8 x the
+// known mean); both from the KNOWN shape only.  INT64_MAX (no list, no tail launch) when no
+// row can be that long (n_cols <= T).
+int64_t long_threshold(int32_t kernel, const kp_csr *A) {
+    static const bool off = [] {  // KP_NO_LONG_ROWS=1: A/B switch (the pre-deferral schedules)
+        const char *e = getenv("KP_NO_LONG_ROWS");
+        return e && e[0] == '1';
+    }();
+    if (off) return INT64_MAX;
+    int64_t t = INT64_MAX;
+    if (kernel == KP_CSR_WM) t = 64 * (int64_t)wm_group(A);
+    else if (kernel == KP_CSR_TM) {
+        const int64_t mean = A->n_rows > 0 ? (A->nnz + A->n_rows - 1) / A->n_rows : 0;
+        t = std::max<int64_t>(256, 8 * mean);
+    }
+    return t < A->n_cols ? t : INT64_MAX;
+}
+// list capacity: rows past T (at most nnz / (T + 1)), then the huge rows past kLongCta
+int64_t long_huge_at(int32_t kernel, const kp_csr *A) {
+    const int64_t t = long_threshold(kernel, A);
+    return t == INT64_MAX ? 0 : A->nnz / (t + 1) + 1;
+}
+int64_t long_slots(int32_t kernel, const kp_csr *A) {
+    const int64_t h = long_huge_at(kernel, A);
+    return h ? h + A->nnz / (kLongCta + 1) + 1 : 0;
+}
+
 int64_t spmv_units(int32_t kernel, const kp_csr *A) {
     switch (kernel) {
         case KP_CSR_MP:
@@ -1681,6 +1815,34 @@ int tm_attrs() {
     return KP_OK;
 }
 
+// PDL tail behind a row-mapped sweep (DeferWs); nothing when no row can be long.
+template <typename V, typename O>
+int launch_long_rows(int32_t kernel, const kp_csr *A, DeferWs *dw, const O *off, const int32_t *col, const V *val,
+                     const V *x, V *y, cudaStream_t s) {
+    const int64_t slots = long_slots(kernel, A);
+    if (!slots) return KP_OK;
+    // enough warps for many medium-long rows (power-law: C2 WM 333 -> 165 us with 2 x SMs
+    // instead of 1 x), fewer when at most a handful of rows can be listed
+    int64_t ctas = std::max<int64_t>(1, std::min<int64_t>((int64_t)num_sms() * 2, (long_huge_at(kernel, A) + 7) / 8));
+    ctas = (ctas + kLongCluster - 1) / kLongCluster * kLongCluster;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)ctas);
+    cfg.blockDim = dim3(kLongThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    at[1].id = cudaLaunchAttributeClusterDimension;
+    at[1].val.clusterDim.x = kLongCluster;
+    at[1].val.clusterDim.y = 1;
+    at[1].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 2;
+    KP_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_long_rows<V, O>, dw, off, col, val, x, y, long_huge_at(kernel, A)));
+    KP_LAUNCHED();
+    return KP_OK;
+}
+
 template <typename V, typename O>
 int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V *y, unsigned char *ws,
            cudaStream_t s, const kp_peers *peers = nullptr) {
@@ -1697,15 +1859,17 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
         case KP_CSR_WM: {
             const int G = P && P->group ? P->group : wm_group(A);
             const int64_t g = (R * G + 255) / 256;
+            const int64_t lt = long_threshold(kernel, A), ha = long_huge_at(kernel, A);
+            DeferWs *dw = reinterpret_cast<DeferWs *>(ws);
             switch (G) {
-                case 2: k_csr_wm<V, O, 2><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R); break;
-                case 4: k_csr_wm<V, O, 4><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R); break;
-                case 8: k_csr_wm<V, O, 8><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R); break;
-                case 16: k_csr_wm<V, O, 16><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R); break;
-                default: k_csr_wm<V, O, 32><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R); break;
+                case 2: k_csr_wm<V, O, 2><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha); break;
+                case 4: k_csr_wm<V, O, 4><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha); break;
+                case 8: k_csr_wm<V, O, 8><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha); break;
+                case 16: k_csr_wm<V, O, 16><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha); break;
+                default: k_csr_wm<V, O, 32><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha); break;
             }
             KP_LAUNCHED();
-            return KP_OK;
+            return launch_long_rows<V, O>(kernel, A, dw, off, col, val, x, y, s);
         }
         case KP_CSR_BM: {
             const int64_t g = R < (int64_t)sms * 512 ? R : (int64_t)sms * 512;
@@ -1728,16 +1892,18 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
                 if (rc) return rc;
             }
             constexpr unsigned bw = kTmRows * kTmSplitWide + 32, bn = kTmRows + 32;
+            const int64_t lt = long_threshold(kernel, A), ha = long_huge_at(kernel, A);
+            DeferWs *dw = reinterpret_cast<DeferWs *>(ws);
             if (aligned && wide)
-                k_csr_tm<V, O, true, kTmUWide, kTmSplitWide><<<(unsigned)g, bw, smem, s>>>(off, col, val, x, y, R, 1, cap);
+                k_csr_tm<V, O, true, kTmUWide, kTmSplitWide><<<(unsigned)g, bw, smem, s>>>(off, col, val, x, y, R, 1, cap, dw, lt, ha);
             else if (aligned)
-                k_csr_tm<V, O, true, 4, 1><<<(unsigned)g, bn, smem, s>>>(off, col, val, x, y, R, rpt, cap);
+                k_csr_tm<V, O, true, 4, 1><<<(unsigned)g, bn, smem, s>>>(off, col, val, x, y, R, rpt, cap, dw, lt, ha);
             else if (wide)
-                k_csr_tm<V, O, false, kTmUWide, kTmSplitWide><<<(unsigned)g, bw, smem, s>>>(off, col, val, x, y, R, 1, cap);
+                k_csr_tm<V, O, false, kTmUWide, kTmSplitWide><<<(unsigned)g, bw, smem, s>>>(off, col, val, x, y, R, 1, cap, dw, lt, ha);
             else
-                k_csr_tm<V, O, false, 4, 1><<<(unsigned)g, bn, smem, s>>>(off, col, val, x, y, R, rpt, cap);
+                k_csr_tm<V, O, false, 4, 1><<<(unsigned)g, bn, smem, s>>>(off, col, val, x, y, R, rpt, cap, dw, lt, ha);
             KP_LAUNCHED();
-            return KP_OK;
+            return launch_long_rows<V, O>(kernel, A, dw, off, col, val, x, y, s);
         }
         case KP_ELL_TM: {
             if (!P || !P->buf) return KP_EINVAL;
@@ -1903,8 +2069,9 @@ int kp_prepare(int32_t kernel, const kp_csr *A, int64_t ell_cap, void *d_buf, si
 
 int kp_spmv_workspace_bytes(int32_t kernel, const kp_csr *A, size_t *bytes) {
     if (!valid_csr(A) || !bytes || kernel < 0 || kernel >= KP_NUM_KERNELS) return KP_EINVAL;
-    const int64_t nu = spmv_units(kernel, A);
-    *bytes = nu ? align_up((size_t)nu * sizeof(int32_t) + 16) + align_up((size_t)nu * val_bytes(A)) : 0;
+    const int64_t nu = spmv_units(kernel, A), nl = long_slots(kernel, A);
+    *bytes = nu ? align_up((size_t)nu * sizeof(int32_t) + 16) + align_up((size_t)nu * val_bytes(A))
+                : (nl ? align_up(offsetof(DeferWs, rows) + (size_t)nl * sizeof(int64_t)) : 0);
     return KP_OK;
 }
 

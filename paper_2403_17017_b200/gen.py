@@ -239,6 +239,85 @@ def constant_rows(n_rows: int, length: int, seed: int = 5, device="cpu", n_cols:
     return from_coo(f"const_{n_rows}_l{length}", n_rows, C, rows, cols, seed)
 
 
+# ------------------------------------------------------ structured families (OOD checks)
+# Held out of the frozen bundle's corpus families: finite-element meshes, circuit
+# (modified-nodal-analysis) matrices and road networks -- the structures SuiteSparse adds on
+# top of the synthetic generators (PAPER.md:330 evaluates on all of SuiteSparse).
+def _sym_coo(name, n, rows, cols, seed, meta=None, diag=True) -> Matrix:
+    dev = rows.device
+    r = torch.cat([rows, cols] + ([torch.arange(n, dtype=torch.int64, device=dev)] if diag else []))
+    c = torch.cat([cols, rows] + ([torch.arange(n, dtype=torch.int64, device=dev)] if diag else []))
+    return from_coo(name, n, n, r, c, seed, meta=meta)
+
+
+def fem_mesh(n: int, order: int = 1, tile: int = 64, seed: int = 21, device="cpu") -> Matrix:
+    """2-D triangulated n x n vertex lattice (each square split along one diagonal): P1
+    elements couple a vertex with its 6 lattice neighbours (7-point rows), P2 with every
+    vertex of the adjacent triangles' edge midpoints as well (order 2: lattice distance
+    <= 2 along the triangulation, ~19-point rows).  Vertices are renumbered inside tiles of
+    `tile` consecutive indices (a mesh generator's local ordering): locality stays, exact
+    bands do not.  Boundary rows are shorter."""
+    N = n * n
+    idx = torch.arange(N, dtype=torch.int64, device=device)
+    i, j = torch.div(idx, n, rounding_mode="floor"), idx % n
+    nb = [(0, 1), (1, 0), (1, -1)] if order == 1 else \
+        [(0, 1), (1, 0), (1, -1), (0, 2), (2, 0), (2, -2), (1, 1), (2, -1), (1, -2)]
+    rows, cols = [], []
+    for di, dj in nb:
+        ok = (i + di < n) & (j + dj >= 0) & (j + dj < n)
+        rows.append(idx[ok])
+        cols.append((idx + di * n + dj)[ok])
+    rows, cols = torch.cat(rows), torch.cat(cols)
+    # renumber within tiles: a hashed permutation of each tile's indices
+    key = torch.div(idx, tile, rounding_mode="floor") * (1 << 40) + (hash2(seed, idx) >> 24)
+    perm = torch.empty_like(idx)
+    perm[torch.argsort(key)] = idx
+    return _sym_coo(f"fem_p{order}_{n}", N, perm[rows], perm[cols], seed, {"grid": n, "order": order})
+
+
+def circuit(n: int, n_rails: int = 8, rail_frac: float = 0.1, seed: int = 23, device="cpu") -> Matrix:
+    """Modified-nodal-analysis-like pattern: every node couples to 1-4 nodes of a local
+    window (a netlist's hierarchical locality, window 256), `n_rails` supply / ground nodes
+    couple to a `rail_frac` fraction of all nodes (dense rows AND dense columns), symmetric
+    with a diagonal."""
+    ctr = torch.arange(n, dtype=torch.int64, device=device)
+    deg = 1 + randint(seed, ctr, 4)
+    src = ctr.repeat_interleave(deg)
+    e = torch.arange(src.numel(), dtype=torch.int64, device=device)
+    dst = (src + randint(seed + 1, e, 512) - 256).clamp_(0, n - 1)
+    rails = randint(seed + 2, torch.arange(n_rails, dtype=torch.int64, device=device), n)
+    m = int(n * rail_frac)
+    rr = [src]
+    cc = [dst]
+    for k, r in enumerate(rails.tolist()):
+        tgt = randint(seed + 10 + k, torch.arange(m, dtype=torch.int64, device=device), n)
+        rr.append(torch.full((m,), r, dtype=torch.int64, device=device))
+        cc.append(tgt)
+    return _sym_coo(f"circuit_{n}_r{n_rails}_f{rail_frac}", n, torch.cat(rr), torch.cat(cc), seed,
+                    {"rails": n_rails, "rail_frac": rail_frac})
+
+
+def road(side: int, keep: float = 0.62, shortcut: float = 0.01, seed: int = 25, device="cpu") -> Matrix:
+    """Road-network-like graph Laplacian pattern: a side x side grid with each lattice edge
+    kept with probability `keep` (mean degree ~2.5), a `shortcut` fraction of vertices with
+    one edge to a vertex within +-2 rows (ramps), row-major vertex order (spatial locality,
+    no band structure beyond the grid width).  Symmetric with a diagonal."""
+    N = side * side
+    idx = torch.arange(N, dtype=torch.int64, device=device)
+    i, j = torch.div(idx, side, rounding_mode="floor"), idx % side
+    rows, cols = [], []
+    for k, (di, dj) in enumerate(((0, 1), (1, 0))):
+        ok = (i + di < side) & (j + dj < side) & (uniform01(seed + k, idx) < keep)
+        rows.append(idx[ok])
+        cols.append((idx + di * side + dj)[ok])
+    sc = idx[uniform01(seed + 5, idx) < shortcut]
+    if sc.numel():
+        off = (randint(seed + 6, sc, 4 * side + 1) - 2 * side)
+        rows.append(sc)
+        cols.append((sc + off).clamp_(0, N - 1))
+    return _sym_coo(f"road_{side}_k{keep}", N, torch.cat(rows), torch.cat(cols), seed, {"side": side})
+
+
 # ---------------------------------------------------------------------------- configs
 def config(name: str, device="cpu", small: bool = False) -> Matrix:
     """BASELINE.json configs by short name (C1..C5); small=True gives a reduced

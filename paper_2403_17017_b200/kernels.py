@@ -88,8 +88,10 @@ _ws_cache: dict = {}
 
 
 def spmv_workspace(A: DeviceCSR, kernel: int, stream=None):
-    """Carry scratch of a split-row kernel, one per (device, kernel, stream): launches on
-    different streams may overlap and must not share carries.  Grows to the largest matrix."""
+    """SpMV scratch (carries of the split-row kernels, the long-row list of CSR,WM / CSR,TM),
+    one per (device, kernel, stream): launches on different streams may overlap and must not
+    share it.  Zeroed at allocation (the C-ABI contract: kernels leave it zeroed).  Grows to
+    the largest matrix."""
     torch = _lib.require_cuda()
     nbytes = ctypes.c_size_t(0)
     _lib.check(_lib.load().kp_spmv_workspace_bytes(kernel, ctypes.byref(A.struct), ctypes.byref(nbytes)),
@@ -100,7 +102,7 @@ def spmv_workspace(A: DeviceCSR, kernel: int, stream=None):
     key = (A.device, kernel, _lib.stream_handle(stream, A.device))
     ws = _ws_cache.get(key)
     if ws is None or ws.numel() < n:
-        ws = torch.empty(n, dtype=torch.uint8, device=A.device)
+        ws = torch.zeros(n, dtype=torch.uint8, device=A.device)
         _ws_cache[key] = ws
     return ws
 

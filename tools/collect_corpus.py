@@ -34,7 +34,10 @@ import torch  # noqa: E402
 from paper_2403_17017_b200 import features, gen, kernels  # noqa: E402
 
 
-def corpus(quick: bool, extra: int = 400):
+STRUCTURED = ("fem", "circuit", "road")
+
+
+def corpus(quick: bool, extra: int = 400, extra_structured: int = 60):
     C = []
     for R in (10_000, 100_000, 1_000_000, 4_000_000):
         for per in (2, 8, 32):
@@ -99,6 +102,7 @@ def corpus(quick: bool, extra: int = 400):
         else:
             C.append(("stencil", dict(n=int(lu(8, 170)))))
     C += large_tier()
+    C += structured(extra_structured)
     if quick:
         C = C[::6]
     uniq, seen = [], set()  # random draws can repeat a grid point (e.g. a stencil size)
@@ -108,6 +112,39 @@ def corpus(quick: bool, extra: int = 400):
             seen.add(key)
             uniq.append((fam, p))
     return uniq
+
+
+def structured(extra: int = 60):
+    """FEM meshes, circuits and road networks (gen.py): absent from the round-1 corpus, so
+    the frozen bundle meets them out of distribution.  A grid plus `extra` seeded draws per
+    family (its own RNG: the original families' draws are unchanged)."""
+    import numpy as np
+    C = []
+    for n in (100, 300, 1000, 2000, 2800):
+        for order in (1, 2):
+            C.append(("fem", dict(n=n, order=order, seed=n + order)))
+    for n in (10_000, 100_000, 1_000_000, 4_000_000):
+        for rails in (2, 16):
+            for frac in (0.01, 0.2):
+                C.append(("circuit", dict(n=n, n_rails=rails, rail_frac=frac, seed=n % 97 + rails)))
+    for side in (100, 300, 1000, 3000, 6000):
+        for keep in (0.5, 0.8):
+            C.append(("road", dict(side=side, keep=keep, seed=side + int(keep * 10))))
+    rng = np.random.default_rng(20261017)
+    lu = lambda lo, hi: float(np.exp(rng.uniform(np.log(lo), np.log(hi))))  # noqa: E731
+    for i in range(extra):
+        for fam in STRUCTURED:
+            sd = 5000 + 3 * i + STRUCTURED.index(fam)
+            if fam == "fem":
+                order = int(rng.integers(1, 3))
+                C.append(("fem", dict(n=int(lu(60, 2800 if order == 2 else 4000)), order=order, seed=sd)))
+            elif fam == "circuit":
+                C.append(("circuit", dict(n=int(lu(5e3, 6e6)), n_rails=int(rng.integers(1, 33)),
+                                          rail_frac=round(lu(0.002, 0.3), 4), seed=sd)))
+            else:
+                C.append(("road", dict(side=int(lu(80, 7000)), keep=round(float(rng.uniform(0.45, 0.9)), 3),
+                                       seed=sd)))
+    return C
 
 
 def large_tier():
@@ -139,6 +176,12 @@ def build(fam, p, dev):
         return gen.rmat(p["scale"], p["edge_factor"], seed=p["seed"], device=dev)
     if fam == "skewed":
         return gen.skewed(p["n_rows"], 8.0, p["n_dense"], p["dense_len"], p["seed"], device=dev)
+    if fam == "fem":
+        return gen.fem_mesh(p["n"], p["order"], seed=p["seed"], device=dev)
+    if fam == "circuit":
+        return gen.circuit(p["n"], p["n_rails"], p["rail_frac"], seed=p["seed"], device=dev)
+    if fam == "road":
+        return gen.road(p["side"], p["keep"], seed=p["seed"], device=dev)
     raise ValueError(fam)
 
 
@@ -277,6 +320,9 @@ def main():
                     help="graph: marginal per-iteration cost inside a plan-like graph (default); "
                          "eager: one L2-flushed launch per SpMV")
     ap.add_argument("--only-large", action="store_true", help="only the large tier (append to a corpus)")
+    ap.add_argument("--families", default=None, help="comma list: collect only these families")
+    ap.add_argument("--shard", default="0/1", help="i/n: every n-th matrix from the i-th (split runs)")
+    ap.add_argument("--extra-structured", type=int, default=60)
     ap.add_argument("--model", default=os.path.join(ROOT, "paper_2403_17017_b200", "models", "seer_b200.json"),
                     help="bundle whose gathered tree drives the plan-overhead measurement ('' = bare K1 time)")
     a = ap.parse_args()
@@ -290,7 +336,13 @@ def main():
         from paper_2403_17017_b200 import seer
         model = seer.SeerModel.load(a.model)
     t_start = time.time()
-    for fam, p in (large_tier() if a.only_large else corpus(a.quick, a.extra)):
+    todo = large_tier() if a.only_large else corpus(a.quick, a.extra, a.extra_structured)
+    if a.families:
+        todo = [(f, p) for f, p in todo if f in a.families.split(",")]
+    si, sn = (int(v) for v in a.shard.split("/"))
+    todo = todo[si::sn]
+    print(f"{len(todo)} matrices", flush=True)
+    for fam, p in todo:
         m = build(fam, p, dev)
         name = fam + "_" + "_".join(f"{k}{v}" for k, v in p.items())
         A = m.to_device_csr(torch.float32, device=dev)
