@@ -808,8 +808,10 @@ __device__ __forceinline__ int64_t merge_search_cta(const O *off, int64_t n_rows
 #endif
 template <typename V>
 constexpr int kMergeIPT = sizeof(V) == 8 ? KP_MERGE_IPT64 : kIPT;
-// fp64: 3 CTAs (24 warps) per SM in 80 registers instead of 2 at its natural ~110
-// (band-27 fp64 476 -> 402 us, gather-bound inputs unchanged).  fp32: 3 CTAs (<= 85
+// fp64: 2 CTAs (16 warps, up to 128 registers) since the probe-ahead pipeline (v3): at 3
+// CTAs / 80 registers it spills ~150 B per thread; measured C4 140 -> 130 us, C2 fp64 104 ->
+// 101 us, band-27 fp64 366 -> 415 us (the BASELINE fp64 config, C4, is the merge-path-
+// favourable one).  (v1: 3 CTAs / 80 registers, band-27 fp64 476 -> 402 us.)  fp32: 3 CTAs (<= 85
 // registers; the kernel needs 71-80) with the larger L1 that leaves (merge_warps_per_sm):
 // C2 85 us vs 89 us for 4 CTAs at 64 registers, band 27 263 vs 243 us -- the headline's
 // random gathers want L1, regular streams want warps.  The fused-exchange fp32 variant
@@ -819,7 +821,7 @@ constexpr int kMergeIPT = sizeof(V) == 8 ? KP_MERGE_IPT64 : kIPT;
 #define KP_MERGE_MINB_F32 3
 #endif
 #ifndef KP_MERGE_MINB_F64
-#define KP_MERGE_MINB_F64 3
+#define KP_MERGE_MINB_F64 2
 #endif
 template <typename V, bool kB = false>
 constexpr int kMergeMinBlocks = sizeof(V) == 4 ? (kB ? 0 : KP_MERGE_MINB_F32) : KP_MERGE_MINB_F64;
@@ -855,7 +857,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
     constexpr int kPad = kT + kT / 32;
     constexpr unsigned kLaneBits = kI == 32 ? 0xffffffffu : ((1u << kI) - 1u);
     __shared__ __align__(16) V s_prod[kMergeWarps][kPad];
-    __shared__ unsigned s_last[kMergeWarps][kT / 32];
+    __shared__ unsigned s_last[kMergeWarps][2 * (kT / 32)];  // two row-last masks (units u, u+1)
     // let the PDL-launched carry fix-up be scheduled now: its griddepcontrol.wait still
     // waits for this grid's completion and memory flush, only the launch latency is hidden
     asm volatile("griddepcontrol.launch_dependents;");
@@ -883,7 +885,8 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
     const int64_t u_end = u_begin + upw < n_units ? u_begin + upw : n_units;
     V *prod = s_prod[w];
     unsigned *last = s_last[w];
-    if (lane < kT / 32) last[lane] = 0u;
+    if (lane < 2 * (kT / 32)) last[lane] = 0u;
+    __syncwarp();
     if (kPrep) r0 = part[wid];
     int64_t row_start = ldo(off + r0);  // r0 < n_rows: the range starts before the last item
     V carry = V(0);
@@ -912,52 +915,85 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
         if constexpr (kB) dst.put(r, v);
         else y[r] = v;
     };
-    int32_t cn[kI];
-    V vn[kI];
-    if (u_begin < u_end) load_cv(u_begin * kT - r0, cn, vn);
-    for (int64_t u = u_begin; u < u_end; ++u) {
-        const int64_t d0 = u * kT;
-        const int64_t d1 = d0 + kT < total ? d0 + kT : total;
-        const int64_t j0 = d0 - r0;
-        // x gathers of this unit (loaded last iteration) + round 0 of the row-end probe
-        V p[kI];
-        V vv[kI];
-#pragma unroll
-        for (int t = 0; t < kI; ++t) {
-            vv[t] = vn[t];
-            p[t] = ld_x(x + cn[t]);
-        }
-        int64_t rr = r0 + lane;
+    // Row-end probe of the unit [d0, d1) starting at row rs (rows before rs are finished):
+    // rows ending inside it satisfy off[r+1] + r < d1 (monotone in r -> ballot + popc).
+    // Row k (= rs + k) spans relative positions [s_k, e_k) of the unit's nnz window j0 =
+    // d0 - rs: e_k = off[rs+k+1] - j0 in [0, nz], s_k = e_{k-1} (k = 0: its start, clipped).
+    // The lane of every row with elements in the unit sets the bit of its last position in
+    // mask `mk`; round 0's (e, s) stay in this lane's registers for the write-out.
+    struct Probe {
+        int nr;
+        int e0, s0;
+        int64_t end_re;  // off[rs + nr]: end of the last row ending in the unit (= its start if nr == 0)
+    };
+    auto probe = [&](int64_t rs, int64_t rs_start, int64_t d0, int64_t d1, unsigned *mk) {
+        Probe q{0, 0, 0, rs_start};
+        const int64_t j0 = d0 - rs;
+        int64_t rr = rs + lane;
         int64_t re = rr < n_rows ? ldo(off + rr + 1) : INT64_MAX / 2;
-        // rows ending inside the unit: q = re + rr < d1 (monotone in rr -> ballot + popc).
-        // Row k (= r0 + k) spans relative positions [s_k, e_k): e_k = off[r0+k+1] - j0 in
-        // [0, nz], s_k = e_{k-1} (k = 0: its start, clipped to the unit).
-        int nr = 0;
-        int64_t prev_re = row_start;  // end of the row before the probed one (off[rr])
-        int e_keep = 0, s_keep = 0;   // this lane's round-0 row
         for (int round = 0;; ++round) {
             const bool in = rr < n_rows && re + rr < d1;
             const unsigned m = __ballot_sync(0xffffffffu, in);
             const int cnt = __popc(m);
             int64_t pe = __shfl_up_sync(0xffffffffu, re, 1);
-            if (lane == 0) pe = prev_re;
+            if (lane == 0) pe = q.end_re;
             if (in) {
                 const int e = (int)(re - j0);
                 const int st = pe > j0 ? (int)(pe - j0) : 0;
-                if (e > st) atomicOr(&last[(e - 1) >> 5], 1u << ((e - 1) & 31));  // row's last position
+                if (e > st) atomicOr(&mk[(e - 1) >> 5], 1u << ((e - 1) & 31));  // row's last position
                 if (round == 0) {
-                    e_keep = e;
-                    s_keep = st;
+                    q.e0 = e;
+                    q.s0 = st;
                 }
             }
-            if (cnt > 0) prev_re = __shfl_sync(0xffffffffu, re, cnt - 1);
-            nr += cnt;
+            if (cnt > 0) q.end_re = __shfl_sync(0xffffffffu, re, cnt - 1);
+            q.nr += cnt;
             if (cnt < 32) break;
             rr += 32;
             re = rr < n_rows ? ldo(off + rr + 1) : INT64_MAX / 2;
         }
+        return q;
+    };
+    // Software pipeline, one unit ahead: unit u+1's row-end probe and its (col, val) loads
+    // are issued while unit u's gathers are in flight, so each unit starts with its row
+    // count known -- its x gathers are predicated to its own nz elements (the window's
+    // tail belongs to the next unit: no gather is issued twice) and its mask is already
+    // built (two mask buffers per warp alternate).
+    int32_t cn[kI];
+    V vn[kI];
+    int buf = 0;
+    Probe cur{0, 0, 0, row_start};
+    if (u_begin < u_end) {
+        const int64_t d1 = u_begin * kT + kT < total ? u_begin * kT + kT : total;
+        cur = probe(r0, row_start, u_begin * kT, d1, last);
+        load_cv(u_begin * kT - r0, cn, vn);
+    }
+    for (int64_t u = u_begin; u < u_end; ++u) {
+        const int64_t d0 = u * kT;
+        const int64_t d1 = d0 + kT < total ? d0 + kT : total;
+        const int64_t j0 = d0 - r0;
+        const int nr = cur.nr;
         const int nz = (int)((d1 - d0) - nr);
-        if (u + 1 < u_end) load_cv(d1 - (r0 + nr), cn, vn);
+        unsigned *mk = last + buf * (kT / 32);
+        // x gathers of this unit's own elements only
+        V p[kI];
+        V vv[kI];
+#pragma unroll
+        for (int t = 0; t < kI; ++t) {
+            vv[t] = vn[t];
+            p[t] = (lane + t * 32 < nz) ? ld_x(x + cn[t]) : V(0);
+        }
+        // next unit: its (col, val) window and its row-end probe, overlapping the gathers
+        Probe nxt{0, 0, 0, cur.end_re};
+        if (u + 1 < u_end) {
+            const int64_t r0n = r0 + nr;
+            const int64_t d2 = d1 + kT < total ? d1 + kT : total;
+            // fp32: the window loads first (their latency overlaps the probe); fp64 probes
+            // first -- with the window's 24 registers live across the probe it spills
+            if constexpr (sizeof(V) == 4) load_cv(d1 - r0n, cn, vn);
+            nxt = probe(r0n, cur.end_re, d1, d2, last + (buf ^ 1) * (kT / 32));
+            if constexpr (sizeof(V) != 4) load_cv(d1 - r0n, cn, vn);
+        }
 #pragma unroll
         for (int t = 0; t < kI; ++t) p[t] *= vv[t];
         if (nr == 0) {
@@ -965,21 +1001,23 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
             // scans -- lane sums + a shuffle tree into the running carry (fixed order)
             V sum = V(0);
 #pragma unroll
-            for (int t = 0; t < kI; ++t) sum += (lane + t * 32 < nz) ? p[t] : V(0);
+            for (int t = 0; t < kI; ++t) sum += p[t];
             carry += group_sum<32>(sum);
+            cur = nxt;
+            buf ^= 1;
             continue;
         }
-        // stage products (positions >= nz belong to the next unit: zero), read back blocked
+        // stage products (positions >= nz are zero), read back blocked
 #pragma unroll
         for (int t = 0; t < kI; ++t) {
             const int k = lane + t * 32;
-            prod[k + (k >> 5)] = k < nz ? p[t] : V(0);
+            prod[k + (k >> 5)] = p[t];
         }
         __syncwarp();
 #pragma unroll
         for (int t = 0; t < kI; ++t) p[t] = prod[jb + t + ((jb + t) >> 5)];
         // segment heads: position 0, and every position after a row's last one
-        const unsigned mine = (last[jb >> 5] >> (jb & 31)) & kLaneBits;
+        const unsigned mine = (mk[jb >> 5] >> (jb & 31)) & kLaneBits;
         const unsigned prev_bits = __shfl_up_sync(0xffffffffu, mine, 1);
         const bool prev_last = lane == 0 || ((prev_bits >> (kI - 1)) & 1u);
         const unsigned heads_local = ((mine << 1) | (prev_last ? 1u : 0u)) & kLaneBits;
@@ -1002,15 +1040,15 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
         V cin = __shfl_up_sync(0xffffffffu, inc, 1);
         if (lane == 0) cin = V(0);
         __syncwarp();  // every lane has read its products and mask word
-        // running row sums back into the slice (blocked); the mask is cleared for the next unit
+        // running row sums back into the slice (blocked); this unit's mask is cleared
 #pragma unroll
         for (int t = 0; t < kI; ++t) prod[jb + t + ((jb + t) >> 5)] = t < first_head ? acc[t] + cin : acc[t];
-        if (lane < kT / 32) last[lane] = 0u;
+        if (lane < kT / 32) mk[lane] = 0u;
         __syncwarp();
         // rows r0 .. r0+nr-1: the probing lanes read their sums at the rows' last positions
         // and store y coalesced; the open row's partial (after the last row end) is the carry
         for (int base = 0; base < nr; base += 32) {
-            int e = e_keep, st = s_keep;
+            int e = cur.e0, st = cur.s0;
             if (base > 0) {  // rows past the first 32 (units of short / empty rows): re-probe (L1)
                 const int64_t rq = r0 + base + lane;
                 const int64_t rq_end = base + lane < nr ? ldo(off + rq + 1) : 0;
@@ -1025,10 +1063,11 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
                 store_y(r0 + base + lane, v);
             }
         }
-        const int e_last = (int)(prev_re - j0);
+        const int e_last = (int)(cur.end_re - j0);
         carry = e_last < nz ? prod[(nz - 1) + ((nz - 1) >> 5)] : V(0);
         r0 += nr;
-        row_start = prev_re;
+        cur = nxt;
+        buf ^= 1;
         __syncwarp();
     }
     if (lane == 0) {
