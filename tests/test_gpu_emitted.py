@@ -42,13 +42,26 @@ def test_emitted_rejects_bad_tree():
     assert L.kp_seer_emitted_predict(3, None, 0, None, None) == _lib.KP_EINVAL
 
 
+def _gathered_cases(model):
+    """(matrix, k) pairs the bundle's own selector sends to USE_GATHERED (the smallest k
+    per matrix), so the test follows a retrained bundle."""
+    out = []
+    for m in (gen.config("C1"), gen.config("C4", small=True), gen.stencil27(20)):
+        for k in (1, 3, 10, 30, 100, 1000):
+            if model.selector_tree.predict(seer.known_vector(m.n_rows, m.n_cols, m.nnz, k)) == seer.USE_GATHERED:
+                out.append((m, k))
+                break
+    assert out, "the bundle never takes the gathered path on the test shapes"
+    return out
+
+
 @pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
 @pytest.mark.parametrize("index", ["int32", "int64"])
 def test_bundle_plan_uses_emitted_trees(dtype, index, orc):
-    """C1 at k = 10 takes USE_GATHERED under the bundle's selector: the plan's selection
-    kernel runs the compiled trees (feature pass -> seer_gathered -> SWITCH)."""
+    """Shapes the bundle's selector sends to USE_GATHERED: the plan's selection kernel runs
+    the compiled trees (feature pass -> seer_gathered -> SWITCH)."""
     model = _bundle()
-    for m, k in ((gen.config("C1"), 10), (gen.config("C4", small=True), 10)):
+    for m, k in _gathered_cases(model):
         A = m.to_device_csr(dtype, index=index)
         x = _x(A.n_cols, dtype)
         y = torch.full((A.n_rows,), float("nan"), dtype=dtype, device="cuda")

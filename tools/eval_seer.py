@@ -38,6 +38,7 @@ def main():
     ap.add_argument("--cap-ms", type=float, default=200.0)
     ap.add_argument("--limit", type=int, default=0)
     ap.add_argument("--extra", type=int, default=1200, help="the corpus' --extra (names of its random draws)")
+    ap.add_argument("--extra-structured", type=int, default=150, help="the corpus' --extra-structured")
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
     iters = [int(v) for v in a.iters.split(",")]
@@ -48,7 +49,7 @@ def main():
     _, test = dataset.split_train_test(rows, 2403, 0.8)
     names = {r.name for r in (rows if a.split == "all" else test)}
     specs = []
-    for fam, p in cc.corpus(False, a.extra):
+    for fam, p in cc.corpus(False, a.extra, a.extra_structured):
         nm = fam + "_" + "_".join(f"{k}{v}" for k, v in p.items())
         if nm in names:
             specs.append((nm, fam, p))
