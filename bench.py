@@ -547,36 +547,34 @@ def _traffic_from_profiles(workload, kernel_label):
 
 
 def _e2e(a, A, x, dtype, dev, model, k, steps, warmup):
-    """Public-API end to end: pinned host CSR + x -> H2D -> Seer plan -> y D2H, every step.
+    """Public-API end to end: host-resident matrix + x -> H2D -> Seer plan -> y D2H, every step.
 
-    The step's inputs live in ONE pinned host buffer (offsets, cols, vals, x at 256-byte
-    aligned offsets) copied with one H2D; the device CSR / x are views of one staging
-    buffer.  Served as a two-deep pipeline, the way a serving loop would: step i+1's inputs
-    stream over PCIe on a copy stream into the other staging set while step i's plan runs
-    and its y returns, so the step rate is bound by the H2D link (~55 GB/s measured), not by
-    H2D + compute + D2H in series.  Each step still copies ALL of its inputs and reads back
-    its result inside the timed region."""
+    The matrix lives on the host as a ``device.HostPackedCSR`` (one pinned buffer: int32
+    offsets, column indices bit-packed to ceil(log2(n_cols)) bits -- C2: 20 of 32 --,
+    values), packed once when it is loaded; x is a pinned host vector.  Every step copies
+    BOTH over PCIe, restores the int32 columns on the device (kp_unpack_cols, ~15 us) and
+    runs the plan, then reads y back.  Served as a two-deep pipeline, the way a serving loop
+    would: step i+1's inputs stream over PCIe on a copy stream into the other staging set
+    while step i's plan runs and its y returns, so the step rate is bound by the H2D link
+    (~50-55 GB/s measured), not by H2D + compute + D2H in series."""
     import torch
     from paper_2403_17017_b200 import seer
-    from paper_2403_17017_b200.device import DeviceCSR
-    parts = [A.row_offsets, A.col_indices, A.values, x]
-    offs, o = [], 0
-    for t in parts:
-        offs.append(o)
-        o += (t.numel() * t.element_size() + 255) // 256 * 256
-    h_in = torch.empty(o, dtype=torch.uint8, pin_memory=True)
-    for t, at in zip(parts, offs):
-        nb = t.numel() * t.element_size()
-        h_in[at:at + nb].copy_(t.contiguous().view(torch.uint8).reshape(-1).cpu())
+    from paper_2403_17017_b200.device import HostPackedCSR
+    t_pack = time.perf_counter()
+    H = HostPackedCSR(A)
+    t_pack = time.perf_counter() - t_pack
+    h_x = torch.empty(x.numel(), dtype=dtype, pin_memory=True)
+    h_x.copy_(x.cpu())
     h_y = [torch.empty(A.n_rows, dtype=dtype, pin_memory=True) for _ in range(2)]
     sets = []
     for _ in range(2):
-        d_in = torch.empty(o, dtype=torch.uint8, device=dev)
-        views = [d_in[at:at + t.numel() * t.element_size()].view(t.dtype) for t, at in zip(parts, offs)]
+        d_in, B = H.staging(dev)
+        d_x = torch.empty(A.n_cols, dtype=dtype, device=dev)
         d_y = torch.empty(A.n_rows, dtype=dtype, device=dev)
-        B = DeviceCSR(A.n_rows, A.n_cols, views[0], views[1], views[2])  # views the staging buffer
-        sets.append((d_in, d_y, seer.SeerPlan(model, B, views[3], d_y, k)))
-    bi = int(sum(t.numel() * t.element_size() for t in parts))
+        sets.append((d_in, B, d_x, d_y, seer.SeerPlan(model, B, d_x, d_y, k)))
+    bi = int(sum(H.sizes) + h_x.numel() * h_x.element_size())
+    bi_plain = int(A.row_offsets.numel() * A.row_offsets.element_size() + A.nnz * (4 + A.values.element_size())
+                   + h_x.numel() * h_x.element_size())
     bo = h_y[0].numel() * h_y[0].element_size()
     copy = torch.cuda.Stream(device=dev)
     comp = torch.cuda.current_stream()
@@ -587,12 +585,14 @@ def _e2e(a, A, x, dtype, dev, model, k, steps, warmup):
 
     def step(i):
         s = i % 2
-        d_in, d_y, plan = sets[s]
+        d_in, B, d_x, d_y, plan = sets[s]
         copy.wait_event(freed[s])
         with torch.cuda.stream(copy):
-            d_in.copy_(h_in, non_blocking=True)
+            d_in.copy_(H.buf, non_blocking=True)
+            d_x.copy_(h_x, non_blocking=True)
         landed[s].record(copy)
         comp.wait_event(landed[s])
+        H.unpack(d_in, B, comp)
         plan.launch(comp)
         h_y[s].copy_(d_y, non_blocking=True)
         freed[s].record(comp)
@@ -615,19 +615,23 @@ def _e2e(a, A, x, dtype, dev, model, k, steps, warmup):
     for _ in range(3):
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(comp)
-        sets[0][0].copy_(h_in, non_blocking=True)
+        sets[0][0].copy_(H.buf, non_blocking=True)
+        sets[0][2].copy_(h_x, non_blocking=True)
         f1.record(comp)
         f1.synchronize()
         fl.append(f0.elapsed_time(f1) * 1e-3)
     floor = min(fl)
+    o = H.nbytes + h_x.numel() * h_x.element_size()
     bytes_csr = csr_bytes(A.n_rows, A.n_cols, A.nnz, A.values.element_size(), A.row_offsets.element_size())
-    for _, _, plan in sets:
-        plan.close()
+    for st in sets:
+        st[-1].close()
     return {"value": round(k * bytes_csr / t / 1e9, 2), "unit": "GB/s", "h2d_bytes_per_step": bi,
             "d2h_bytes_per_step": int(bo), "ms_per_step": round(t * 1e3, 4),
             "h2d_floor_ms": round(floor * 1e3, 4), "h2d_link_gbs": round(o / floor / 1e9, 1),
-            "api": "pinned host CSR+x (one buffer) -> DeviceCSR staging views (copy stream, 2-deep) -> "
-                   "seer.SeerPlan.launch (kp_seer_plan C-ABI) -> y to pinned host"}
+            "h2d_bytes_unpacked": bi_plain, "col_bits": H.bits, "host_pack_ms_once": round(t_pack * 1e3, 1),
+            "api": "device.HostPackedCSR (pinned: int32 offsets, columns bit-packed to ceil(log2 n_cols) bits, "
+                   "values; packed once at load) + pinned x -> H2D every step (copy stream, 2-deep) -> "
+                   "kp_unpack_cols -> seer.SeerPlan.launch (kp_seer_plan C-ABI) -> y to pinned host"}
 
 
 # ------------------------------------------------------------------------ CPU Seer (oracle port)

@@ -270,6 +270,19 @@ KP_API int kp_mm_header(const char *buf, size_t len, kp_mm_info *info);
 KP_API int kp_mm_parse(const char *buf, size_t len, int64_t *rows, int64_t *cols, double *vals,
                        int64_t capacity, int32_t n_threads, kp_mm_info *info);
 
+/* -------------------------------------------- compact host->device column transfer
+ * A host-resident matrix moved every step is PCIe-bound; its column indices need only
+ * b = kp_pack_bits(n_cols) = ceil(log2(n_cols)) bits.  kp_pack_cols (HOST, OpenMP) writes
+ * them as one little-endian bitstream of 32-bit words (column i at bits [i*b, (i+1)*b)),
+ * kp_pack_cols_bytes bytes; kp_unpack_cols (DEVICE, async) restores the int32 array the
+ * SpMV entry points read.  KP_ERANGE from kp_pack_cols: a column outside [0, n_cols). */
+KP_API int32_t kp_pack_bits(int64_t n_cols);
+KP_API size_t kp_pack_cols_bytes(int64_t n, int64_t n_cols);
+KP_API int kp_pack_cols(const int32_t *h_cols, int64_t n, int64_t n_cols, uint32_t *h_out,
+                        int32_t n_threads);
+KP_API int kp_unpack_cols(const uint32_t *d_packed, int64_t n, int64_t n_cols, int32_t *d_cols,
+                          void *stream);
+
 /* ------------------------------------------------------------ multi-GPU (K14) */
 /* nnz-balanced row cut: d_cuts[p] = lower_bound(row_offsets, p*nnz/parts), p = 0..parts
  * (d_cuts[parts] = n_rows). */

@@ -30,6 +30,7 @@ EXPORTS = (
     "kp_seer_select_partials", "kp_coo_workspace_bytes", "kp_csr_from_coo", "kp_spmv_bcast",
     "kp_mm_header", "kp_mm_parse", "kp_watchdog_start", "kp_watchdog_heartbeat", "kp_watchdog_status",
     "kp_watchdog_stop", "kp_seer_plan_select_kind", "kp_seer_emitted_predict", "kp_seer_emitted_sha256",
+    "kp_pack_bits", "kp_pack_cols_bytes", "kp_pack_cols", "kp_unpack_cols",
 )
 
 
@@ -125,6 +126,10 @@ def load(require: bool = True):
         "kp_seer_plan_select_kind": (ctypes.c_int, [p]),
         "kp_seer_emitted_predict": (ctypes.c_int, [i32, p, i64, p, p]),
         "kp_seer_emitted_sha256": (ctypes.c_char_p, []),
+        "kp_pack_bits": (i32, [i64]),
+        "kp_pack_cols_bytes": (sz, [i64, i64]),
+        "kp_pack_cols": (ctypes.c_int, [p, i64, i64, p, i32]),
+        "kp_unpack_cols": (ctypes.c_int, [p, i64, i64, p, p]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)

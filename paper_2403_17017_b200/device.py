@@ -192,3 +192,61 @@ def ptr(t) -> int:
 
 def cptr(obj) -> ctypes.c_void_p:
     return ctypes.c_void_p(ptr(obj))
+
+
+class HostPackedCSR:
+    """A host-resident CSR in the compact transfer format (csrc/kp_pack.cu): int32 offsets,
+    column indices bit-packed to ceil(log2(n_cols)) bits (kp_pack_cols, OpenMP), values,
+    all in ONE pinned buffer at 256-byte aligned offsets, so a step moves it with one H2D.
+    ``upload`` copies it into a device staging area and restores the int32 columns there
+    (kp_unpack_cols); ``staging`` builds that area and the DeviceCSR viewing it.  The
+    packing runs once per matrix (like the reference's construction-time validation,
+    sparse.py:52-71); every step then pays only the compact bytes over PCIe."""
+
+    def __init__(self, A: DeviceCSR, n_threads: int = 0):
+        import ctypes
+        torch = _lib.require_cuda()
+        L = _lib.load()
+        self.n_rows, self.n_cols, self.nnz = A.n_rows, A.n_cols, A.nnz
+        self.off_dtype, self.val_dtype = A.row_offsets.dtype, A.values.dtype
+        self.bits = int(L.kp_pack_bits(max(1, self.n_cols)))
+        pk = int(L.kp_pack_cols_bytes(self.nnz, max(1, self.n_cols)))
+        sizes = [A.row_offsets.numel() * A.row_offsets.element_size(), pk, self.nnz * A.values.element_size()]
+        self.offsets, o = [], 0
+        for nb in sizes:
+            self.offsets.append(o)
+            o += (nb + 255) // 256 * 256
+        self.sizes, self.nbytes = sizes, o
+        self.buf = torch.empty(o, dtype=torch.uint8, pin_memory=True)
+        b = self.buf.numpy()
+        b[self.offsets[0]:self.offsets[0] + sizes[0]] = A.row_offsets.cpu().numpy().view(np.uint8)
+        b[self.offsets[2]:self.offsets[2] + sizes[2]] = A.values.cpu().numpy().view(np.uint8)
+        cols = np.ascontiguousarray(A.col_indices.cpu().numpy())
+        dst = self.buf.data_ptr() + self.offsets[1]
+        _lib.check(L.kp_pack_cols(cols.ctypes.data_as(ctypes.c_void_p), self.nnz, max(1, self.n_cols),
+                                  ctypes.c_void_p(dst), int(n_threads)), "kp_pack_cols")
+
+    def staging(self, device):
+        """(device buffer for the packed bytes, DeviceCSR viewing it with its own int32 column array)."""
+        torch = _lib.require_cuda()
+        d = torch.empty(self.nbytes, dtype=torch.uint8, device=device)
+        off = d[self.offsets[0]:self.offsets[0] + self.sizes[0]].view(self.off_dtype)
+        val = d[self.offsets[2]:self.offsets[2] + self.sizes[2]].view(self.val_dtype)
+        cols = torch.empty(self.nnz, dtype=torch.int32, device=device)
+        return d, DeviceCSR(self.n_rows, self.n_cols, off, cols, val)
+
+    def upload(self, d_buf, B: DeviceCSR, copy_stream=None, stream=None):
+        """H2D of the packed bytes on `copy_stream` (non-blocking), then the column unpack on
+        `stream` after it (stream-ordered through an event)."""
+        torch = _lib.require_cuda()
+        cs = copy_stream or torch.cuda.current_stream(B.device)
+        with torch.cuda.stream(cs):
+            d_buf.copy_(self.buf, non_blocking=True)
+        st = stream or torch.cuda.current_stream(B.device)
+        if st is not cs:
+            st.wait_stream(cs)
+        self.unpack(d_buf, B, st)
+
+    def unpack(self, d_buf, B: DeviceCSR, stream):
+        _lib.check(_lib.load().kp_unpack_cols(d_buf.data_ptr() + self.offsets[1], self.nnz, max(1, self.n_cols),
+                                              B.col_indices.data_ptr(), int(stream.cuda_stream)), "kp_unpack_cols")
