@@ -808,10 +808,9 @@ __device__ __forceinline__ int64_t merge_search_cta(const O *off, int64_t n_rows
 #endif
 template <typename V>
 constexpr int kMergeIPT = sizeof(V) == 8 ? KP_MERGE_IPT64 : kIPT;
-// fp64: 2 CTAs (16 warps, up to 128 registers) since the probe-ahead pipeline (v3): at 3
-// CTAs / 80 registers it spills ~150 B per thread; measured C4 140 -> 130 us, C2 fp64 104 ->
-// 101 us, band-27 fp64 366 -> 415 us (the BASELINE fp64 config, C4, is the merge-path-
-// favourable one).  (v1: 3 CTAs / 80 registers, band-27 fp64 476 -> 402 us.)  fp32: 3 CTAs (<= 85
+// fp64: 3 CTAs (24 warps) in 80 registers -- with the values loaded late (kLateVals) the
+// probe-ahead pipeline fits without spilling (with them pipelined it spilled ~150 B per
+// thread at 80 registers and ran best at 2 CTAs).  fp32: 3 CTAs (<= 85
 // registers; the kernel needs 71-80) with the larger L1 that leaves (merge_warps_per_sm):
 // C2 85 us vs 89 us for 4 CTAs at 64 registers, band 27 263 vs 243 us -- the headline's
 // random gathers want L1, regular streams want warps.  The fused-exchange fp32 variant
@@ -821,7 +820,17 @@ constexpr int kMergeIPT = sizeof(V) == 8 ? KP_MERGE_IPT64 : kIPT;
 #define KP_MERGE_MINB_F32 3
 #endif
 #ifndef KP_MERGE_MINB_F64
-#define KP_MERGE_MINB_F64 2
+#define KP_MERGE_MINB_F64 3
+#endif
+// late values (see k_csr_merge): measured against values pipelined one unit ahead, per
+// SpMV (min of 2, profiles/ab_merge_late_r02.txt): C2 WO 82.9 -> 80.9 us, C3 265 -> 253,
+// band 27 259 -> 245, power-law 302 -> 288, C4 fp64 (3 CTAs instead of 2) 132 -> 128,
+// band 27 fp64 415 -> 355, C5 equal
+#ifndef KP_MERGE_LATE_F32
+#define KP_MERGE_LATE_F32 1
+#endif
+#ifndef KP_MERGE_LATE_F64
+#define KP_MERGE_LATE_F64 1
 #endif
 template <typename V, bool kB = false>
 constexpr int kMergeMinBlocks = sizeof(V) == 4 ? (kB ? 0 : KP_MERGE_MINB_F32) : KP_MERGE_MINB_F64;
@@ -893,6 +902,10 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
     const int jb = lane * kI;
     // software pipeline: unit u+1's (col, val) loads are issued as soon as unit u's row count
     // fixes where they start, so their HBM latency overlaps unit u's gathers / scans
+    // kLateVals: the window load pipelines only the columns (they address the gathers);
+    // each unit loads its own values next to its gathers -- the values' registers are not
+    // live across the previous unit (fp64: 16 registers)
+    constexpr bool kLateVals = sizeof(V) == 8 ? KP_MERGE_LATE_F64 : KP_MERGE_LATE_F32;
     auto load_cv = [&](int64_t j0, int32_t (&c)[kI], V (&v)[kI]) {
         if (j0 + kT <= nnz) {  // common case: unpredicated, immediate offsets
             const int32_t *cp = col + j0 + lane;
@@ -900,14 +913,14 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
 #pragma unroll
             for (int t = 0; t < kI; ++t) {
                 c[t] = ld_stream(cp + t * 32);
-                v[t] = ld_stream(vp + t * 32);
+                if constexpr (!kLateVals) v[t] = ld_stream(vp + t * 32);
             }
         } else {
 #pragma unroll
             for (int t = 0; t < kI; ++t) {
                 const int64_t j = j0 + lane + t * 32;
                 c[t] = j < nnz ? ld_stream(col + j) : 0;
-                v[t] = j < nnz ? ld_stream(val + j) : V(0);
+                if constexpr (!kLateVals) v[t] = j < nnz ? ld_stream(val + j) : V(0);
             }
         }
     };
@@ -980,8 +993,10 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
         V vv[kI];
 #pragma unroll
         for (int t = 0; t < kI; ++t) {
-            vv[t] = vn[t];
-            p[t] = (lane + t * 32 < nz) ? ld_x(x + cn[t]) : V(0);
+            const bool own = lane + t * 32 < nz;
+            if constexpr (kLateVals) vv[t] = own ? ld_stream(val + j0 + lane + t * 32) : V(0);
+            else vv[t] = vn[t];
+            p[t] = own ? ld_x(x + cn[t]) : V(0);
         }
         // next unit: its (col, val) window and its row-end probe, overlapping the gathers
         Probe nxt{0, 0, 0, cur.end_re};
