@@ -110,14 +110,29 @@ struct YDst {
 // tail's last CTA re-zeroes the counter.  No row can exceed n_cols elements, so T >= n_cols
 // disables the list and the tail launch altogether.
 struct DeferWs {
-    unsigned int count, n_huge, done, pad;
-    int64_t rows[1];  // [0, huge_at): rows up to kLongCta elements; [huge_at, ...): longer ones
+    unsigned int count, n_huge, n_giant, done;
+    // [0, huge_at): rows up to kLongCta elements (a warp each); [huge_at, giant_at): up to
+    // kLongCluster (a CTA each); [giant_at, ...): longer (a thread-block cluster each)
+    int64_t rows[1];
 };
 constexpr int64_t kLongCta = 4096;
+constexpr int64_t kLongGiant = 65536;
 constexpr int kLongThreads = 512;
-__device__ __forceinline__ void defer_row(DeferWs *dw, int64_t row, int64_t len, int64_t huge_at) {
-    if (len > kLongCta) dw->rows[huge_at + atomicAdd(&dw->n_huge, 1u)] = row;
-    else dw->rows[atomicAdd(&dw->count, 1u)] = row;
+// One atomic per list per warp (the lanes that list a row of the same tier coalesce): a
+// matrix whose rows are ALL long (a 300-wide band under CSR,TM) lists every row, and
+// per-lane atomics on one counter serialised at the L2 (band 300: TM 107 us).
+__device__ __forceinline__ void defer_append(unsigned int *cnt, int64_t *rows, int64_t row) {
+    namespace cg = cooperative_groups;
+    cg::coalesced_group g = cg::coalesced_threads();
+    unsigned base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(cnt, (unsigned)g.size());
+    base = g.shfl(base, 0);
+    rows[base + g.thread_rank()] = row;
+}
+__device__ __forceinline__ void defer_row(DeferWs *dw, int64_t row, int64_t len, int64_t huge_at, int64_t giant_at) {
+    if (len > kLongGiant) defer_append(&dw->n_giant, dw->rows + giant_at, row);
+    else if (len > kLongCta) defer_append(&dw->n_huge, dw->rows + huge_at, row);
+    else defer_append(&dw->count, dw->rows, row);
 }
 
 // ================================================================= CSR,WM (K4)
@@ -144,14 +159,14 @@ template <typename V, typename O, int G>
 __global__ void __launch_bounds__(256) k_csr_wm(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                 const V *__restrict__ val, const V *__restrict__ x,
                                                 V *__restrict__ y, int64_t n_rows, DeferWs *dw, int64_t long_t,
-                                                int64_t huge_at) {
+                                                int64_t huge_at, int64_t giant_at) {
     constexpr int U = 4;
     const int64_t row = ((int64_t)blockIdx.x * 256 + threadIdx.x) / G;
     if (row >= n_rows) return;  // whole groups exit together (G divides 32)
     const int gl = threadIdx.x % G;
     const int64_t s = ldo(off + row), e = ldo(off + row + 1);
     if (e - s > long_t) {  // listed for k_long_rows (the whole group leaves together)
-        if (gl == 0) defer_row(dw, row, e - s, huge_at);
+        if (gl == 0) defer_row(dw, row, e - s, huge_at, giant_at);
         return;
     }
     V sum = 0;
@@ -179,18 +194,52 @@ __device__ __forceinline__ V block_sum(V v, V *sred) {
     return t;  // valid in thread 0
 }
 
+// Block-mapped: a CTA per row, so long rows get 128 x 4 gathers in flight and one block
+// reduction.  A CTA spent on a row of a handful of elements is the schedule's pitfall
+// (round-1 corpus: 5-70x behind the best kernel on short-row matrices, C2 443 us, road
+// networks 69x), so rows are taken four at a time: each of the CTA's 4 warps sums one row
+// of up to kBmShort elements (lane-strided batches + shuffle tree), and the group's longer
+// rows then get the whole CTA, one after another (block_sum, as before).  Fixed reduction
+// orders either way: y is bit-identical run to run.
+constexpr int64_t kBmShort = 256;
 template <typename V, typename O>
 __global__ void __launch_bounds__(128) k_csr_bm(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                 const V *__restrict__ val, const V *__restrict__ x,
                                                 V *__restrict__ y, int64_t n_rows) {
     __shared__ V sred[32];
-    for (int64_t row = blockIdx.x; row < n_rows; row += gridDim.x) {
-        const int64_t s = ldo(off + row), e = ldo(off + row + 1);
-        V sum = 0;
-        for (int64_t j = s + threadIdx.x; j < e; j += 4 * 128) sum = batch_dot<4, 128>(col, val, x, j, e, sum);
-        V t = block_sum(sum, sred);
-        if (threadIdx.x == 0) y[row] = t;
+    __shared__ int64_t s_s[4], s_e[4];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t r0 = (int64_t)blockIdx.x * 4; r0 < n_rows; r0 += (int64_t)gridDim.x * 4) {
+        const int64_t row = r0 + w;
+        int64_t s = 0, e = 0;
+        if (row < n_rows) {
+            s = ldo(off + row);
+            e = ldo(off + row + 1);
+        }
+        if (e - s <= kBmShort) {  // short (or past the end): this warp
+            if (row < n_rows) {
+                V sum = 0;
+                for (int64_t j = s + lane; j < e; j += 4 * 32) sum = batch_dot<4, 32>(col, val, x, j, e, sum);
+                sum = group_sum<32>(sum);
+                if (lane == 0) y[row] = sum;
+            }
+            s = e = 0;  // nothing left for the CTA
+        }
+        if (lane == 0) {
+            s_s[w] = s;
+            s_e[w] = e;
+        }
         __syncthreads();
+        for (int q = 0; q < 4; ++q) {  // the group's long rows: the whole CTA each
+            const int64_t qs = s_s[q], qe = s_e[q];
+            if (qe - qs <= kBmShort) continue;  // uniform over the CTA
+            V sum = 0;
+            for (int64_t j = qs + threadIdx.x; j < qe; j += 4 * 128) sum = batch_dot<4, 128>(col, val, x, j, qe, sum);
+            const V t = block_sum(sum, sred);
+            if (threadIdx.x == 0) y[r0 + q] = t;
+            __syncthreads();  // sred reuse
+        }
+        __syncthreads();  // s_s / s_e reuse
     }
 }
 
@@ -243,7 +292,8 @@ template <typename V, typename O, bool kTma, int kTmU, int kSplit>
 __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                          const V *__restrict__ val, const V *__restrict__ x,
                                                          V *__restrict__ y, int64_t n_rows, int rpt, int kCap,
-                                                         DeferWs *dw, int64_t long_t, int64_t huge_at) {
+                                                         DeferWs *dw, int64_t long_t, int64_t huge_at,
+                                                         int64_t giant_at) {
     using Cfg = TmCfg<V, O>;
     const size_t stage = Cfg::stage_bytes(kCap);
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -357,7 +407,7 @@ __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__res
                 const int64_t s = (int64_t)so[rl], e = (int64_t)so[rl + 1];
                 if (e - s > long_t) {  // listed for k_long_rows
                     act = false;
-                    if (part == 0) defer_row(dw, r0 + rl, e - s, huge_at);
+                    if (part == 0) defer_row(dw, r0 + rl, e - s, huge_at, giant_at);
                 } else {
                     const int64_t chunk = (e - s + kSplit - 1) / kSplit;
                     const int64_t a = s + part * chunk, b = a + chunk < e ? a + chunk : e;
@@ -373,7 +423,7 @@ __global__ void __launch_bounds__(kTmRows * kSplit + 32) k_csr_tm(const O *__res
                 const int rl = tid + q * kTmRows;
                 if (q >= rpt || r0 + rl >= n_rows) break;
                 const int64_t s = (int64_t)so[rl], e = (int64_t)so[rl + 1];
-                if (e - s > long_t) defer_row(dw, r0 + rl, e - s, huge_at);  // listed for k_long_rows
+                if (e - s > long_t) defer_row(dw, r0 + rl, e - s, huge_at, giant_at);  // listed for k_long_rows
                 else y[r0 + rl] = row_sum(s, e);
             }
         }
@@ -480,34 +530,36 @@ __global__ void __launch_bounds__(kEllTailThreads) k_ell_tail(const PrepHeader *
 }
 
 // Finishes the rows CSR,WM / CSR,TM listed (see DeferWs): whole rows, written once.
-// Rows past kLongCta elements take a thread-block CLUSTER of kLongCluster CTAs each (the
+// Rows past kLongGiant elements take a thread-block CLUSTER of kLongCluster CTAs each (the
 // CTAs stride the row together, 8 x 512 x 4 gathers in flight; rank 0 folds the CTAs'
-// partials through distributed shared memory in rank order -- C4's 1 M-element rows in
-// one pass instead of one CTA walking them); the others a warp each.
+// partials through distributed shared memory in rank order -- C4's 1 M-element rows in one
+// pass instead of one CTA walking them); rows past kLongCta a CTA each; the rest a warp each.
 constexpr int kLongCluster = 8;
 template <typename V, typename O>
 __global__ void __launch_bounds__(kLongThreads) k_long_rows(DeferWs *__restrict__ dw, const O *__restrict__ off,
                                                             const int32_t *__restrict__ col, const V *__restrict__ val,
                                                             const V *__restrict__ x, V *__restrict__ y,
-                                                            int64_t huge_at) {
+                                                            int64_t huge_at, int64_t giant_at) {
     namespace cg = cooperative_groups;
     cg::cluster_group cl = cg::this_cluster();
     __shared__ V sred[32];
     __shared__ V s_part;
-    __shared__ int64_t s_n, s_h;
+    __shared__ int64_t s_n[3];
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if (threadIdx.x == 0) {
-        s_n = (int64_t)*reinterpret_cast<volatile unsigned int *>(&dw->count);
-        s_h = (int64_t)*reinterpret_cast<volatile unsigned int *>(&dw->n_huge);
+        s_n[0] = (int64_t)*reinterpret_cast<volatile unsigned int *>(&dw->count);
+        s_n[1] = (int64_t)*reinterpret_cast<volatile unsigned int *>(&dw->n_huge);
+        s_n[2] = (int64_t)*reinterpret_cast<volatile unsigned int *>(&dw->n_giant);
     }
     __syncthreads();
-    const int64_t n = s_n, nh = s_h;
-    if (n == 0 && nh == 0) return;  // the common case: nothing listed, nothing to reset
+    const int64_t n = s_n[0], nh = s_n[1], ng = s_n[2];
+    if (n == 0 && nh == 0 && ng == 0) return;  // the common case: nothing listed, nothing to reset
     const volatile int64_t *rows = dw->rows;
+    // giant rows: a cluster each (identical trip sequence in every CTA of a cluster)
     const unsigned cr = cl.block_rank();
     const int64_t cid = blockIdx.x / kLongCluster, ncl = gridDim.x / kLongCluster;
-    for (int64_t t = cid; t < nh; t += ncl) {  // identical trip sequence in every CTA of a cluster
-        const int64_t row = rows[huge_at + t];
+    for (int64_t t = cid; t < ng; t += ncl) {
+        const int64_t row = rows[giant_at + t];
         const int64_t s = ldo(off + row), e = ldo(off + row + 1);
         V sum = 0;
         constexpr int S = kLongThreads * kLongCluster;
@@ -523,6 +575,16 @@ __global__ void __launch_bounds__(kLongThreads) k_long_rows(DeferWs *__restrict_
         }
         cl.sync();  // s_part / sred are reused by the next row
     }
+    // large rows: a CTA each
+    for (int64_t t = blockIdx.x; t < nh; t += gridDim.x) {
+        const int64_t row = rows[huge_at + t];
+        const int64_t s = ldo(off + row), e = ldo(off + row + 1);
+        V sum = 0;
+        for (int64_t j = s + threadIdx.x; j < e; j += 4 * kLongThreads) sum = batch_dot<4, kLongThreads>(col, val, x, j, e, sum);
+        const V tot = block_sum(sum, sred);
+        if (threadIdx.x == 0) y[row] = tot;
+        __syncthreads();  // sred reuse
+    }
     // the others: a warp each (lane-strided batches + shuffle tree)
     const int lane = threadIdx.x & 31;
     const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -534,13 +596,14 @@ __global__ void __launch_bounds__(kLongThreads) k_long_rows(DeferWs *__restrict_
         sum = group_sum<32>(sum);
         if (lane == 0) y[row] = sum;
     }
-    // every CTA has read the count: the last one re-zeroes the list for the next launch
+    // every CTA has read the counts: the last one re-zeroes the lists for the next launch
     __syncthreads();
     if (threadIdx.x == 0) {
         __threadfence();
         if (atomicAdd(&dw->done, 1u) == gridDim.x - 1) {
             dw->count = 0;
             dw->n_huge = 0;
+            dw->n_giant = 0;
             dw->done = 0;
             __threadfence();
         }
@@ -1740,8 +1803,8 @@ Layout prep_layout(int32_t kernel, const kp_csr *A, int64_t cap) {
 }
 
 // Long-row threshold of the row-mapped schedules (DeferWs): WM lists rows longer than 64
-// lanes-worth of its group (16 batches of 4 per lane), TM rows longer than max(256, 8 x the
-// known mean); both from the KNOWN shape only.  INT64_MAX (no list, no tail launch) when no
+// lanes-worth of its group (16 batches of 4 per lane), TM rows longer than 256 elements;
+// both from the KNOWN shape only.  INT64_MAX (no list, no tail launch) when no
 // row can be that long (n_cols <= T).
 int64_t long_threshold(int32_t kernel, const kp_csr *A) {
     static const bool off = [] {  // KP_NO_LONG_ROWS=1: A/B switch (the pre-deferral schedules)
@@ -1751,10 +1814,8 @@ int64_t long_threshold(int32_t kernel, const kp_csr *A) {
     if (off) return INT64_MAX;
     int64_t t = INT64_MAX;
     if (kernel == KP_CSR_WM) t = 64 * (int64_t)wm_group(A);
-    else if (kernel == KP_CSR_TM) {
-        const int64_t mean = A->n_rows > 0 ? (A->nnz + A->n_rows - 1) / A->n_rows : 0;
-        t = std::max<int64_t>(256, 8 * mean);
-    }
+    else if (kernel == KP_CSR_TM) t = 256;  // a thread walking more than ~64 batches is the pitfall
+                                          // whatever the mean (dense bands: 120x behind BM)
     return t < A->n_cols ? t : INT64_MAX;
 }
 // list capacity: rows past T (at most nnz / (T + 1)), then the huge rows past kLongCta
@@ -1762,9 +1823,13 @@ int64_t long_huge_at(int32_t kernel, const kp_csr *A) {
     const int64_t t = long_threshold(kernel, A);
     return t == INT64_MAX ? 0 : A->nnz / (t + 1) + 1;
 }
-int64_t long_slots(int32_t kernel, const kp_csr *A) {
+int64_t long_giant_at(int32_t kernel, const kp_csr *A) {
     const int64_t h = long_huge_at(kernel, A);
     return h ? h + A->nnz / (kLongCta + 1) + 1 : 0;
+}
+int64_t long_slots(int32_t kernel, const kp_csr *A) {
+    const int64_t g = long_giant_at(kernel, A);
+    return g ? g + A->nnz / (kLongGiant + 1) + 1 : 0;
 }
 
 int64_t spmv_units(int32_t kernel, const kp_csr *A) {
@@ -1892,7 +1957,8 @@ int launch_long_rows(int32_t kernel, const kp_csr *A, DeferWs *dw, const O *off,
     at[1].val.clusterDim.z = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    KP_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_long_rows<V, O>, dw, off, col, val, x, y, long_huge_at(kernel, A)));
+    KP_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_long_rows<V, O>, dw, off, col, val, x, y, long_huge_at(kernel, A),
+                                   long_giant_at(kernel, A)));
     KP_LAUNCHED();
     return KP_OK;
 }
@@ -1913,20 +1979,21 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
         case KP_CSR_WM: {
             const int G = P && P->group ? P->group : wm_group(A);
             const int64_t g = (R * G + 255) / 256;
-            const int64_t lt = long_threshold(kernel, A), ha = long_huge_at(kernel, A);
+            const int64_t lt = long_threshold(kernel, A), ha = long_huge_at(kernel, A), ga = long_giant_at(kernel, A);
             DeferWs *dw = reinterpret_cast<DeferWs *>(ws);
             switch (G) {
-                case 2: k_csr_wm<V, O, 2><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha); break;
-                case 4: k_csr_wm<V, O, 4><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha); break;
-                case 8: k_csr_wm<V, O, 8><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha); break;
-                case 16: k_csr_wm<V, O, 16><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha); break;
-                default: k_csr_wm<V, O, 32><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha); break;
+                case 2: k_csr_wm<V, O, 2><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha, ga); break;
+                case 4: k_csr_wm<V, O, 4><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha, ga); break;
+                case 8: k_csr_wm<V, O, 8><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha, ga); break;
+                case 16: k_csr_wm<V, O, 16><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha, ga); break;
+                default: k_csr_wm<V, O, 32><<<(unsigned)g, 256, 0, s>>>(off, col, val, x, y, R, dw, lt, ha, ga); break;
             }
             KP_LAUNCHED();
             return launch_long_rows<V, O>(kernel, A, dw, off, col, val, x, y, s);
         }
         case KP_CSR_BM: {
-            const int64_t g = R < (int64_t)sms * 512 ? R : (int64_t)sms * 512;
+            const int64_t groups = (R + 3) / 4;
+            const int64_t g = groups < (int64_t)sms * 512 ? groups : (int64_t)sms * 512;
             k_csr_bm<V, O><<<(unsigned)g, 128, 0, s>>>(off, col, val, x, y, R);
             KP_LAUNCHED();
             return KP_OK;
@@ -1946,16 +2013,16 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
                 if (rc) return rc;
             }
             constexpr unsigned bw = kTmRows * kTmSplitWide + 32, bn = kTmRows + 32;
-            const int64_t lt = long_threshold(kernel, A), ha = long_huge_at(kernel, A);
+            const int64_t lt = long_threshold(kernel, A), ha = long_huge_at(kernel, A), ga = long_giant_at(kernel, A);
             DeferWs *dw = reinterpret_cast<DeferWs *>(ws);
             if (aligned && wide)
-                k_csr_tm<V, O, true, kTmUWide, kTmSplitWide><<<(unsigned)g, bw, smem, s>>>(off, col, val, x, y, R, 1, cap, dw, lt, ha);
+                k_csr_tm<V, O, true, kTmUWide, kTmSplitWide><<<(unsigned)g, bw, smem, s>>>(off, col, val, x, y, R, 1, cap, dw, lt, ha, ga);
             else if (aligned)
-                k_csr_tm<V, O, true, 4, 1><<<(unsigned)g, bn, smem, s>>>(off, col, val, x, y, R, rpt, cap, dw, lt, ha);
+                k_csr_tm<V, O, true, 4, 1><<<(unsigned)g, bn, smem, s>>>(off, col, val, x, y, R, rpt, cap, dw, lt, ha, ga);
             else if (wide)
-                k_csr_tm<V, O, false, kTmUWide, kTmSplitWide><<<(unsigned)g, bw, smem, s>>>(off, col, val, x, y, R, 1, cap, dw, lt, ha);
+                k_csr_tm<V, O, false, kTmUWide, kTmSplitWide><<<(unsigned)g, bw, smem, s>>>(off, col, val, x, y, R, 1, cap, dw, lt, ha, ga);
             else
-                k_csr_tm<V, O, false, 4, 1><<<(unsigned)g, bn, smem, s>>>(off, col, val, x, y, R, rpt, cap, dw, lt, ha);
+                k_csr_tm<V, O, false, 4, 1><<<(unsigned)g, bn, smem, s>>>(off, col, val, x, y, R, rpt, cap, dw, lt, ha, ga);
             KP_LAUNCHED();
             return launch_long_rows<V, O>(kernel, A, dw, off, col, val, x, y, s);
         }

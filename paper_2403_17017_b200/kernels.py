@@ -46,13 +46,15 @@ class Prepared:
 
 
 def default_ell_cap(A: DeviceCSR, budget_bytes: int | None = None) -> int:
-    """Reserved ELL width: 2x the mean row length + 8, capped by a memory budget.
-    Rows longer than the actual width spill to the CSR tail, so any cap is correct."""
+    """Reserved ELL width: 2x the mean row length + 8, at most 128 slots (a thread walking
+    more is ELL's pitfall: a dense 8192-wide band ran 71x behind CSR,BM at width 8192), and
+    within a memory budget.  Rows longer than the actual width are finished by the ELL tail
+    kernel (warp / CTA per row), so any cap is correct."""
     torch = _lib.require_cuda()
     if A.n_rows == 0:
         return 1
     mean = A.nnz / A.n_rows
-    cap = int(math.ceil(2 * mean)) + 8
+    cap = min(int(math.ceil(2 * mean)) + 8, 128)
     if budget_bytes is None:
         free, _ = torch.cuda.mem_get_info(A.device)
         budget_bytes = free // 4

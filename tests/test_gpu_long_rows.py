@@ -27,11 +27,11 @@ def _mk(name, lens, n_cols, seed=3):
 def _fixtures():
     base = [5] * 3000
     lens = list(base)
-    # rows on both sides of the WM / TM thresholds (64 x G, max(256, 8 x mean)), of the tail's
-    # warp / CTA split (4096) and far past it
-    for i, l in enumerate([127, 128, 129, 255, 256, 257, 4095, 4096, 4097, 30000, 0, 1]):
-        lens[100 + 211 * i] = l
-    return [_mk("long_rows", lens, 40000), gen.powerlaw_rows(40000, 10.0, 1.2, seed=9),
+    # rows on both sides of the WM / TM thresholds (64 x G, 256), of the tail's warp / CTA
+    # split (4096), of its CTA / cluster split (65536) and past it
+    for i, l in enumerate([127, 128, 129, 255, 256, 257, 4095, 4096, 4097, 30000, 65536, 65537, 90000, 0, 1]):
+        lens[100 + 191 * i] = l
+    return [_mk("long_rows", lens, 100000), gen.powerlaw_rows(40000, 10.0, 1.2, seed=9),
             gen.config("C4", small=True), gen.config("C2", small=True)]
 
 
@@ -53,7 +53,7 @@ def test_long_rows_parity_and_repeat(kern, dtype, index, orc):
         assert ok, (m.name, kernels.KERNELS[kern], dtype, index, r)
         ws = kernels.spmv_workspace(A, kern)
         if ws is not None:  # the tail re-zeroed its counters
-            assert int(ws[:16].count_nonzero()) == 0, (m.name, kernels.KERNELS[kern])
+            assert int(ws[:16].count_nonzero()) == 0  # count, n_huge, n_giant, done, (m.name, kernels.KERNELS[kern])
 
 
 def test_no_list_when_rows_cannot_be_long():

@@ -37,6 +37,10 @@ MATS = {
     "u1m": lambda d: (gen.uniform_random(500_000, 500_000, 1_000_000, seed=5, device=d), torch.float32),
     "rmat15": lambda d: (gen.rmat(15, 16, device=d), torch.float32),
     "st43": lambda d: (gen.stencil27(43, device=d), torch.float32),
+    # round-2 pitfall cases: a dense band, a medium-width band, a road network
+    "dband": lambda d: (gen.banded(8192, 8192, device=d), torch.float32),
+    "band300": lambda d: (gen.banded(6641, 307, device=d), torch.float32),
+    "road": lambda d: (gen.road(3000, 0.62, device=d), torch.float32),
     # fp64 variants (C4 is the only fp64 BASELINE config)
     "C2d": lambda d: (gen.config("C2", device=d), torch.float64),
     "band27d": lambda d: (gen.banded(4_000_000, 27, device=d), torch.float64),
