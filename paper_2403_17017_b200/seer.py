@@ -338,7 +338,7 @@ def selector_label(row, known_pred: int, gathered_pred: int, k: int) -> int:
 
 def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int = 1,
                kernels=KERNELS, meta: dict | None = None, weighting: str = "none",
-               near_best: float = 0.0, selector_folds: int = 0) -> SeerModel:
+               near_best: float = 0.0, selector_folds: int = 0, gathered_depth: int | None = None) -> SeerModel:
     """labels = fastest_kernel per (matrix, k); known tree on the known
     schema, gathered tree on the full schema, selector on labels from the two
     sub-models' own predictions on the training rows.
@@ -353,8 +353,12 @@ def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int 
     near_best > 0 (extension) relabels each example with the kernel that is most often
     within (1 + near_best) x the best time across the training set, among the kernels
     within that factor on this example: ties between near-equal kernels stop being label
-    noise for CART (the realised cost changes by < near_best)."""
+    noise for CART (the realised cost changes by < near_best).
+
+    gathered_depth (extension): a separate depth for the gathered tree, which sees 8
+    features (and the iteration count) where the known and selector trees see 4."""
     nk = len(kernels)
+    gd = max_depth if gathered_depth is None else int(gathered_depth)
     pref = np.zeros(nk)
     if near_best > 0:
         for r in rows:
@@ -390,12 +394,12 @@ def train_seer(rows, iterations=(1,), max_depth: int = 5, min_samples_leaf: int 
     if not y:
         raise ValueError("no labelled examples")
     if weighting in ("cost-log", "cost-rel", "cost-mix"):
-        return _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, weighting, selector_folds)
+        return _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, weighting, selector_folds, gd)
     if weighting not in ("none", "regret"):
         raise ValueError("weighting must be 'none', 'regret', 'cost-log', 'cost-rel' or 'cost-mix'")
     w = None if weighting == "none" else np.asarray(wk) + 1e-3
     kt = train_tree(Xk, y, max_depth, min_samples_leaf, nk, KNOWN_SCHEMA, w)
-    gt = train_tree(Xg, y, max_depth, min_samples_leaf, nk, GATHERED_SCHEMA, w)
+    gt = train_tree(Xg, y, gd, min_samples_leaf, nk, GATHERED_SCHEMA, w)
     ys, wsel = [], []
     for (r, k), xk, xg in zip(ex, Xk, Xg):
         kp, gp = kt.predict(xk), gt.predict(xg)
@@ -426,7 +430,7 @@ def _loss(costs, kind: str, cap: float = 1e3):
 
 
 def _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, kind,
-                     selector_folds: int = 0) -> SeerModel:
+                     selector_folds: int = 0, gathered_depth=None) -> SeerModel:
     """Cost-sensitive trio (extension): kernel trees minimise the summed loss of the
     realised per-iteration-count cost (log or relative regret vs the example's best
     kernel), the selector minimises the loss of the realised known vs gathered path
@@ -441,7 +445,8 @@ def _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, kin
     nk = len(kernels)
     Ck = np.stack([_loss([r.cost(j, k) for j in range(nk)], kind) for r, k in ex])
     kt = train_cost_tree(Xk, Ck, max_depth, min_samples_leaf, KNOWN_SCHEMA)
-    gt = train_cost_tree(Xg, Ck, max_depth, min_samples_leaf, GATHERED_SCHEMA)
+    gd = max_depth if gathered_depth is None else gathered_depth
+    gt = train_cost_tree(Xg, Ck, gd, min_samples_leaf, GATHERED_SCHEMA)
     kpred = [kt.predict(xk) for xk in Xk]
     gpred = [gt.predict(xg) for xg in Xg]
     if selector_folds > 1:
@@ -454,7 +459,7 @@ def _train_seer_cost(ex, Xk, Xg, max_depth, min_samples_leaf, kernels, meta, kin
             if len(te) == 0 or len(tr) == 0:
                 continue
             kt_f = train_cost_tree(Xk_a[tr], Ck[tr], max_depth, min_samples_leaf, KNOWN_SCHEMA)
-            gt_f = train_cost_tree(Xg_a[tr], Ck[tr], max_depth, min_samples_leaf, GATHERED_SCHEMA)
+            gt_f = train_cost_tree(Xg_a[tr], Ck[tr], gd, min_samples_leaf, GATHERED_SCHEMA)
             for i in te:
                 kpred[i] = kt_f.predict(Xk[i])
                 gpred[i] = gt_f.predict(Xg[i])

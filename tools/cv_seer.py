@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--depths", default="4,5,6")
     ap.add_argument("--leaves", default="1,4")
     ap.add_argument("--selector-folds", default="0,5")
+    ap.add_argument("--gathered-depths", default="0", help="gathered-tree depths (0 = same as --depths)")
     a = ap.parse_args()
     rows = load(a.corpus)
     train, _ = dataset.split_train_test(rows, a.seed, 0.8)
@@ -35,15 +36,16 @@ def main():
     fold = {n: i % a.folds for i, n in enumerate(names)}
     nk = len(kernels.KERNELS)
     grid = itertools.product([int(v) for v in a.depths.split(",")], [int(v) for v in a.leaves.split(",")],
-                             [int(v) for v in a.selector_folds.split(",")])
-    for depth, leaf, sf in grid:
+                             [int(v) for v in a.selector_folds.split(",")], [int(v) for v in a.gathered_depths.split(",")])
+    for depth, leaf, sf, gdep in grid:
         sel = {k: 0.0 for k in ITERS}
         fixed = {k: [0.0] * nk for k in ITERS}
         real = {k: [] for k in ITERS}
         for f in range(a.folds):
             tr = [r for r in train if fold[r.name] != f]
             te = [r for r in train if fold[r.name] == f]
-            m = seer.train_seer(tr, ITERS, depth, leaf, kernels.KERNELS, weighting="cost-mix", selector_folds=sf)
+            m = seer.train_seer(tr, ITERS, depth, leaf, kernels.KERNELS, weighting="cost-mix", selector_folds=sf,
+                                gathered_depth=gdep or None)
             for k in ITERS:
                 for r in te:
                     c = seer.realized_cost(m, r, k)[0]
@@ -59,7 +61,7 @@ def main():
             bf = min(range(nk), key=lambda K: fixed[k][K])
             per = math.exp(sum(math.log(r.cost(bf, k) / c) for r, c in real[k]) / len(real[k]))
             out.append(f"k{k}: agg {fixed[k][bf] / sel[k]:.3f} per-matrix {per:.3f}")
-        print(f"depth {depth} leaf {leaf} selector_folds {sf}  " + "  ".join(out), flush=True)
+        print(f"depth {depth} gathered_depth {gdep or depth} leaf {leaf} selector_folds {sf}  " + "  ".join(out), flush=True)
 
 
 if __name__ == "__main__":

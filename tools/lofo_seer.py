@@ -57,7 +57,7 @@ def main():
     frozen = seer.SeerModel.load(a.bundle)
     meta = frozen.meta
     fams = sorted({family(r.name) for r in rows})
-    out = {"hyper_parameters": {k: meta.get(k) for k in ("max_depth", "min_samples_leaf", "weighting",
+    out = {"hyper_parameters": {k: meta.get(k) for k in ("max_depth", "gathered_depth", "min_samples_leaf", "weighting",
                                                          "selector_folds", "iterations")},
            "families": {}}
     for f in fams:
@@ -65,7 +65,7 @@ def main():
         train = [r for r in rows if family(r.name) != f]
         m = seer.train_seer(train, ITERS, meta.get("max_depth", 5), meta.get("min_samples_leaf", 16),
                             kernels.KERNELS, weighting=meta.get("weighting", "cost-mix"),
-                            selector_folds=meta.get("selector_folds", 0))
+                            selector_folds=meta.get("selector_folds", 0), gathered_depth=meta.get("gathered_depth"))
         res = {"n_held_out": len(held), "n_train": len(train), "k": {}}
         for k in ITERS:
             lofo, fr = realise(m, held, k), realise(frozen, held, k)

@@ -75,6 +75,7 @@ def main():
     ap.add_argument("--out", required=True)
     ap.add_argument("--report", default=None)
     ap.add_argument("--max-depth", type=int, default=5)
+    ap.add_argument("--gathered-depth", type=int, default=0, help="gathered-tree depth (0 = --max-depth)")
     ap.add_argument("--min-leaf", type=int, default=4,
                     help="min training examples per leaf (tools/cv_seer.py: 4 is robust, 1 overfits)")
     ap.add_argument("--seed", type=int, default=2403)
@@ -91,8 +92,9 @@ def main():
                              "iterations": list(ITERS), "max_depth": a.max_depth, "min_samples_leaf": a.min_leaf,
                              "split_seed": a.seed,
                              "n_train": len(train), "n_test": len(test), "near_best": a.near_best,
-                             "selector_folds": a.selector_folds},
-                            weighting=a.weighting, near_best=a.near_best, selector_folds=a.selector_folds)
+                             "selector_folds": a.selector_folds, "gathered_depth": a.gathered_depth or a.max_depth},
+                            weighting=a.weighting, near_best=a.near_best, selector_folds=a.selector_folds,
+                            gathered_depth=a.gathered_depth or None)
     model.save(a.out)
     plain = seer.train_seer(train, ITERS, a.max_depth, 1, kernels.KERNELS, weighting="none")
     rep = {"weighting": a.weighting, "n_train": len(train), "n_test": len(test),
