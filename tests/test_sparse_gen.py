@@ -53,3 +53,36 @@ def test_gpu_parity_fixtures_are_canonical():
     """The GPU parity matrices themselves must be valid CSR (caught an out-of-range fixture)."""
     import test_gpu_spmv as t
     assert len(t.mats()) >= 13
+
+
+@pytest.mark.parametrize("make", [
+    lambda: gen.fem_mesh(40, 1), lambda: gen.fem_mesh(30, 2), lambda: gen.circuit(3000, 4, 0.05),
+    lambda: gen.road(50, 0.6)])
+def test_structured_families_are_canonical_and_symmetric(make):
+    """The OOD families (gen.fem_mesh / circuit / road): canonical CSR (sorted, unique, in
+    range -- SparseMatrixCSR's checks), a symmetric pattern with a full diagonal, and the
+    row-length shapes they stand for."""
+    m = make()
+    sp = m.to_sparse_csr()
+    off, col = np.asarray(sp.row_offsets), np.asarray(sp.col_indices)
+    n = m.n_rows
+    rows = np.repeat(np.arange(n), np.diff(off))
+    pairs = set(zip(rows.tolist(), col.tolist()))
+    assert all((c, r) in pairs for r, c in pairs)
+    assert all((i, i) in pairs for i in range(n))
+    ln = np.diff(off)
+    if m.name.startswith("fem_p1"):
+        assert ln.max() == 7 and ln.min() >= 3
+    elif m.name.startswith("fem_p2"):
+        assert ln.max() == 19
+    elif m.name.startswith("circuit"):
+        assert ln.max() > 10 * np.median(ln)  # supply rails: dense rows (and columns)
+    else:
+        assert ln.max() <= 8 and 2.5 < ln.mean() < 4.5
+
+
+def test_structured_families_are_seeded():
+    a, b = gen.circuit(2000, 3, 0.1, seed=5), gen.circuit(2000, 3, 0.1, seed=5)
+    assert np.array_equal(a.col_indices.numpy(), b.col_indices.numpy())
+    c = gen.circuit(2000, 3, 0.1, seed=6)
+    assert not (c.nnz == a.nnz and np.array_equal(a.col_indices.numpy(), c.col_indices.numpy()))
