@@ -1803,7 +1803,7 @@ Layout prep_layout(int32_t kernel, const kp_csr *A, int64_t cap) {
 }
 
 // Long-row threshold of the row-mapped schedules (DeferWs): WM lists rows longer than 64
-// lanes-worth of its group (16 batches of 4 per lane), TM rows longer than 256 elements;
+// lanes-worth of its group (16 batches of 4 per lane), TM rows longer than 128 elements;
 // both from the KNOWN shape only.  INT64_MAX (no list, no tail launch) when no
 // row can be that long (n_cols <= T).
 int64_t long_threshold(int32_t kernel, const kp_csr *A) {
@@ -1814,8 +1814,17 @@ int64_t long_threshold(int32_t kernel, const kp_csr *A) {
     if (off) return INT64_MAX;
     int64_t t = INT64_MAX;
     if (kernel == KP_CSR_WM) t = 64 * (int64_t)wm_group(A);
-    else if (kernel == KP_CSR_TM) t = 256;  // a thread walking more than ~64 batches is the pitfall
-                                          // whatever the mean (dense bands: 120x behind BM)
+    else if (kernel == KP_CSR_TM) {
+        // a thread walking more than ~32 batches of 4 is the pitfall whatever the mean (dense
+        // bands ran 120x behind BM).  A/B of the threshold (profiles/ab_tm_long_r02.txt, per
+        // SpMV): 256 -> 128: C2 216 -> 174 us, band 300 108 -> 22 us, power-law 503 -> 443 us,
+        // C3 / band 27 / stencils unchanged; 64 cost C3 1 %.  KP_TM_LONG overrides (A/B).
+        static const int64_t tm_t = [] {
+            const char *e = getenv("KP_TM_LONG");
+            return e ? (int64_t)atoll(e) : (int64_t)128;
+        }();
+        t = tm_t;
+    }
     return t < A->n_cols ? t : INT64_MAX;
 }
 // list capacity: rows past T (at most nnz / (T + 1)), then the huge rows past kLongCta

@@ -27,7 +27,7 @@ def _mk(name, lens, n_cols, seed=3):
 def _fixtures():
     base = [5] * 3000
     lens = list(base)
-    # rows on both sides of the WM / TM thresholds (64 x G, 256), of the tail's warp / CTA
+    # rows on both sides of the WM / TM thresholds (64 x G, 128), of the tail's warp / CTA
     # split (4096), of its CTA / cluster split (65536) and past it
     for i, l in enumerate([127, 128, 129, 255, 256, 257, 4095, 4096, 4097, 30000, 65536, 65537, 90000, 0, 1]):
         lens[100 + 191 * i] = l
