@@ -59,7 +59,7 @@ def test_long_rows_parity_and_repeat(kern, dtype, index, orc):
 def test_no_list_when_rows_cannot_be_long():
     L = _lib.load()
     m = gen.banded(5000, 27)  # n_cols 5000 > both thresholds: a list is sized
-    narrow = _mk("narrow", [50] * 2000, 200)  # no row can exceed 200 <= both thresholds
+    narrow = _mk("narrow", [50] * 2000, 100)  # no row can exceed 100 <= both thresholds
     for mm, want_zero in ((narrow, True), (m, False)):
         A = mm.to_device_csr(torch.float32)
         for k in (kernels.CSR_WM, kernels.CSR_TM):
