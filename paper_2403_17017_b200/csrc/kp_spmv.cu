@@ -1813,7 +1813,13 @@ int64_t long_threshold(int32_t kernel, const kp_csr *A) {
     }();
     if (off) return INT64_MAX;
     int64_t t = INT64_MAX;
-    if (kernel == KP_CSR_WM) t = 64 * (int64_t)wm_group(A);
+    if (kernel == KP_CSR_WM) {
+        static const int64_t wm_m = [] {  // KP_WM_LONG_MULT overrides (A/B)
+            const char *e = getenv("KP_WM_LONG_MULT");
+            return e ? (int64_t)atoll(e) : (int64_t)64;
+        }();
+        t = wm_m * (int64_t)wm_group(A);
+    }
     else if (kernel == KP_CSR_TM) {
         // a thread walking more than ~32 batches of 4 is the pitfall whatever the mean (dense
         // bands ran 120x behind BM).  A/B of the threshold (profiles/ab_tm_long_r02.txt, per
