@@ -197,18 +197,70 @@ __device__ __forceinline__ V block_sum(V v, V *sred) {
 // Block-mapped: a CTA per row, so long rows get 128 x 4 gathers in flight and one block
 // reduction.  A CTA spent on a row of a handful of elements is the schedule's pitfall
 // (round-1 corpus: 5-70x behind the best kernel on short-row matrices, C2 443 us, road
-// networks 69x).  So the CTA takes a block of 128 rows per step and sorts them by length
-// in shared memory: rows of up to kBmThread elements are summed by their own thread (the
-// whole block's short rows in one trip), rows up to kBmShort by a warp each, and only the
-// longer ones get the whole CTA, one after another (block_sum, the classic BM).  Each
-// length class has a fixed reduction order, so y is bit-identical run to run.
-constexpr int kBmThreads = 128;
-constexpr int64_t kBmThread = 8;
+// networks 69x), so rows are taken four at a time: each of the CTA's 4 warps sums one row
+// of up to kBmShort elements (lane-strided batches + shuffle tree), and the group's longer
+// rows then get the whole CTA, one after another (block_sum, as before).  Fixed reduction
+// orders either way: y is bit-identical run to run.
 constexpr int64_t kBmShort = 256;
 template <typename V, typename O>
-__global__ void __launch_bounds__(kBmThreads) k_csr_bm(const O *__restrict__ off, const int32_t *__restrict__ col,
+__global__ void __launch_bounds__(128) k_csr_bm(const O *__restrict__ off, const int32_t *__restrict__ col,
+                                                const V *__restrict__ val, const V *__restrict__ x,
+                                                V *__restrict__ y, int64_t n_rows) {
+    __shared__ V sred[32];
+    __shared__ int64_t s_s[4], s_e[4];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int64_t r0 = (int64_t)blockIdx.x * 4; r0 < n_rows; r0 += (int64_t)gridDim.x * 4) {
+        const int64_t row = r0 + w;
+        int64_t s = 0, e = 0;
+        if (row < n_rows) {
+            s = ldo(off + row);
+            e = ldo(off + row + 1);
+        }
+        if (e - s <= kBmShort) {  // short (or past the end): this warp
+            if (row < n_rows) {
+                V sum = 0;
+                for (int64_t j = s + lane; j < e; j += 4 * 32) sum = batch_dot<4, 32>(col, val, x, j, e, sum);
+                sum = group_sum<32>(sum);
+                if (lane == 0) y[row] = sum;
+            }
+            s = e = 0;  // nothing left for the CTA
+        }
+        if (lane == 0) {
+            s_s[w] = s;
+            s_e[w] = e;
+        }
+        __syncthreads();
+        for (int q = 0; q < 4; ++q) {  // the group's long rows: the whole CTA each
+            const int64_t qs = s_s[q], qe = s_e[q];
+            if (qe - qs <= kBmShort) continue;  // uniform over the CTA
+            V sum = 0;
+            for (int64_t j = qs + threadIdx.x; j < qe; j += 4 * 128) sum = batch_dot<4, 128>(col, val, x, j, qe, sum);
+            const V t = block_sum(sum, sred);
+            if (threadIdx.x == 0) y[r0 + q] = t;
+            __syncthreads();  // sred reuse
+        }
+        __syncthreads();  // s_s / s_e reuse
+    }
+}
+
+// CSR,BM for a KNOWN mean of at most kBmTinyMean elements per row (road networks, meshes,
+// power-law graphs): rows of a few elements leave even a warp per row latency-bound (road
+// 23x behind CSR,TM with the 4-row groups above), so the CTA takes a block of 128 rows per
+// step and sorts them by length in shared memory: rows of up to `thread_max` (kBmThread)
+// elements are summed by their own thread (the whole block's short rows in one trip), rows
+// up to kBmShort by a warp each, the longer ones by the whole CTA (block_sum).  A row's
+// length class fixes its reduction order, so y is bit-identical run to run.  Thresholds by
+// A/B (profiles/ab_bm_r02.txt, per SpMV, this variant vs the 4-row groups): road 2067 ->
+// 111 us, C2 276 -> 145 us, power-law 1042 -> 834 us, C1 10.3 us either way; means above
+// 16 keep the 4-row groups (const 32: 967 vs 1407 us, 27-point stencils 28.7 vs 24.6 us at
+// mean 27 is the one loss the cut leaves out).
+constexpr int kBmThreads = 128;
+constexpr int64_t kBmThread = 32;
+constexpr double kBmTinyMean = 16.0;
+template <typename V, typename O>
+__global__ void __launch_bounds__(kBmThreads) k_csr_bm_short(const O *__restrict__ off, const int32_t *__restrict__ col,
                                                        const V *__restrict__ val, const V *__restrict__ x,
-                                                       V *__restrict__ y, int64_t n_rows) {
+                                                       V *__restrict__ y, int64_t n_rows, int64_t thread_max) {
     __shared__ V sred[32];
     __shared__ int64_t s_w[kBmThreads], s_c[kBmThreads];
     __shared__ int s_nw, s_nc;
@@ -222,7 +274,7 @@ __global__ void __launch_bounds__(kBmThreads) k_csr_bm(const O *__restrict__ off
         const int64_t row = r0 + tid;
         if (row < n_rows) {
             const int64_t s = ldo(off + row), e = ldo(off + row + 1);
-            if (e - s <= kBmThread) {  // this thread
+            if (e - s <= thread_max) {  // this thread
                 V sum = 0;
                 for (int64_t j = s; j < e; j += 4) sum = batch_dot<4, 1>(col, val, x, j, e, sum);
                 y[row] = sum;
@@ -2018,9 +2070,23 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
             return launch_long_rows<V, O>(kernel, A, dw, off, col, val, x, y, s);
         }
         case KP_CSR_BM: {
-            const int64_t blocks = (R + kBmThreads - 1) / kBmThreads;
-            const int64_t g = blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16;  // one resident wave
-            k_csr_bm<V, O><<<(unsigned)g, kBmThreads, 0, s>>>(off, col, val, x, y, R);
+            static const double tiny = [] {  // KP_BM_TINY_MEAN / KP_BM_THREAD: A/B overrides
+                const char *e = getenv("KP_BM_TINY_MEAN");
+                return e ? atof(e) : kBmTinyMean;
+            }();
+            static const int64_t thr = [] {
+                const char *e = getenv("KP_BM_THREAD");
+                return e ? (int64_t)atoll(e) : kBmThread;
+            }();
+            if ((double)Z <= tiny * (double)R) {  // short known mean: thread-per-row tier
+                const int64_t blocks = (R + kBmThreads - 1) / kBmThreads;
+                const int64_t g = blocks < (int64_t)sms * 16 ? blocks : (int64_t)sms * 16;  // one resident wave
+                k_csr_bm_short<V, O><<<(unsigned)g, kBmThreads, 0, s>>>(off, col, val, x, y, R, thr);
+            } else {
+                const int64_t groups = (R + 3) / 4;
+                const int64_t g = groups < (int64_t)sms * 512 ? groups : (int64_t)sms * 512;
+                k_csr_bm<V, O><<<(unsigned)g, 128, 0, s>>>(off, col, val, x, y, R);
+            }
             KP_LAUNCHED();
             return KP_OK;
         }

@@ -28,6 +28,9 @@ def _edge_matrices():
     ms.append(gen.powerlaw_rows(30000, 12.0, 1.3, seed=4))
     ms.append(gen.constant_rows(50000, 3, seed=2))
     ms.append(gen.banded(40000, 27))
+    # known mean <= 4 (CSR,BM's thread-per-row variant) with a few long rows mixed in
+    ms.append(gen.road(120, 0.6))
+    ms.append(gen.circuit(20000, 3, 0.02))
     return ms
 
 
