@@ -30,4 +30,29 @@ for m in t.mats():
             print(m.name, dt, kernels.KERNELS[k], flush=True)
             kernels.spmv(A, x, k)
             torch.cuda.synchronize()
+# round 2: long-row lists + tail (WM / TM), the compact column transfer, emitted-tree plans
+import test_gpu_long_rows as tl  # noqa: E402
+for m in tl._fixtures():
+    A = m.to_device_csr(torch.float32)
+    x = torch.rand(A.n_cols, device="cuda")
+    for k in (kernels.CSR_WM, kernels.CSR_TM, kernels.CSR_BM):
+        print(m.name, "long rows", kernels.KERNELS[k], flush=True)
+        kernels.spmv(A, x, k)
+        torch.cuda.synchronize()
+    H = device.HostPackedCSR(A)
+    d_buf, B = H.staging(A.device)
+    H.upload(d_buf, B)
+    torch.cuda.synchronize()
+    assert torch.equal(B.col_indices, A.col_indices)
+print("long rows / pack ok", flush=True)
+from paper_2403_17017_b200 import gen, seer  # noqa: E402
+model = seer.SeerModel.load(os.path.join(ROOT, "paper_2403_17017_b200", "models", "seer_b200.json"))
+A = gen.config("C1").to_device_csr(torch.float32)
+x = torch.rand(A.n_cols, device="cuda")
+y = torch.empty(A.n_rows, device="cuda")
+plan = seer.SeerPlan(model, A, x, y, 100)  # the bundle's gathered path (emitted trees)
+plan.launch()
+torch.cuda.synchronize()
+print("plan", plan.select_kind(), flush=True)
+plan.close()
 print("all ok")
