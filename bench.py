@@ -220,23 +220,16 @@ class Timer:
         return out
 
     def paired(self, fa, fb, reps):
-        """fa enqueues work directly (the Seer plan); fb is captured once as a graph (a fixed
-        kernel's prep + k SpMVs).  Samples alternate a, b, a, b ... so both legs see the same
-        clock / power state over the run; returns (a samples, b samples) in seconds."""
-        torch = self.torch
+        """fa, fb each enqueue one graph launch (the Seer plan; a fixed kernel's constant-model
+        plan).  Samples alternate a, b, a, b ... so both legs see the same clock / power state
+        over the run; returns (a samples, b samples) in seconds."""
+        fa()
         fb()
-        cs = torch.cuda.Stream()
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=cs):
-            fb()
-        g.replay()
-        torch.cuda.synchronize()
+        self.torch.cuda.synchronize()
         ta, tb = [], []
         for _ in range(reps):
             ta += self.direct(fa, 1)
-            tb += self.direct(g.replay, 1)
-        del g
+            tb += self.direct(fb, 1)
         return ta, tb
 
     def graph(self, fn, reps, warm=1):
@@ -348,18 +341,18 @@ def measure(name, dev, model, a, *, steps, warmup, headline=False, sweep=True, e
         for kk in range(len(kernels.KERNELS)):
             Pk = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
 
-            def total(kk=kk):
-                PP = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
-                for _ in range(k):
-                    kernels.spmv(A, x, kk, y=y, prepared=PP)
-
             def prep_only(kk=kk):
                 kernels.prepare(A, kk, cache=False)
 
             def iters_only(kk=kk, Pk=Pk):
                 for _ in range(k):
                     kernels.spmv(A, x, kk, y=y, prepared=Pk)
-            t_tot = statistics.median(T.graph(total, reps))
+            # totals as constant-model Seer plans: built and launched like the Seer plan
+            # itself (a torch-captured graph of the same calls is ~1-2 us slower per launch,
+            # tools/graph_launch_probe.py, which would flatter Seer on small inputs)
+            fp = seer.SeerPlan(seer.fixed_model(kk), A, x, y, k)
+            t_tot = statistics.median(T.direct(fp.launch, reps))
+            fp.close()
             t_prep = statistics.median(T.graph(prep_only, reps)) if kk in kernels.NEEDS_PREP else 0.0
             t_sp = statistics.median(T.graph(iters_only, reps)) / k
             w = None
@@ -380,11 +373,9 @@ def measure(name, dev, model, a, *, steps, warmup, headline=False, sweep=True, e
         # clock / power drift between the Seer leg and the sweep cannot bias it
         kb = kernels.KERNELS.index(best)
 
-        def best_total(kk=kb):
-            PP = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
-            for _ in range(k):
-                kernels.spmv(A, x, kk, y=y, prepared=PP)
-        ta, tb = T.paired(plan.launch, best_total, max(5, steps // 2))
+        bp = seer.SeerPlan(seer.fixed_model(kb), A, x, y, k)
+        ta, tb = T.paired(plan.launch, bp.launch, max(5, steps // 2))
+        bp.close()
         res["speedup_vs_best_fixed"] = round(statistics.median(tb) / statistics.median(ta), 3)
         res["paired"] = {"seer_us_median": round(statistics.median(ta) * 1e6, 2),
                          "best_fixed_us_median": round(statistics.median(tb) * 1e6, 2), "samples": len(ta),

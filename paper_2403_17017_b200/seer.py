@@ -500,6 +500,16 @@ def geomean_speedup(rows, model: SeerModel, k: int) -> dict:
             "oracle_total": rep.predictors["oracle"].total_realized_cost}
 
 
+def fixed_model(kernel) -> SeerModel:
+    """A constant model: the selector always takes the known path and both trees answer
+    `kernel`.  A SeerPlan of it is that fixed kernel's prep + k SpMVs built and launched
+    exactly like a Seer plan (same capture, same graph launch) -- the baseline the
+    Seer-vs-fixed comparisons time."""
+    k = kernel if isinstance(kernel, int) else KERNELS.index(kernel)
+    return SeerModel(leaf_tree(k, len(KERNELS), 4), leaf_tree(k, len(KERNELS), 8), leaf_tree(USE_KNOWN, 2, 4),
+                     KERNELS, {"fixed_kernel": KERNELS[k]})
+
+
 def bootstrap_model() -> SeerModel:
     """A rule-derived placeholder used only until a B200-measured bundle exists
     (models/seer_b200.json).  Selector always gathers; gathered tree splits on

@@ -212,18 +212,10 @@ def _plan_overhead(model, A, x, y, flush, ev, reps: int = 5):
 
     t_plan = med(plan.launch)
     plan.close()
-
-    def body():
-        P = kernels.prepare(A, kern, cache=False) if kern in kernels.NEEDS_PREP else None
-        kernels.spmv(A, x, kern, y=y, prepared=P)
-    body()
-    cs = torch.cuda.Stream()
-    torch.cuda.synchronize()
-    g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g, stream=cs):
-        body()
-    t_body = med(g.replay)
-    del g
+    # the same body as a constant-model plan: same graph construction and launch
+    body = seer.SeerPlan(seer.fixed_model(kern), A, x, y, 1)
+    t_body = med(body.launch)
+    body.close()
     return max(t_plan - t_body, 1e-6)
 
 
@@ -259,9 +251,9 @@ def _eager_costs(A, x, y, k, flush, ev, reps, cap_ms):
 
 
 def _graph_costs(A, x, y, k, flush, ev, reps, cap_ms):
-    """(runtime, preprocess) as the Seer plan realises them: the kernel's prep + n SpMVs
-    captured as ONE graph (like kp_seer_plan's body and tools/eval_seer.py's fixed
-    kernels), L2 flushed before each launch.  runtime = the marginal cost of one more
+    """(runtime, preprocess) as the Seer plan realises them: the kernel's prep + n SpMVs as
+    ONE graph -- a constant-model kp_seer_plan, i.e. exactly the Seer plan's body --, L2
+    flushed before each launch.  runtime = the marginal cost of one more
     iteration, (t_n - t_1) / (n - 1) -- later iterations find a matrix that fits in L2
     warm, as a real iterative run does; preprocess = t_1 - runtime, so prep + k x runtime
     reproduces the measured 1-iteration graph exactly and the n-iteration one by
@@ -283,23 +275,23 @@ def _graph_costs(A, x, y, k, flush, ev, reps, cap_ms):
         return _eager_costs(A, x, y, k, flush, ev, 0, cap_ms)
 
     def graph_time(n):
-        cs = torch.cuda.Stream()
-        torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g, stream=cs):
-            body(n)
-        g.replay()
+        # prep + n SpMVs as a constant-model Seer plan: the graph the Seer plan's body is,
+        # built and launched the same way (a torch-captured graph of the same calls runs
+        # ~1-2 us slower per launch, tools/graph_launch_probe.py)
+        from paper_2403_17017_b200 import seer
+        plan = seer.SeerPlan(seer.fixed_model(k), A, x, y, n)
+        plan.launch()
         torch.cuda.synchronize()
         ts = []
         for _ in range(reps):
             flush.zero_()
             a0, a1 = ev(), ev()
             a0.record()
-            g.replay()
+            plan.launch()
             a1.record()
             a1.synchronize()
             ts.append(a0.elapsed_time(a1) * 1e-3)
-        del g
+        plan.close()
         return statistics.median(ts)
 
     t1 = graph_time(1)

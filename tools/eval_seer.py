@@ -9,6 +9,9 @@ configs C1-C4: the Seer plan (kp_seer_plan: selection -> chosen preprocessing ->
 one graph) and every fixed kernel's prep + k SpMVs (captured as a graph the same way) are
 timed with CUDA events, L2 flushed, median of --reps.  Kernels whose single SpMV exceeds
 --cap-ms are timed once and extrapolated (prep + k x t) -- they are never the best.
+Fixed kernels are timed as constant-model Seer plans (seer.fixed_model): the same graph
+construction and launch as the Seer plan, so launch machinery cancels (a torch-captured
+graph of the same calls runs ~1-2 us slower, tools/graph_launch_probe.py).
 Reported per k: per-matrix geomean of T_best_fixed_kernel / T_seer (the north star's "beats
 the best single fixed kernel in geomean"), aggregate T_best_fixed / T_seer (paper's 2x),
 geomean over kernels of T_K / T_seer (paper's 6.5x), T_seer / T_oracle, and selection
@@ -133,11 +136,11 @@ def main():
                     fixed[kk] = single[kk] * k  # slow kernel: SpMVs alone (lower bound; never the best)
                     continue
 
-                def step(kk=kk):
-                    P = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
-                    for _ in range(k):
-                        kernels.spmv(A, x, kk, y=y, prepared=P)
-                fixed[kk] = t_graph(step, a.reps)
+                # the fixed kernel's prep + k SpMVs built and launched exactly like the Seer
+                # plan (a constant-model kp_seer_plan), so launch machinery cancels out
+                fp = seer.SeerPlan(seer.fixed_model(kk), A, x, y, k)
+                fixed[kk] = t_direct(fp.launch, a.reps)
+                fp.close()
             rec["k"][str(k)] = {"seer_s": t_seer, "kernel": kernels.KERNELS[int(o.kernel)], "path": int(o.path),
                                 "host_kernel": kernels.KERNELS[hk], "host_path": hp,
                                 "fixed_s": {kernels.KERNELS[kk]: v for kk, v in fixed.items()}}
