@@ -701,12 +701,25 @@ __global__ void __launch_bounds__(256) k_prep_ell(PrepHeader *__restrict__ hdr, 
     bool is_long = false;
     if (row < n_rows) {
         const int64_t s = ldo(off + row), e = ldo(off + row + 1);
-        for (int64_t k = 0; k < W; ++k) {
-            const int64_t j = s + k;
-            const bool in = j < e;
-            const int64_t slot = (row >> 5) * 32 * W + k * 32 + (row & 31);
-            ecol[slot] = in ? __ldg(col + j) : 0;
-            evalv[slot] = in ? __ldg(val + j) : V(0);
+        // 8 slots per trip: all 16 loads issued before the stores (a slot-at-a-time loop
+        // kept one load pair in flight per thread: 64 M x 8 const rows took ~36 ms)
+        for (int64_t k0 = 0; k0 < W; k0 += 8) {
+            int32_t c[8];
+            V v[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                const int64_t j = s + k0 + i;
+                const bool in = k0 + i < W && j < e;
+                c[i] = in ? __ldg(col + j) : 0;
+                v[i] = in ? __ldg(val + j) : V(0);
+            }
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (k0 + i >= W) break;
+                const int64_t slot = (row >> 5) * 32 * W + (k0 + i) * 32 + (row & 31);
+                ecol[slot] = c[i];
+                evalv[slot] = v[i];
+            }
         }
         if (e - s > W) {
             is_long = e - s - W > kEllLongTail;

@@ -263,15 +263,20 @@ def _graph_costs(A, x, y, k, flush, ev, reps, cap_ms):
         for _ in range(n):
             kernels.spmv(A, x, k, y=y, prepared=P)
 
-    body(1)  # first use: attributes, workspaces
+    body(1)  # first use: attributes, workspaces, allocations
     torch.cuda.synchronize()
-    e0, e1 = ev(), ev()
-    flush.zero_()
-    e0.record()
-    body(1)
-    e1.record()
-    e1.synchronize()
-    if e0.elapsed_time(e1) > cap_ms:
+    # the cap check on a WARM eager run (the first one pays allocations: a 64 M-row ELL
+    # layout took > 40 ms cold and its eager preparation then landed in the corpus as 36 ms)
+    t_warm = []
+    for _ in range(2):
+        e0, e1 = ev(), ev()
+        flush.zero_()
+        e0.record()
+        body(1)
+        e1.record()
+        e1.synchronize()
+        t_warm.append(e0.elapsed_time(e1))
+    if min(t_warm) > cap_ms:
         return _eager_costs(A, x, y, k, flush, ev, 0, cap_ms)
 
     def graph_time(n):

@@ -41,6 +41,7 @@ MATS = {
     "dband": lambda d: (gen.banded(8192, 8192, device=d), torch.float32),
     "band300": lambda d: (gen.banded(6641, 307, device=d), torch.float32),
     "road": lambda d: (gen.road(3000, 0.62, device=d), torch.float32),
+    "const8big": lambda d: (gen.constant_rows(64_000_000, 8, seed=78, device=d), torch.float32),
     # fp64 variants (C4 is the only fp64 BASELINE config)
     "C2d": lambda d: (gen.config("C2", device=d), torch.float64),
     "band27d": lambda d: (gen.banded(4_000_000, 27, device=d), torch.float64),
