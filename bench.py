@@ -374,10 +374,16 @@ def measure(name, dev, model, a, *, steps, warmup, headline=False, sweep=True, e
         kb = kernels.KERNELS.index(best)
 
         bp = seer.SeerPlan(seer.fixed_model(kb), A, x, y, k)
-        ta, tb = T.paired(plan.launch, bp.launch, max(5, steps // 2))
+        # CUDA event timestamps tick in ~2 us steps on this part: a 10 us step is a few ticks,
+        # so a small config gets enough alternating samples (>= ~20 ms of timed work per
+        # leg) and the ratio of MEANS, which the launch-to-launch jitter dithers below the tick
+        reps = int(min(400, max(max(5, steps // 2), 0.02 / max(seer_mean, 1e-6))))
+        ta, tb = T.paired(plan.launch, bp.launch, reps)
         bp.close()
-        res["speedup_vs_best_fixed"] = round(statistics.median(tb) / statistics.median(ta), 3)
-        res["paired"] = {"seer_us_median": round(statistics.median(ta) * 1e6, 2),
+        res["speedup_vs_best_fixed"] = round(statistics.mean(tb) / statistics.mean(ta), 3)
+        res["paired"] = {"seer_us_mean": round(statistics.mean(ta) * 1e6, 2),
+                         "best_fixed_us_mean": round(statistics.mean(tb) * 1e6, 2),
+                         "seer_us_median": round(statistics.median(ta) * 1e6, 2),
                          "best_fixed_us_median": round(statistics.median(tb) * 1e6, 2), "samples": len(ta),
                          "unpaired_speedup": round(ratios[best], 3)}
     if clocks:
