@@ -221,15 +221,19 @@ class Timer:
 
     def paired(self, fa, fb, reps):
         """fa, fb each enqueue one graph launch (the Seer plan; a fixed kernel's constant-model
-        plan).  Samples alternate a, b, a, b ... so both legs see the same clock / power state
-        over the run; returns (a samples, b samples) in seconds."""
+        plan).  Samples alternate (a b, b a, a b, ...) so both legs see the same clock / power
+        state and the same slot positions over the run; returns (a samples, b samples) in s."""
         fa()
         fb()
         self.torch.cuda.synchronize()
         ta, tb = [], []
-        for _ in range(reps):
-            ta += self.direct(fa, 1)
-            tb += self.direct(fb, 1)
+        for i in range(reps):  # ABBA order: whatever the first / second slot of a pair costs cancels
+            if i % 2 == 0:
+                ta += self.direct(fa, 1)
+                tb += self.direct(fb, 1)
+            else:
+                tb += self.direct(fb, 1)
+                ta += self.direct(fa, 1)
         return ta, tb
 
     def graph(self, fn, reps, warm=1):
