@@ -377,12 +377,17 @@ def measure(name, dev, model, a, *, steps, warmup, headline=False, sweep=True, e
         # clock / power drift between the Seer leg and the sweep cannot bias it
         kb = kernels.KERNELS.index(best)
 
+        # both legs built back to back (a fresh Seer plan -- deterministic, the same graph as
+        # `plan` -- and the best fixed kernel's constant-model plan), so neither carries the
+        # history of the sweep in between
+        sp = seer.SeerPlan(model, A, x, y, k)
         bp = seer.SeerPlan(seer.fixed_model(kb), A, x, y, k)
         # CUDA event timestamps tick in ~2 us steps on this part: a 10 us step is a few ticks,
         # so a small config gets enough alternating samples (>= ~20 ms of timed work per
         # leg) and the ratio of MEANS, which the launch-to-launch jitter dithers below the tick
         reps = int(min(400, max(max(5, steps // 2), 0.02 / max(seer_mean, 1e-6))))
-        ta, tb = T.paired(plan.launch, bp.launch, reps)
+        ta, tb = T.paired(sp.launch, bp.launch, reps)
+        sp.close()
         bp.close()
         res["speedup_vs_best_fixed"] = round(statistics.mean(tb) / statistics.mean(ta), 3)
         res["paired"] = {"seer_us_mean": round(statistics.mean(ta) * 1e6, 2),

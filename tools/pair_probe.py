@@ -43,6 +43,17 @@ kk = int(sp.outcome().kernel)
 f1 = seer.SeerPlan(seer.fixed_model(kk), A, x, y, 1)
 f2 = seer.SeerPlan(seer.fixed_model(kk), A, x, y, 1)
 print("kernel", kernels.KERNELS[kk], sp.select_kind(), f1.select_kind())
+if "--bench-like" in sys.argv:  # what bench.measure does between building the Seer plan and pairing
+    for _ in range(5):
+        kernels.spmv(A, x, kk, y=y)
+    for k2 in range(len(kernels.KERNELS)):
+        fp = seer.SeerPlan(seer.fixed_model(k2), A, x, y, 1)
+        for _ in range(5):
+            fp.launch()
+        torch.cuda.synchronize()
+        fp.close()
+    f2.close()
+    f2 = seer.SeerPlan(seer.fixed_model(kk), A, x, y, 1)
 for name, a, b in (("fixed vs fixed", f1.launch, f2.launch), ("seer vs fixed", sp.launch, f1.launch),
                    ("fixed vs seer", f1.launch, sp.launch), ("seer vs seer", sp.launch, sp.launch)):
     ma, mb = paired(a, b)
