@@ -103,6 +103,10 @@ FAVOURABLE = {
     "CSR,TM": ("band27", "band 4M x 27 (thread per short regular row)"),
     "COO,WM": ("band4", "band 32M x 4 (row-sorted COO, short rows)"),
     "ELL,TM": ("C3", "BASELINE configs[2] (ELL-favourable 27-point stencil)"),
+    # the merge-path kernels also on long regular rows (local gathers): BASELINE's C4 is
+    # merge-path-favourable for its 1 M-element rows, but its 16 M random gathers bound it
+    "CSR,MP@band2k": ("band2k", "band 65,536 x 2048 (local gathers; C4 above is the BASELINE input)"),
+    "CSR,WO@band2k": ("band2k", "band 65,536 x 2048 (local gathers; C4 above is the BASELINE input)"),
 }
 
 
@@ -428,7 +432,7 @@ def measure_favourable(dev, a, peak):
         y = torch.empty(A.n_rows, device=dev, dtype=dtype)
         T = Timer(dev)
         for kname, why in ks:
-            kk = kernels.kernel_index(kname)
+            kk = kernels.kernel_index(kname.split("@")[0])
             P = kernels.prepare(A, kk, cache=False) if kk in kernels.NEEDS_PREP else None
             kernels.spmv(A, x, kk, y=y, prepared=P)
             ts = T.direct(lambda: kernels.spmv(A, x, kk, y=y, prepared=P), 10)
