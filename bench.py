@@ -806,6 +806,35 @@ def run_sharded(a):
     exchange = a.exchange if backend == "nccl" else "host"
     run = kdist.ShardedSeer(model, A, plan, k, R, C, Z, exchange=exchange)
     kern = run.kernel
+    npdt = np.float32 if dtype == torch.float32 else np.float64
+
+    def sampled_parity():
+        """One SpMV + exchange from a random x; sampled global rows vs the fp64 oracle:
+        max |err| / (1e-5 * sum |a_ij x_j|) over the samples (<= 1 passes)."""
+        x_in = torch.rand(world * plan.r_max, dtype=torch.float64, generator=torch.Generator().manual_seed(7))
+        x_in = x_in.to(dtype).to(dev)
+        x_out = run.step(x_in, iters=1).clone()
+        xg_in = plan.unpad(x_in).double().cpu().numpy()
+        xg_out = plan.unpad(x_out).double().cpu().numpy()
+        errs = []
+        for r, c, v in samp:
+            vv = v.astype(npdt).astype(np.float64)
+            yr = float(np.dot(vv, xg_in[c]))
+            bound = 1e-5 * float(np.abs(vv * xg_in[c]).sum()) + 1e-300
+            errs.append(abs(float(xg_out[r]) - yr) / bound)
+        return max(errs)
+
+    # the fused NVLink exchange is verified on one GPU only (loopback, symmetric memory at
+    # world 1): check it on the real ranks before timing and fall back to the NCCL
+    # all-gather -- on every rank -- if any rank's sampled rows disagree
+    fallback = None
+    if run.exchange == "fused":
+        err0 = sampled_parity()
+        okt = torch.tensor([1.0 if err0 <= 1.0 else 0.0], dtype=torch.float64, device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if okt.item() < 1.0:
+            fallback = f"fused exchange failed the pre-timing sampled-row parity (max err/bound {err0:.3g}); NCCL all-gather used"
+            run = kdist.ShardedSeer(model, A, plan, k, R, C, Z, exchange="nccl", kernel=kern)
     x0 = torch.full((world * plan.r_max,), 1.0 / R, dtype=dtype, device=dev)
     sv, so = 4 if dtype == torch.float32 else 8, 4
     bytes_csr = csr_bytes(R, C, Z, sv, so)
@@ -849,18 +878,7 @@ def run_sharded(a):
         ts.append(m0.elapsed_time(m1) * 1e-3)
     clk = clocks.stop()
     # sampled-row parity of one full iteration (SpMV + exchange) vs the fp64 oracle
-    x_in = torch.rand(world * plan.r_max, dtype=torch.float64, generator=torch.Generator().manual_seed(7))
-    x_in = x_in.to(dtype).to(dev)
-    x_out = run.step(x_in, iters=1).clone()
-    xg_in = plan.unpad(x_in).double().cpu().numpy()
-    xg_out = plan.unpad(x_out).double().cpu().numpy()
-    errs = []
-    npdt = np.float32 if dtype == torch.float32 else np.float64
-    for r, c, v in samp:
-        vv = v.astype(npdt).astype(np.float64)
-        yr = float(np.dot(vv, xg_in[c]))
-        bound = 1e-5 * float(np.abs(vv * xg_in[c]).sum()) + 1e-300
-        errs.append(abs(float(xg_out[r]) - yr) / bound)
+    errs = [sampled_parity()]
     parity_ok = bool(max(errs) <= 1.0)
     if wd:
         wstat = wd.stop()
@@ -884,7 +902,7 @@ def run_sharded(a):
                        "generation_s": round(t_gen, 1)},
             "comm": {"backend": backend, "nranks": dist.get_world_size(), "exchange": run.exchange,
                      "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None,
-                     "watchdog": wstat if wd else None,
+                     "watchdog": wstat if wd else None, "exchange_fallback": fallback,
                      "note": None if backend == "nccl" else "ranks share GPUs over gloo: control flow only"},
             "seer": {"kernel": kernels.KERNELS[kern], "path": "gathered" if run.outcome.path else "known",
                      "dispatch": "global selection from the ranks' K1 partials at setup (device)",
