@@ -94,3 +94,53 @@ def test_split():
     tr, te = dataset.split_train_test(list(range(10)), 3)
     assert len(tr) == 8 and len(te) == 2 and sorted(tr + te) == list(range(10))
     assert dataset.split_train_test(list(range(10)), 3) == (tr, te)
+
+
+@pytest.mark.parametrize("kern", [0, 3, 7])
+def test_fixed_model_is_that_kernel_everywhere(kern):
+    """The constant-model plan used as the Seer-vs-fixed baseline (bench.py, eval_seer.py)
+    must take the known path and answer `kern` for any features, and its realised cost
+    must be exactly that kernel's total cost."""
+    m = seer.fixed_model(kern)
+    assert m.meta["fixed_kernel"] == seer.KERNELS[kern]
+    rng = np.random.default_rng(kern)
+    for _ in range(50):
+        r, c = int(10 ** rng.uniform(1, 8)), int(10 ** rng.uniform(1, 8))
+        nnz, k = int(10 ** rng.uniform(1, 9)), int(rng.choice([1, 10, 100]))
+        o = seer.infer_features(m, (r, c, nnz), k, (1.0, 0.5, 2.0, 0.01))
+        assert (o.chosen_kernel, o.path) == (kern, seer.USE_KNOWN)
+    row = DatasetRow("f", (100, 100, 500), (0.1, 0.0, 0.05, 0.001), 10.0,
+                     [1e-3 * (i + 1) for i in range(8)], [1e-4 * i for i in range(8)])
+    for k in (1, 10, 100):
+        assert seer.realized_cost(m, row, k)[0] == pytest.approx(row.cost(kern, k))
+
+
+def test_lofo_realise_on_corpus_subset():
+    """tools/lofo_seer.py's realisation on a small slice of the committed corpus: the
+    selector can never beat the per-matrix oracle, and the frozen bundle's per-family
+    numbers are well formed."""
+    import importlib.util
+    import os
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    tools = os.path.join(root, "tools")
+    import sys
+    sys.path.insert(0, tools)
+    spec = importlib.util.spec_from_file_location("lofo_seer", os.path.join(tools, "lofo_seer.py"))
+    lofo = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(lofo)
+    rows = lofo.load(os.path.join(root, "paper_2403_17017_b200", "models", "corpus"))
+    fams = {}
+    for r in rows:
+        fams.setdefault(lofo.family(r.name), []).append(r)
+    assert len(fams) >= 5
+    frozen = seer.SeerModel.load(os.path.join(root, "paper_2403_17017_b200", "models", "seer_b200.json"))
+    held_f = sorted(fams)[0]
+    held = fams[held_f][:40]
+    train = [r for f, rs in fams.items() if f != held_f for r in rs[:40]]
+    m = seer.train_seer(train, (1, 10), 3, 4, seer.KERNELS)
+    for model in (m, frozen):
+        for k in (1, 10):
+            res = lofo.realise(model, held, k)
+            assert res["selector_over_oracle"] >= 1.0 - 1e-12
+            assert res["oracle_total_s"] <= res["best_fixed_total_s"] * (1 + 1e-12)
+            assert res["best_fixed"] in seer.KERNELS and res["aggregate_vs_best_fixed"] > 0
