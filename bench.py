@@ -804,7 +804,10 @@ def run_sharded(a):
     t_gen = time.time() - t0
     model, model_src = _load_model()
     exchange = a.exchange if backend == "nccl" else "host"
+    t0 = time.time()
     run = kdist.ShardedSeer(model, A, plan, k, R, C, Z, exchange=exchange)
+    torch.cuda.synchronize()
+    t_setup = time.time() - t0  # selection + column blocking + exchange rendezvous (once)
     kern = run.kernel
     npdt = np.float32 if dtype == torch.float32 else np.float64
 
@@ -865,17 +868,24 @@ def run_sharded(a):
         tt = tt.to(dev)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     total = float(tt.item())
-    # this rank's SpMV alone (dominant kernel) for the roofline
+    # this rank's SpMV alone (dominant kernel: the column-blocked local SpMV, no exchange)
+    # for the roofline, and the same SpMV unblocked for comparison
+    Ps = run.prepare()
     P = kernels.prepare(A, kern) if kern in kernels.NEEDS_PREP else None
-    ys = torch.empty(plan.local_rows, dtype=dtype, device=dev)
-    ts = []
-    for _ in range(5):
-        m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        m0.record()
-        kernels.spmv(A, run.bufs[0], kern, y=ys, prepared=P)
-        m1.record()
-        m1.synchronize()
-        ts.append(m0.elapsed_time(m1) * 1e-3)
+    ys = torch.empty(max(1, plan.local_rows), dtype=dtype, device=dev)
+
+    def _evt(fn, n=5):
+        out = []
+        for _ in range(n):
+            m0, m1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            m0.record()
+            fn()
+            m1.record()
+            m1.synchronize()
+            out.append(m0.elapsed_time(m1) * 1e-3)
+        return out
+    ts = _evt(lambda: run.spmv_into(run.bufs[0], [ys], 0, Ps))
+    ts_unblocked = _evt(lambda: kernels.spmv(A, run.bufs[0], kern, y=ys, prepared=P)) if run.col_slices > 1 else ts
     clk = clocks.stop()
     # sampled-row parity of one full iteration (SpMV + exchange) vs the fp64 oracle
     errs = [sampled_parity()]
@@ -899,10 +909,11 @@ def run_sharded(a):
                        "parallelism": f"row-sharded x{world} (nnz-balanced, y exchanged every iteration)",
                        "l2": "inputs larger than L2 (A: %.1f GB)" % (bytes_csr / 1e9), "model": model_src,
                        "byte_model": "nnz*(4+sv)+(R+1)*so+C*sv+R*sv per iteration, x counted once",
-                       "generation_s": round(t_gen, 1)},
+                       "generation_s": round(t_gen, 1), "setup_s": round(t_setup, 2)},
             "comm": {"backend": backend, "nranks": dist.get_world_size(), "exchange": run.exchange,
                      "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None,
                      "watchdog": wstat if wd else None, "exchange_fallback": fallback,
+                     "col_slices": run.col_slices,
                      "note": None if backend == "nccl" else "ranks share GPUs over gloo: control flow only"},
             "seer": {"kernel": kernels.KERNELS[kern], "path": "gathered" if run.outcome.path else "known",
                      "dispatch": "global selection from the ranks' K1 partials at setup (device)",
@@ -915,7 +926,9 @@ def run_sharded(a):
             "roofline": {"bound": "hbm", "achieved": round(kb / per / 1e9, 1), "peak": peak, "unit": "GB/s",
                          "frac": round(kb / per / 1e9 / peak, 4), "traffic": None, "kernel": kernels.KERNELS[kern],
                          "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
-                         "note": "rank 0's local SpMV"},
+                         "col_slices": run.col_slices, "ms": round(per * 1e3, 3),
+                         "unblocked_ms": round(statistics.median(ts_unblocked) * 1e3, 3),
+                         "note": "rank 0's local SpMV (column-blocked when col_slices > 1: x slices L2-resident)"},
             "e2e": None, "gpu_launches": int(launches), "cpu_baseline": None, "clocks": clk,
         }), flush=True)
     dist.destroy_process_group()

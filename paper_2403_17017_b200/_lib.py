@@ -27,7 +27,7 @@ EXPORTS = (
     "kp_tree_predict", "kp_seer_select", "kp_prepare_bytes", "kp_prepare",
     "kp_spmv_workspace_bytes", "kp_spmv", "kp_seer_plan_bytes", "kp_seer_plan_create", "kp_seer_plan_launch",
     "kp_seer_plan_destroy", "kp_shard_partition", "kp_version", "kp_launch_count", "kp_debug_set_wave_warps",
-    "kp_seer_select_partials", "kp_coo_workspace_bytes", "kp_csr_from_coo", "kp_spmv_bcast",
+    "kp_seer_select_partials", "kp_coo_workspace_bytes", "kp_csr_from_coo", "kp_spmv_bcast", "kp_spmv_bcast_acc",
     "kp_mm_header", "kp_mm_parse", "kp_watchdog_start", "kp_watchdog_heartbeat", "kp_watchdog_status",
     "kp_watchdog_stop", "kp_seer_plan_select_kind", "kp_seer_emitted_predict", "kp_seer_emitted_sha256",
     "kp_pack_bits", "kp_pack_cols_bytes", "kp_pack_cols", "kp_unpack_cols",
@@ -117,6 +117,7 @@ def load(require: bool = True):
         "kp_coo_workspace_bytes": (ctypes.c_int, [i64, i64, i64, P(sz)]),
         "kp_csr_from_coo": (ctypes.c_int, [i64, i64, p, p, p, i64, p, p, p, p, p, sz, p]),
         "kp_spmv_bcast": (ctypes.c_int, [i32, P(kp_csr), P(kp_prepared), p, P(kp_peers), p, sz, p]),
+        "kp_spmv_bcast_acc": (ctypes.c_int, [i32, P(kp_csr), P(kp_prepared), p, p, P(kp_peers), p, sz, p]),
         "kp_mm_header": (ctypes.c_int, [ctypes.c_char_p, sz, P(kp_mm_info)]),
         "kp_mm_parse": (ctypes.c_int, [ctypes.c_char_p, sz, p, p, p, i64, i32, P(kp_mm_info)]),
         "kp_watchdog_start": (ctypes.c_int, [p, i64, i64, P(p)]),

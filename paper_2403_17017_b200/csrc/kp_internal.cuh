@@ -60,7 +60,33 @@ int launch_plan_select(const void *d_off, int32_t off_type, int64_t n_rows, int6
 // ----------------------------------------------------------------- load helpers
 
 // Streamed (read-once) data: non-coherent path, do not allocate in L1 so the x
-// gathers keep the L1.
+// gathers keep the L1.  KP_STREAM_L2_EF (A/B): also mark the lines evict-first in L2 so
+// the streams do not push the x gathers' lines out.
+#ifndef KP_STREAM_L2_EF
+#define KP_STREAM_L2_EF 0
+#endif
+#if KP_STREAM_L2_EF
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ int32_t ld_stream(const int32_t *p) {
+    int32_t v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.b32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(l2_evict_first_policy()));
+    return v;
+}
+__device__ __forceinline__ float ld_stream(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(l2_evict_first_policy()));
+    return v;
+}
+__device__ __forceinline__ double ld_stream(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_evict_first_policy()));
+    return v;
+}
+#else
 __device__ __forceinline__ int32_t ld_stream(const int32_t *p) {
     int32_t v;
     asm volatile("ld.global.nc.L1::no_allocate.b32 %0, [%1];" : "=r"(v) : "l"(p));
@@ -76,6 +102,7 @@ __device__ __forceinline__ double ld_stream(const double *p) {
     asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
     return v;
 }
+#endif
 __device__ __forceinline__ int64_t ld_stream(const int64_t *p) {
     int64_t v;
     asm volatile("ld.global.nc.L1::no_allocate.s64 %0, [%1];" : "=l"(v) : "l"(p));
@@ -97,8 +124,29 @@ __device__ __forceinline__ void prefetch_l2(const void *p) {
     asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
 }
 // x gathers: read-only path, L1-allocating (reuse across rows / lanes).
+#ifndef KP_X_L2_EL
+#define KP_X_L2_EL 0
+#endif
+#if KP_X_L2_EL  // A/B: x gathers marked evict-last in L2
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
+__device__ __forceinline__ float ld_x(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(l2_evict_last_policy()));
+    return v;
+}
+__device__ __forceinline__ double ld_x(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_evict_last_policy()));
+    return v;
+}
+#else
 template <typename T>
 __device__ __forceinline__ T ld_x(const T *p) { return __ldg(p); }
+#endif
 
 // ----------------------------------------------------------------- warp helpers
 template <int G, typename T>

@@ -88,6 +88,11 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cu
 template <typename V>
 struct YDst {
     V *y[KP_MAX_PEERS];
+    // column-blocked accumulation (kp_spmv_bcast_acc): the merge kernel's row stores add
+    // acc[r] (null: none).  Each row is stored exactly once there (by the unit holding its
+    // end), so acc is added once; the fix-up then adds carries onto y[self] as usual.
+    // acc may alias y[self]: the same thread reads acc[r] before it stores y[.][r].
+    const V *acc;
     int32_t n, self;
     __device__ __forceinline__ void put(int64_t i, V v) const {
         // fully unrolled with a predicate: a dynamic index into this by-value parameter
@@ -971,8 +976,11 @@ constexpr int kMergeIPT = sizeof(V) == 8 ? KP_MERGE_IPT64 : kIPT;
 #ifndef KP_MERGE_LATE_F64
 #define KP_MERGE_LATE_F64 1
 #endif
+#ifndef KP_MERGE_MINB_F32B
+#define KP_MERGE_MINB_F32B 3
+#endif
 template <typename V, bool kB = false>
-constexpr int kMergeMinBlocks = sizeof(V) == 4 ? (kB ? 0 : KP_MERGE_MINB_F32) : KP_MERGE_MINB_F64;
+constexpr int kMergeMinBlocks = sizeof(V) == 4 ? (kB ? KP_MERGE_MINB_F32B : KP_MERGE_MINB_F32) : KP_MERGE_MINB_F64;
 constexpr int kMergeWarps = 8;        // warps per CTA
 
 // Persistent merge-path warps (Merrill & Garland, restructured for B200).  The merge of
@@ -1064,7 +1072,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
         }
     };
     auto store_y = [&](int64_t r, V v) {
-        if constexpr (kB) dst.put(r, v);
+        if constexpr (kB) dst.put(r, dst.acc ? v + dst.acc[r] : v);
         else y[r] = v;
     };
     // Row-end probe of the unit [d0, d1) starting at row rs (rows before rs are finished):
@@ -2056,7 +2064,7 @@ int launch_long_rows(int32_t kernel, const kp_csr *A, DeferWs *dw, const O *off,
 
 template <typename V, typename O>
 int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V *y, unsigned char *ws,
-           cudaStream_t s, const kp_peers *peers = nullptr) {
+           cudaStream_t s, const kp_peers *peers = nullptr, const V *acc = nullptr) {
     const O *off = reinterpret_cast<const O *>(A->row_offsets);
     const int32_t *col = A->col_indices;
     const V *val = reinterpret_cast<const V *>(A->values);
@@ -2177,6 +2185,7 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
                 for (int p = 0; p < peers->n; ++p) d.y[p] = reinterpret_cast<V *>(peers->y[p]);
                 d.n = peers->n;
                 d.self = peers->self;
+                d.acc = acc;
                 const int64_t *part = nullptr;
                 if (kernel == KP_CSR_MP) {
                     if (!P || !P->buf) return KP_EINVAL;
@@ -2333,6 +2342,11 @@ int64_t kp_debug_set_wave_warps(int64_t warps) {
 
 int kp_spmv_bcast(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x, const kp_peers *peers,
                   void *d_ws, size_t ws_bytes, void *stream) {
+    return kp_spmv_bcast_acc(kernel, A, P, d_x, nullptr, peers, d_ws, ws_bytes, stream);
+}
+
+int kp_spmv_bcast_acc(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x, const void *d_acc,
+                      const kp_peers *peers, void *d_ws, size_t ws_bytes, void *stream) {
     KP_NVTX("kp_spmv_bcast");
     if (!valid_csr(A) || !peers || peers->n < 1 || peers->n > KP_MAX_PEERS || peers->self < 0 ||
         peers->self >= peers->n || (kernel != KP_CSR_MP && kernel != KP_CSR_WO) || (A->n_cols > 0 && !d_x))
@@ -2345,17 +2359,25 @@ int kp_spmv_bcast(int32_t kernel, const kp_csr *A, const kp_prepared *P, const v
     if (P && P->buf && P->kernel != kernel) return KP_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     if (A->n_rows == 0) return KP_OK;
-    if (A->nnz == 0) {
-        for (int p = 0; p < peers->n; ++p)
-            KP_CUDA_TRY(cudaMemsetAsync(peers->y[p], 0, (size_t)A->n_rows * val_bytes(A), s));
+    const size_t yb = (size_t)A->n_rows * val_bytes(A);
+    if (A->nnz == 0) {  // y = acc (or 0) everywhere
+        for (int p = 0; p < peers->n; ++p) {
+            if (!d_acc) KP_CUDA_TRY(cudaMemsetAsync(peers->y[p], 0, yb, s));
+            else if (peers->y[p] != d_acc) KP_CUDA_TRY(cudaMemcpyAsync(peers->y[p], d_acc, yb, cudaMemcpyDefault, s));
+        }
         return KP_OK;
     }
     unsigned char *ws = reinterpret_cast<unsigned char *>(d_ws);
-    if (A->val_type == KP_F32)
-        return A->off_type == KP_I32 ? spmv_t<float, int32_t>(kernel, A, P, (const float *)d_x, nullptr, ws, s, peers)
-                                     : spmv_t<float, int64_t>(kernel, A, P, (const float *)d_x, nullptr, ws, s, peers);
-    return A->off_type == KP_I32 ? spmv_t<double, int32_t>(kernel, A, P, (const double *)d_x, nullptr, ws, s, peers)
-                                 : spmv_t<double, int64_t>(kernel, A, P, (const double *)d_x, nullptr, ws, s, peers);
+    if (A->val_type == KP_F32) {
+        const float *acc = (const float *)d_acc;
+        return A->off_type == KP_I32
+                   ? spmv_t<float, int32_t>(kernel, A, P, (const float *)d_x, nullptr, ws, s, peers, acc)
+                   : spmv_t<float, int64_t>(kernel, A, P, (const float *)d_x, nullptr, ws, s, peers, acc);
+    }
+    const double *acc = (const double *)d_acc;
+    return A->off_type == KP_I32
+               ? spmv_t<double, int32_t>(kernel, A, P, (const double *)d_x, nullptr, ws, s, peers, acc)
+               : spmv_t<double, int64_t>(kernel, A, P, (const double *)d_x, nullptr, ws, s, peers, acc);
 }
 
 int kp_shard_partition(const void *d_off, int32_t off_type, int64_t n_rows, int32_t parts, int64_t *d_cuts,

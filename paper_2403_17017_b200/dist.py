@@ -128,6 +128,67 @@ def all_gather_slices(buf, plan: ShardPlan, group=None) -> None:
         buf.copy_(host)
 
 
+# ---------------------------------------------------------------------- column blocking
+# A rank's SpMV gathers x over the WHOLE padded x (C5: 64M fp32 = 268 MB, twice the 126 MB
+# L2): on R-MAT every gather misses, and ncu counts 6.4x the algorithmic DRAM bytes
+# (profiles/ncu_C5_r01.md).  Column blocking keeps each gather window L2-resident: the
+# block is split once, at shard time, into S column slices A_0..A_{S-1} (each a CSR over
+# the same rows), and an iteration is y = A_0 x + ... + A_{S-1} x, accumulated slice by
+# slice in the merge kernel's own row stores (kp_spmv_bcast_acc; the last slice's stores
+# are the exchange).  Cost: S passes over the row bookkeeping (offsets, row ends) and
+# S - 1 reads of the accumulator.  Per-rank SpMV of C5 (profiles/shard_scaling_r02.json,
+# rank-emulated on one GPU): P = 1 10.20 -> 6.16 ms at S = 2 (6.16 at S = 3, 6.80 at 4);
+# P = 8 1.34 -> 0.88 ms at S = 2 (0.92 at 3, 1.04 at 4).  Two slices of 134 MB each beat
+# three that fit the 126 MB L2: R-MAT's gathers are skewed, so a slice's hot lines stay
+# resident while each extra slice costs a pass over the row bookkeeping.
+COL_SLICE_L2_FRACTION = 1.25  # an x slice may be this multiple of the L2 (measured sweep)
+MAX_COL_SLICES = 8
+
+
+def auto_col_slices(x_bytes: int, l2_bytes: int) -> int:
+    """Slices so that one x slice fits in COL_SLICE_L2_FRACTION of the L2 (1: no blocking)."""
+    budget = max(1, int(COL_SLICE_L2_FRACTION * l2_bytes))
+    return int(min(MAX_COL_SLICES, max(1, -(-int(x_bytes) // budget))))
+
+
+def col_slice_bounds(n_cols: int, slices: int) -> list:
+    """Equal-width column ranges [b_s, b_{s+1}) over the (padded) x."""
+    if slices < 1:
+        raise ValueError("slices must be >= 1")
+    return [(int(n_cols) * s) // slices for s in range(slices + 1)]
+
+
+def split_columns(row_offsets, col_indices, values, lo: int, hi: int):
+    """The entries of a CSR with lo <= col < hi, as a CSR over the same rows (int64
+    offsets; entry order within each row kept).  Torch tensors on any device."""
+    import torch
+    off = row_offsets.to(torch.int64)
+    n_rows = off.numel() - 1
+    keep = (col_indices >= lo) & (col_indices < hi)
+    idx = torch.nonzero(keep).squeeze(1)
+    del keep
+    rows = torch.searchsorted(off, idx, right=True) - 1
+    cnt = torch.bincount(rows, minlength=n_rows)
+    del rows
+    out = torch.zeros(n_rows + 1, dtype=torch.int64, device=off.device)
+    if n_rows:
+        torch.cumsum(cnt, 0, out=out[1:])
+    return out, col_indices[idx], values[idx]
+
+
+def column_blocks(A, slices: int):
+    """DeviceCSR -> ``slices`` DeviceCSRs (same rows and n_cols), one per column range."""
+    import torch
+    from .device import DeviceCSR
+    out = []
+    b = col_slice_bounds(A.n_cols, slices)
+    for s in range(slices):
+        o, c, v = split_columns(A.row_offsets, A.col_indices, A.values, b[s], b[s + 1])
+        o = o.to(torch.int32) if int(o[-1]) < 2**31 - 1 else o
+        out.append(DeviceCSR(A.n_rows, A.n_cols, o, c, v))
+    return out
+
+
 class Watchdog:
     """Failure detection for the NCCL path: ``kp_watchdog_*`` polls
     ncclCommGetAsyncError on this rank's communicator and a heartbeat the host sends every
@@ -264,7 +325,7 @@ class ShardedSeer:
     slice of the next x, in-place NCCL all-gather of the slices over NVLink)."""
 
     def __init__(self, model, A, plan: ShardPlan, k: int, n_rows: int, n_cols: int, nnz: int, group=None,
-                 exchange: str = "auto", kernel=None):
+                 exchange: str = "auto", kernel=None, col_slices="auto"):
         import torch
         from . import kernels
         from .features import decode_outcome
@@ -295,6 +356,19 @@ class ShardedSeer:
                 self.fused_error = repr(exc)
         if self.exchange in ("nccl", "host"):
             self.bufs = [torch.zeros(plan.world * plan.r_max, dtype=dt, device=A.device) for _ in range(2)]
+        # column blocking (merge-path kernels: the accumulating store is theirs); "auto" =
+        # when the padded x exceeds the L2 budget, env KP_COL_SLICES overrides
+        import os
+        S = os.environ.get("KP_COL_SLICES", col_slices)
+        if S == "auto":
+            l2 = int(getattr(torch.cuda.get_device_properties(A.device), "L2_cache_size", 0) or 126 << 20)
+            S = auto_col_slices(plan.world * plan.r_max * A.values.element_size(), l2)
+        S = int(S)
+        if S < 1:
+            raise ValueError("col_slices must be >= 1")
+        self.col_slices = S if self.kernel in (kernels.CSR_MP, kernels.CSR_WO) and A.nnz > 0 else 1
+        self.blocks = column_blocks(A, self.col_slices) if self.col_slices > 1 else [A]
+        self.acc = torch.empty(max(1, plan.local_rows), dtype=dt, device=A.device) if self.col_slices > 1 else None
 
     def _setup_fused(self, dt):
         import torch
@@ -314,6 +388,30 @@ class ShardedSeer:
                        for q in range(p.world)] for h in self.hdl]
         self.hdl[0].barrier(channel=0)
 
+    def prepare(self):
+        """The chosen kernel's preprocessing of every column block (None: needs none)."""
+        K = self._kernels
+        return [K.prepare(B, self.kernel, cache=False) if self.kernel in K.NEEDS_PREP else None for B in self.blocks]
+
+    def spmv_into(self, x, dests, self_index: int, Ps) -> None:
+        """This rank's y = A x stored into ``dests`` (``dests[self_index]`` the local copy).
+        Column-blocked: the blocks accumulate into self.acc, the last block's stores (acc +
+        its part) go to the destinations.  Unblocked non-merge kernels: kp_spmv."""
+        K = self._kernels
+        if len(self.blocks) == 1 and self.kernel not in (K.CSR_MP, K.CSR_WO):
+            K.spmv(self.A, x, self.kernel, y=dests[self_index], prepared=Ps[0])
+            for i, d in enumerate(dests):
+                if i != self_index:
+                    d.copy_(dests[self_index])
+            return
+        for s_, (B, Pb) in enumerate(zip(self.blocks[:-1], Ps[:-1])):
+            if s_ == 0:  # the first block has nothing to add: the plain kernel (kp_spmv)
+                K.spmv(B, x, self.kernel, y=self.acc, prepared=Pb)
+            else:
+                K.spmv_bcast(B, x, self.kernel, [self.acc], 0, prepared=Pb, acc=self.acc)
+        K.spmv_bcast(self.blocks[-1], x, self.kernel, dests, self_index, prepared=Ps[-1],
+                     acc=self.acc if len(self.blocks) > 1 else None)
+
     def _slice(self, buf):
         p = self.plan
         return buf[p.rank * p.r_max: p.rank * p.r_max + p.local_rows]
@@ -326,8 +424,9 @@ class ShardedSeer:
         k = self.k if iters is None else int(iters)
         if x_pad is not None:
             self.bufs[0].copy_(x_pad)
-        P = K.prepare(self.A, self.kernel, cache=False) if self.kernel in K.NEEDS_PREP else None
+        Ps = self.prepare()
         cur = 0
+        spmv_into = lambda x, dests, i: self.spmv_into(x, dests, i, Ps)  # noqa: E731
         if self.exchange == "fused":
             if x_pad is not None:
                 self.hdl[0].barrier(channel=0)  # every rank's buffer 0 holds x before anyone reads
@@ -335,13 +434,16 @@ class ShardedSeer:
                 nxt = 1 - cur
                 # y -> every rank's next-x slice from the kernel epilogue; the barrier orders
                 # all ranks' stores before the next iteration's reads (and frees buffer cur)
-                K.spmv_bcast(self.A, self.bufs[cur], self.kernel, self.dests[nxt], p.rank, prepared=P)
+                spmv_into(self.bufs[cur], self.dests[nxt], p.rank)
                 self.hdl[nxt].barrier(channel=0)
                 cur = nxt
             return self.bufs[cur]
         for _ in range(k):
             nxt = 1 - cur
-            K.spmv(self.A, self.bufs[cur], self.kernel, y=self._slice(self.bufs[nxt]), prepared=P)
+            if len(self.blocks) > 1:
+                spmv_into(self.bufs[cur], [self._slice(self.bufs[nxt])], 0)
+            else:  # unblocked: plain kp_spmv (every kernel)
+                K.spmv(self.A, self.bufs[cur], self.kernel, y=self._slice(self.bufs[nxt]), prepared=Ps[0])
             all_gather_slices(self.bufs[nxt], p, self.group)
             cur = nxt
         return self.bufs[cur]

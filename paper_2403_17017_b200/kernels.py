@@ -144,10 +144,13 @@ def check_vector(v, A, n: int, name: str, out: bool = False) -> None:
                          f"{v.dtype} on {v.device})")
 
 
-def spmv_bcast(A, x, kernel, dests, self_index: int, *, prepared: Prepared | None = None, stream=None):
+def spmv_bcast(A, x, kernel, dests, self_index: int, *, prepared: Prepared | None = None, stream=None,
+               acc=None):
     """kp_spmv_bcast: y = A.x written from the kernel's own epilogue into every tensor of
     ``dests`` (this rank's slice of each rank's next-x buffer; peer-mapped symmetric memory
-    or local tensors), ``dests[self_index]`` being the local copy.  Merge-path kernels only."""
+    or local tensors), ``dests[self_index]`` being the local copy.  Merge-path kernels only.
+    ``acc`` (n_rows elements, may be ``dests[self_index]``): y = acc + A.x instead
+    (kp_spmv_bcast_acc, the column-blocked iteration of dist.ShardedSeer)."""
     torch = _lib.require_cuda()
     A = as_device(A)
     k = kernel_index(kernel)
@@ -161,6 +164,9 @@ def spmv_bcast(A, x, kernel, dests, self_index: int, *, prepared: Prepared | Non
             raise ValueError("each destination needs n_rows contiguous elements of the matrix value dtype")
     if k in NEEDS_PREP and prepared is None:
         prepared = prepare(A, k, stream=stream)
+    if acc is not None and (acc.dtype != A.values.dtype or acc.numel() < A.n_rows or not acc.is_contiguous()
+                            or not acc.is_cuda):
+        raise ValueError("acc needs n_rows contiguous elements of the matrix value dtype")
     pe = _lib.kp_peers()
     for i, d in enumerate(dests):
         pe.y[i] = d.data_ptr()
@@ -168,6 +174,8 @@ def spmv_bcast(A, x, kernel, dests, self_index: int, *, prepared: Prepared | Non
     ws = spmv_workspace(A, k, stream)
     P = ctypes.byref(prepared.struct) if prepared is not None else None
     with torch.cuda.device(A.device):
-        _lib.check(_lib.load().kp_spmv_bcast(k, ctypes.byref(A.struct), P, x.data_ptr(), ctypes.byref(pe),
-                                             0 if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
-                                             _lib.stream_handle(stream, A.device)), f"kp_spmv_bcast[{KERNELS[k]}]")
+        _lib.check(_lib.load().kp_spmv_bcast_acc(k, ctypes.byref(A.struct), P, x.data_ptr(),
+                                                 0 if acc is None else acc.data_ptr(), ctypes.byref(pe),
+                                                 0 if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
+                                                 _lib.stream_handle(stream, A.device)),
+                   f"kp_spmv_bcast_acc[{KERNELS[k]}]")

@@ -203,3 +203,120 @@ def test_nccl_watchdog_heartbeat_and_timeout():
     p = subprocess.run([sys.executable, "-c", _WD_SCRIPT, root], capture_output=True, text=True, timeout=300)
     assert "OK_STATE ok" in p.stdout, (p.stdout, p.stderr[-2000:])
     assert "TIMEOUT_RAISED" in p.stdout and "FINAL timeout" in p.stdout, (p.stdout, p.stderr[-2000:])
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("kern", [kernels.CSR_WO, kernels.CSR_MP])
+@pytest.mark.parametrize("mode", ["none", "separate", "alias"])
+def test_bcast_acc_matches_oracle(dtype, kern, mode, orc):
+    """kp_spmv_bcast_acc: every destination receives acc + A.x; acc may be the self
+    destination itself (the in-place accumulation of the column blocks)."""
+    from paper_2403_17017_b200 import _lib
+    L = _lib.load()
+    prev = L.kp_debug_set_wave_warps(7)  # range-end carries: the fix-up must not re-add acc
+    try:
+        m = gen.config("C5", small=True, device="cuda")
+        A = m.to_device_csr(dtype)
+        off, col, val = m.numpy()
+        rng = np.random.default_rng(3)
+        x = rng.uniform(0, 1, m.n_cols)
+        a0 = rng.normal(size=m.n_rows)
+        vv = val.astype(np.float32).astype(np.float64) if dtype == torch.float32 else val
+        yref, absy = orc.spmv_csr(off, col.astype(np.int32), vv, x.astype(np.float32).astype(np.float64)
+                                  if dtype == torch.float32 else x)
+        xd = torch.from_numpy(x).to(dtype).cuda()
+        dests = [torch.full((m.n_rows,), float("nan"), dtype=dtype, device="cuda") for _ in range(3)]
+        acc = None
+        if mode != "none":
+            a0 = torch.from_numpy(a0).to(dtype).double().numpy()
+            if mode == "alias":
+                dests[1].copy_(torch.from_numpy(a0))
+                acc = dests[1]
+            else:
+                acc = torch.from_numpy(a0).to(dtype).cuda()
+            yref, absy = yref + a0, absy + np.abs(a0)
+        kernels.spmv_bcast(A, xd, kern, dests, 1, acc=acc)
+        torch.cuda.synchronize()
+        tol = 1e-5 if dtype == torch.float32 else 1e-12
+        for q, d in enumerate(dests):
+            ok, r = orc.spmv_check(d.double().cpu().numpy(), yref, absy, tol)
+            assert ok, (q, mode, r)
+    finally:
+        L.kp_debug_set_wave_warps(prev)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+@pytest.mark.parametrize("S", [2, 3, 5])
+def test_column_blocks_loopback_matches_oracle(world, S, orc):
+    """Column-blocked row shards (dist.column_blocks + accumulating stores, the last block's
+    stores to every rank's next-x buffer), `world` simulated ranks on one GPU."""
+    m = gen.config("C5", small=True, device="cuda")
+    off, col, val = m.numpy()
+    x = np.random.default_rng(13).uniform(0, 1, m.n_cols)
+    yref, absy = orc.spmv_csr(off, col.astype(np.int32), val, x)
+    shards = [kdist.shard_device(m.row_offsets, m.col_indices, m.values, m.n_cols, r, world, torch.float64)
+              for r in range(world)]
+    plan0 = shards[0][1]
+    n = world * plan0.r_max
+    nxt = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(world)]
+    for r, (A, plan, _) in enumerate(shards):
+        blocks = kdist.column_blocks(A, S)
+        assert sum(B.nnz for B in blocks) == A.nnz
+        xp = plan.pad(torch.from_numpy(x).cuda())
+        acc = torch.empty(plan.local_rows, dtype=torch.float64, device="cuda")
+        for s, B in enumerate(blocks[:-1]):
+            kernels.spmv_bcast(B, xp, kernels.CSR_WO, [acc], 0, acc=acc if s else None)
+        dests = [nxt[q][r * plan.r_max: r * plan.r_max + plan.local_rows] for q in range(world)]
+        kernels.spmv_bcast(blocks[-1], xp, kernels.CSR_MP, dests, r, acc=acc)
+    torch.cuda.synchronize()
+    for q in range(world):
+        ok, ratio = orc.spmv_check(plan0.unpad(nxt[q]).cpu().numpy(), yref, absy, 1e-12)
+        assert ok, (world, S, q, ratio)
+
+
+@pytest.mark.parametrize("S", [1, 3, 4])
+@pytest.mark.parametrize("kern", [kernels.CSR_WO, kernels.CSR_MP])
+def test_sharded_seer_column_blocked_power_iteration(S, kern, orc):
+    """ShardedSeer(col_slices=S) at world 1 (no process group: local exchange) == the
+    oracle's power iteration; S = 1 is the unblocked path."""
+    m = gen.config("C5", small=True, device="cuda")
+    A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, m.n_cols, 0, 1, torch.float64)
+    run = kdist.ShardedSeer(_model(), A, plan, 3, m.n_rows, m.n_cols, m.nnz, kernel=kern, col_slices=S)
+    assert run.col_slices == S and len(run.blocks) == S
+    x0 = torch.full((m.n_rows,), 1.0 / m.n_rows, dtype=torch.float64, device="cuda")
+    got = run.step(x0).cpu().numpy()
+    off, col, val = m.numpy()
+    ref = x0.cpu().numpy()
+    for _ in range(3):
+        ref, _ = orc.spmv_csr(off, col.astype(np.int32), val, ref)
+    assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+
+
+def test_sharded_seer_column_blocked_fused_world1(orc):
+    """Column blocks + the fused symmetric-memory exchange (world 1), fp32 at 1e-5."""
+    import socket
+    import torch.distributed as tdist
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    tdist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                             device_id=torch.device("cuda", 0))
+    try:
+        m = gen.config("C5", small=True, device="cuda")
+        A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, m.n_cols, 0, 1, torch.float32)
+        run = kdist.ShardedSeer(_model(), A, plan, 2, m.n_rows, m.n_cols, m.nnz, exchange="fused",
+                                kernel=kernels.CSR_WO, col_slices=3)
+        assert run.exchange == "fused" and run.col_slices == 3
+        x0 = torch.rand(m.n_rows, dtype=torch.float32, device="cuda")
+        got = run.step(x0).double().cpu().numpy()
+        off, col, val = m.numpy()
+        v32 = val.astype(np.float32).astype(np.float64)
+        ref = x0.double().cpu().numpy()
+        y1, _ = orc.spmv_csr(off, col.astype(np.int32), v32, ref)
+        y1 = y1.astype(np.float32).astype(np.float64)
+        y2, absy = orc.spmv_csr(off, col.astype(np.int32), v32, y1)
+        ok, ratio = orc.spmv_check(got, y2, absy, 2e-5)
+        assert ok, ratio
+    finally:
+        tdist.destroy_process_group()

@@ -1,7 +1,9 @@
 """Strong-scaling projection of the row-sharded C5 SpMV on ONE GPU (this round has 1 GPU):
 for P = 1, 2, 4, 8 the matrix is cut exactly as `dist.shard_device` cuts it for P ranks,
 and every rank's local SpMV (the chosen kernel, rank-padded x) is timed in turn; the
-step time of P GPUs is bounded below by the slowest rank.  Reports per-P max / mean rank
+step time of P GPUs is bounded below by the slowest rank.  Each rank's SpMV runs as
+dist.ShardedSeer runs it (column blocks when its x exceeds the L2 budget; --col-slices
+lists the settings to time, the last one is the headline).  Reports per-P max / mean rank
 time, the compute-only speedup t(1) / max_p t_p(P), and the bytes each rank must push per
 iteration in the y exchange (fused into the SpMV epilogue over NVLink, kp_spmv_bcast).
 
@@ -28,6 +30,8 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default=None)
     ap.add_argument("--bcast", action="store_true", help="only measure the fused-exchange epilogue cost")
+    ap.add_argument("--col-slices", default="1,auto",
+                    help="column blocking of each rank's SpMV (dist.ShardedSeer col_slices), comma list")
     a = ap.parse_args()
     if a.bcast:
         bcast_overhead()
@@ -37,32 +41,41 @@ def main():
     R, C, Z = m.n_rows, m.n_cols, m.nnz
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
     res = {"matrix": "C5 R-MAT s26 ef16", "rows": R, "nnz": Z, "kernel": a.kernel, "parts": {}}
+    slices = a.col_slices.split(",")
     for P in [int(v) for v in a.parts.split(",")]:
-        times, nnzs = [], []
+        times = {S: [] for S in slices}
+        nnzs, used = [], {}
         for rank in range(P):
             A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, C, rank, P, torch.float32)
             x = torch.rand(P * plan.r_max, device="cuda", dtype=torch.float32)
             y = torch.empty(plan.local_rows, device="cuda", dtype=torch.float32)
-            Pp = kernels.prepare(A, kern) if kern in kernels.NEEDS_PREP else None
-            kernels.spmv(A, x, kern, y=y, prepared=Pp)
-            ts = []
-            for _ in range(a.reps):
-                flush.zero_()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record()
-                kernels.spmv(A, x, kern, y=y, prepared=Pp)
-                e1.record()
-                e1.synchronize()
-                ts.append(e0.elapsed_time(e1) * 1e-3)
-            times.append(statistics.median(ts))
+            for S in slices:
+                # the rank's local SpMV exactly as ShardedSeer runs it (column blocks and all)
+                run = kdist.ShardedSeer(None, A, plan, 1, R, C, Z, exchange="nccl", kernel=kern, col_slices=S)
+                used[S] = run.col_slices
+                Ps = run.prepare()
+                run.spmv_into(x, [y], 0, Ps)
+                ts = []
+                for _ in range(a.reps):
+                    flush.zero_()
+                    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                    e0.record()
+                    run.spmv_into(x, [y], 0, Ps)
+                    e1.record()
+                    e1.synchronize()
+                    ts.append(e0.elapsed_time(e1) * 1e-3)
+                times[S].append(statistics.median(ts))
+                del run, Ps
             nnzs.append(A.nnz)
-            del A, x, y, Pp
+            del A, x, y
             torch.cuda.empty_cache()
-        rec = {"max_rank_ms": max(times) * 1e3, "mean_rank_ms": statistics.mean(times) * 1e3,
-               "rank_ms": [t * 1e3 for t in times], "rank_nnz": nnzs,
-               "exchange_bytes_per_rank_per_iter": int(4 * (R // P) * (P - 1))}
-        res["parts"][str(P)] = rec
-        print(P, json.dumps({k: v for k, v in rec.items() if k not in ("rank_ms", "rank_nnz")}), flush=True)
+        for S in slices:
+            rec = {"col_slices": used[S], "max_rank_ms": max(times[S]) * 1e3,
+                   "mean_rank_ms": statistics.mean(times[S]) * 1e3,
+                   "rank_ms": [t * 1e3 for t in times[S]], "rank_nnz": nnzs,
+                   "exchange_bytes_per_rank_per_iter": int(4 * (R // P) * (P - 1))}
+            res["parts"][f"{P}" if S == slices[-1] else f"{P}/S={S}"] = rec
+            print(P, S, json.dumps({k: v for k, v in rec.items() if k not in ("rank_ms", "rank_nnz")}), flush=True)
     t1 = res["parts"]["1"]["max_rank_ms"] if "1" in res["parts"] else None
     if t1:
         for P, rec in res["parts"].items():
