@@ -1072,7 +1072,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
         }
     };
     auto store_y = [&](int64_t r, V v) {
-        if constexpr (kB) dst.put(r, dst.acc ? v + dst.acc[r] : v);
+        if constexpr (kB) dst.put(r, v);
         else y[r] = v;
     };
     // Row-end probe of the unit [d0, d1) starting at row rs (rows before rs are finished):
@@ -1144,6 +1144,12 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
             if constexpr (kLateVals) vv[t] = own ? ld_stream(val + j0 + lane + t * 32) : V(0);
             else vv[t] = vn[t];
             p[t] = own ? ld_x(x + cn[t]) : V(0);
+        }
+        // accumulating stores (kp_spmv_bcast_acc): the first 32 rows' acc values load here,
+        // next to the gathers, instead of as a dependent load in front of each store
+        V a_pre = V(0);
+        if constexpr (kB) {
+            if (dst.acc && lane < nr) a_pre = dst.acc[r0 + lane];
         }
         // next unit: its (col, val) window and its row-end probe, overlapping the gathers
         Probe nxt{0, 0, 0, cur.end_re};
@@ -1222,6 +1228,9 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
             if (base + lane < nr) {
                 V v = e > st ? prod[(e - 1) + ((e - 1) >> 5)] : V(0);
                 if (base + lane == 0) v += carry;
+                if constexpr (kB) {
+                    if (dst.acc) v += base == 0 ? a_pre : dst.acc[r0 + base + lane];
+                }
                 store_y(r0 + base + lane, v);
             }
         }
