@@ -143,6 +143,23 @@ __device__ __forceinline__ double ld_x(const double *p) {
     asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(l2_evict_last_policy()));
     return v;
 }
+#elif defined(KP_X_MODE) && KP_X_MODE == 1  // A/B: x gathers not allocated in L1
+__device__ __forceinline__ float ld_x(const float *p) {
+    float v;
+    asm volatile("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ double ld_x(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+#elif defined(KP_X_MODE) && KP_X_MODE == 2  // A/B: x gathers cached in L2 only (.cg)
+__device__ __forceinline__ float ld_x(const float *p) { return __ldcg(p); }
+__device__ __forceinline__ double ld_x(const double *p) { return __ldcg(p); }
+#elif defined(KP_X_CG_F64) && KP_X_CG_F64  // fp64 gathers L2-only (.cg), fp32 through L1
+__device__ __forceinline__ float ld_x(const float *p) { return __ldg(p); }
+__device__ __forceinline__ double ld_x(const double *p) { return __ldcg(p); }
 #else
 template <typename T>
 __device__ __forceinline__ T ld_x(const T *p) { return __ldg(p); }
