@@ -320,3 +320,29 @@ def test_sharded_seer_column_blocked_fused_world1(orc):
         assert ok, ratio
     finally:
         tdist.destroy_process_group()
+
+
+@pytest.mark.parametrize("kern", [kernels.CSR_WO, kernels.CSR_MP])
+def test_column_blocks_with_an_empty_block(kern, orc):
+    """A block with no entries (every column in the first half): the accumulating store
+    path must still deliver acc + 0 to the destinations (the nnz == 0 branch of
+    kp_spmv_bcast_acc), and an empty first block zero-initialises the accumulator."""
+    rng = np.random.default_rng(21)
+    n = 5000
+    lens = rng.integers(0, 9, n)
+    off = np.concatenate([[0], np.cumsum(lens)]).astype(np.int64)
+    for lo, hi in ((0, n // 2 - 1), (n // 2 + 1, n)):   # entries only in one half
+        col = np.concatenate([np.sort(rng.choice(np.arange(lo, hi), size=k, replace=False)) for k in lens])
+        val = rng.uniform(0, 1, col.size)
+        from paper_2403_17017_b200.device import DeviceCSR
+        A = DeviceCSR(n, n, torch.from_numpy(off).cuda(), torch.from_numpy(col.astype(np.int32)).cuda(),
+                      torch.from_numpy(val).cuda())
+        plan = kdist.ShardPlan(0, 1, np.array([0, n]), n)
+        run = kdist.ShardedSeer(None, A, plan, 2, n, n, int(col.size), kernel=kern, col_slices=2)
+        assert min(B.nnz for B in run.blocks) == 0
+        x0 = torch.from_numpy(rng.uniform(0, 1, n)).cuda()
+        got = run.step(x0).cpu().numpy()
+        ref = x0.cpu().numpy()
+        for _ in range(2):
+            ref, _ = orc.spmv_csr(off, col.astype(np.int32), val, ref)
+        assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
