@@ -71,6 +71,7 @@ def _args():
     ap.add_argument("--scale", type=int, default=26, help="C5 R-MAT scale (26 = BASELINE configs[4])")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true", help="C5: skip the end-to-end (host-resident shard) leg")
     ap.add_argument("--no-configs", action="store_true", help="skip per_config (C1, C3, C4) and favourable")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--config-cpu-seconds", type=float, default=4.0)
@@ -707,10 +708,13 @@ def run_reference(a):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    if a.workload == "C5":
+        run_reference_c5(a)
+        return
     import torch
     import numpy as np
     from oracle import oracle as orc
-    name = a.workload if a.workload != "C5" else "C2"  # the CPU arm times one host; C5 is the multi-GPU config
+    name = a.workload
     k_default, dt_name, desc = CFG[name]
     k = a.iters or k_default
     dev = "cuda" if torch.cuda.is_available() else "cpu"
@@ -747,6 +751,80 @@ def run_reference(a):
                                       if core else "oracle C restatement") if path else
                                       "known path (no feature pass, SPEC.md:388)")
                                    + f" -> restated predict -> {k} OpenMP CPU SpMV (the reference has no SpMV)"},
+        "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def run_reference_c5(a):
+    """Reference arm of the multi-GPU configuration (BASELINE configs[4]) on one host: the
+    faithful CPU Seer pipeline on the C5 matrix -- selection from the FULL matrix' known
+    features (and its row-offsets pass when the selector gathers), then ``k`` OpenMP SpMVs
+    over a BOUNDED sample: a contiguous row block holding 1/KP_REF_C5_SAMPLE (default 16) of
+    the nonzeros, gathering from the full 64 M-entry x.  The metric is a rate (GB/s), so
+    the sample's rate is charged with its nnz share of the byte model.  Generation only on
+    the device (torch), as for the other arms; nothing of ours computes the timed part."""
+    import torch
+    import numpy as np
+    from oracle import oracle as orc
+    k_default, dt_name, desc = CFG["C5"]
+    k = a.iters or k_default
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    m = _make_matrix("C5", dev, a.scale)
+    R, C, Z = m.n_rows, m.n_cols, m.nnz
+    share = max(1, int(os.environ.get("KP_REF_C5_SAMPLE", "16")))
+    off_d = m.row_offsets.to(torch.int64)
+    rb = int(torch.searchsorted(off_d, torch.tensor([Z // share], device=off_d.device)).item())
+    rb = max(1, min(R, rb))
+    zb = int(off_d[rb].item())
+    off64 = off_d.cpu().numpy()                      # the full offsets: the feature pass reads them
+    offb = off64[:rb + 1].astype(np.int32)
+    colb = m.col_indices[:zb].to(torch.int32).cpu().numpy()
+    valb = m.values[:zb].to(torch.float32).cpu().numpy()
+    del m, off_d
+    if dev == "cuda":
+        torch.cuda.empty_cache()
+    xh = np.random.default_rng(1234).uniform(0, 1, C).astype(np.float32)
+    bytes_full = csr_bytes(R, C, Z, 4, 4)
+    bytes_sample = bytes_full * zb / Z
+    model, _ = _load_model()
+    md = _model_dict(model)
+    core = orc.ref_core()
+    known = (float(R), float(C), float(Z), float(k))
+
+    def pipeline():
+        path = orc.tree_predict(md["selector"], known)
+        if path == 0:
+            kern = orc.tree_predict(md["known"], known)
+        else:
+            lo, hi, s1, s2 = core.length_stats(off64) if core is not None else orc.length_stats(off64)
+            kern = orc.tree_predict(md["gathered"], known + tuple(orc.features_epilogue(lo, hi, s1, s2, R, C)))
+        for _ in range(k):
+            orc.spmv_native(offb, colb, valb, xh)
+        return kern, path
+
+    for _ in range(a.warmup):
+        pipeline()
+    t0 = time.perf_counter()
+    for _ in range(a.steps):
+        kern, path = pipeline()
+    el = time.perf_counter() - t0
+    v = a.steps * k * bytes_sample / el / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC,
+        "value": round(v, 3), "unit": "GB/s", "n_gpus": int(os.environ.get("WORLD_SIZE", "1")), "steps": a.steps,
+        "warmup": a.warmup, "ms_per_step": round(el / a.steps * 1e3, 3), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (counter-hash R-MAT generated on device; sampled rows copied to the host)",
+        "config": {"workload": "C5", "desc": desc if a.scale == 26 else desc.replace("s26", f"s{a.scale}"),
+                   "rows": R, "cols": C, "nnz": Z, "iterations": k,
+                   "sample": {"rows": rb, "nnz": zb, "share_of_nnz": round(zb / Z, 5)}},
+        "cpu_baseline": {"value": round(v, 3), "unit": "GB/s", "cores": orc.threads(), "kind": "port",
+                         "sample": f"{a.steps} faithful CPU Seer pipelines on C5: selector -> "
+                                   + ("gathered path: features of the full matrix via "
+                                      + ("compiled reference _core" if core is not None else "oracle C")
+                                      if path else "known path") + f" -> predict ({model.kernels[int(kern)]}) -> "
+                                   f"{k} OpenMP SpMVs over rows [0, {rb}) ({zb} nnz, 1/{share} of the matrix) "
+                                   "gathering from the full x; rate charged with the sample's nnz share"},
         "e2e": {"value": round(v, 3), "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }), flush=True)
 
@@ -889,6 +967,7 @@ def run_sharded(a):
     clk = clocks.stop()
     # sampled-row parity of one full iteration (SpMV + exchange) vs the fp64 oracle
     errs = [sampled_parity()]
+    e2e = _c5_e2e(run, plan, x0, k, bytes_csr, max(2, a.steps), backend, dev) if not a.no_e2e else None
     parity_ok = bool(max(errs) <= 1.0)
     if wd:
         wstat = wd.stop()
@@ -929,11 +1008,65 @@ def run_sharded(a):
                          "col_slices": run.col_slices, "ms": round(per * 1e3, 3),
                          "unblocked_ms": round(statistics.median(ts_unblocked) * 1e3, 3),
                          "note": "rank 0's local SpMV (column-blocked when col_slices > 1: x slices L2-resident)"},
-            "e2e": None, "gpu_launches": int(launches), "cpu_baseline": None, "clocks": clk,
+            "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": None, "clocks": clk,
         }), flush=True)
     dist.destroy_process_group()
     if not parity_ok:
         raise SystemExit(f"C5 sampled-row parity failed: max err/bound {max(errs)}")
+
+
+def _c5_e2e(run, plan, x0, k, bytes_csr, steps, backend, dev):
+    """C5 end to end through the public API: every step uploads this rank's WHOLE shard
+    (its column blocks: offsets, columns, values -- the host copy is stored in the blocked
+    layout, as a loaded matrix would be) and x0 from pinned host memory, runs the sharded
+    Seer step (prep + k iterations with the exchange) and reads this rank's final x slice
+    back.  Device time over the steps, max over ranks; None (with the reason) when the
+    shard would not fit a pinned host copy."""
+    import torch
+    import torch.distributed as dist
+    blocks = run.blocks
+    tens = [t for B in blocks for t in (B.row_offsets, B.col_indices, B.values)]
+    nbytes = sum(t.numel() * t.element_size() for t in tens)
+    if nbytes > int(os.environ.get("KP_C5_E2E_MAX_BYTES", str(48 << 30))):
+        return {"value": None, "unavailable": f"shard of {nbytes / 1e9:.1f} GB exceeds the pinned-host budget"}
+    host = []
+    for t in tens:
+        h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        h.copy_(t)
+        host.append(h)
+    h_x = torch.empty(x0.shape, dtype=x0.dtype, pin_memory=True)
+    h_x.copy_(x0)
+    d_x = torch.empty_like(x0)
+    n_out = max(1, plan.local_rows)
+    h_y = torch.empty(n_out, dtype=x0.dtype, pin_memory=True)
+
+    def step():
+        for t, h in zip(tens, host):
+            t.copy_(h, non_blocking=True)
+        d_x.copy_(h_x, non_blocking=True)
+        out = run.step(d_x)
+        h_y.copy_(out[plan.rank * plan.r_max: plan.rank * plan.r_max + n_out], non_blocking=True)
+
+    step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        step()
+    e1.record()
+    e1.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64)
+    if backend == "nccl":
+        t = t.to(dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total = float(t.item())
+    bi = nbytes + h_x.numel() * h_x.element_size()
+    return {"value": round(steps * k * bytes_csr / total / 1e9, 2), "unit": "GB/s",
+            "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(h_y.numel() * h_y.element_size()),
+            "ms_per_step": round(total / steps * 1e3, 3), "steps": steps,
+            "note": "per rank per step: its column-blocked shard + x0 H2D, prep + k iterations with the "
+                    "exchange, its final x slice D2H; device time, max over ranks"}
 
 
 # ------------------------------------------------------------------------ local launcher
