@@ -12,7 +12,10 @@ line carries `per_config` (C1, C3 k = 100, C4 fp64: Seer vs every fixed kernel, 
 the chosen kernel, e2e, CPU baseline) and `favourable` (every kernel on the input BASELINE
 names for it, by its own byte model).
 N > 1: workload C5 = BASELINE configs[4] (R-MAT scale 26, ~1.06 B nnz, 20 power iterations),
-row-sharded over the ranks (nnz-balanced), y exchanged every iteration; strong scaling.
+row-sharded over the ranks (nnz-balanced), each shard column-blocked when its x exceeds the
+L2, y exchanged every iteration; strong scaling.  Its e2e uploads every rank's whole shard
+each step.  `--impl reference` with C5: the faithful CPU Seer pipeline on a 1/16 row sample
+of the same matrix (rate charged by the sample's nnz share).
 `python bench.py --gpus N` without torchrun spawns N local ranks itself (NCCL, one GPU per
 rank; with fewer GPUs than ranks the ranks share GPUs over gloo -- control-flow check only).
 
