@@ -55,4 +55,14 @@ plan.launch()
 torch.cuda.synchronize()
 print("plan", plan.select_kind(), flush=True)
 plan.close()
+# column-blocked shard: accumulating fused-exchange stores (acc aliasing the destination)
+from paper_2403_17017_b200 import dist as kdist  # noqa: E402
+m = gen.config("C5", small=True, device="cuda")
+for dt in (torch.float32, torch.float64):
+    A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, m.n_cols, 0, 1, dt)
+    for kern in (kernels.CSR_WO, kernels.CSR_MP):
+        run = kdist.ShardedSeer(None, A, plan, 2, m.n_rows, m.n_cols, m.nnz, kernel=kern, col_slices=3)
+        run.step(torch.rand(m.n_rows, device="cuda", dtype=dt))
+        torch.cuda.synchronize()
+        print("column blocks", dt, kernels.KERNELS[kern], flush=True)
 print("all ok")
