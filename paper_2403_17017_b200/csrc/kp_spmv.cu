@@ -308,6 +308,10 @@ __global__ void __launch_bounds__(kBmThreads) k_csr_bm_short(const O *__restrict
             if (tid == 0) y[rc] = t;
             __syncthreads();  // sred reuse
         }
+        // the counters and lists are reset / refilled by the next group: every warp must
+        // have read them first (racecheck: thread 0 could zero s_nw / s_nc while a slower
+        // warp had yet to read them, dropping that warp's rows)
+        __syncthreads();
     }
 }
 
