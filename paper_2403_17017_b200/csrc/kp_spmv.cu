@@ -1076,8 +1076,15 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
         }
     };
     auto store_y = [&](int64_t r, V v) {
-        if constexpr (kB) dst.put(r, v);
-        else y[r] = v;
+        if constexpr (kB) {
+            // one destination (the accumulating column blocks, a 1-rank exchange): the
+            // kernel's own y (== dst.y[dst.self]) -- the general put re-reads its pointer
+            // table from the constant bank per store (ncu: +70 % constant-cache requests)
+            if (dst.n == 1) y[r] = v;
+            else dst.put(r, v);
+        } else {
+            y[r] = v;
+        }
     };
     // Row-end probe of the unit [d0, d1) starting at row rs (rows before rs are finished):
     // rows ending inside it satisfy off[r+1] + r < d1 (monotone in r -> ballot + popc).
