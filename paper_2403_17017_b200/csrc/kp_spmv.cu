@@ -85,6 +85,48 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, cu
     return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
 }
 
+// accumulator reads of kp_spmv_bcast_acc: read once, coherent (acc may alias y[self]);
+// KP_ACC_EF (A/B): L2 evict-first, so the accumulator stream does not displace the
+// column slice's x lines
+#ifndef KP_ACC_EF
+#define KP_ACC_EF 0
+#endif
+template <typename V>
+__device__ __forceinline__ V ld_acc(const V *p) {
+#if KP_ACC_EF
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    if constexpr (sizeof(V) == 4) {
+        float v;
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+        return v;
+    } else {
+        double v;
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+        return v;
+    }
+#else
+    return *p;
+#endif
+}
+
+#ifndef KP_Y1_EF
+#define KP_Y1_EF 0
+#endif
+template <typename V>
+__device__ __forceinline__ void st_y1(V *p, V v) {
+#if KP_Y1_EF
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+    if constexpr (sizeof(V) == 4)
+        asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(p), "f"(v), "l"(pol) : "memory");
+    else
+        asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
+#else
+    *p = v;
+#endif
+}
+
 template <typename V>
 struct YDst {
     V *y[KP_MAX_PEERS];
@@ -1080,7 +1122,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
             // one destination (the accumulating column blocks, a 1-rank exchange): the
             // kernel's own y (== dst.y[dst.self]) -- the general put re-reads its pointer
             // table from the constant bank per store (ncu: +70 % constant-cache requests)
-            if (dst.n == 1) y[r] = v;
+            if (dst.n == 1) st_y1(y + r, v);
             else dst.put(r, v);
         } else {
             y[r] = v;
@@ -1160,7 +1202,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
         // next to the gathers, instead of as a dependent load in front of each store
         V a_pre = V(0);
         if constexpr (kB) {
-            if (dst.acc && lane < nr) a_pre = dst.acc[r0 + lane];
+            if (dst.acc && lane < nr) a_pre = ld_acc(dst.acc + r0 + lane);
         }
         // next unit: its (col, val) window and its row-end probe, overlapping the gathers
         Probe nxt{0, 0, 0, cur.end_re};
@@ -1240,7 +1282,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
                 V v = e > st ? prod[(e - 1) + ((e - 1) >> 5)] : V(0);
                 if (base + lane == 0) v += carry;
                 if constexpr (kB) {
-                    if (dst.acc) v += base == 0 ? a_pre : dst.acc[r0 + base + lane];
+                    if (dst.acc) v += base == 0 ? a_pre : ld_acc(dst.acc + r0 + base + lane);
                 }
                 store_y(r0 + base + lane, v);
             }
