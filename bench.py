@@ -970,7 +970,7 @@ def run_sharded(a):
     clk = clocks.stop()
     # sampled-row parity of one full iteration (SpMV + exchange) vs the fp64 oracle
     errs = [sampled_parity()]
-    e2e = _c5_e2e(run, plan, x0, k, bytes_csr, max(2, a.steps), backend, dev) if not a.no_e2e else None
+    e2e = _c5_e2e(run, plan, x0, k, bytes_csr, max(4, a.steps), backend, dev, A, (R, C, Z)) if not a.no_e2e else None
     parity_ok = bool(max(errs) <= 1.0)
     if wd:
         wstat = wd.stop()
@@ -1018,58 +1018,117 @@ def run_sharded(a):
         raise SystemExit(f"C5 sampled-row parity failed: max err/bound {max(errs)}")
 
 
-def _c5_e2e(run, plan, x0, k, bytes_csr, steps, backend, dev):
+def _c5_e2e(run, plan, x0, k, bytes_csr, steps, backend, dev, A=None, dims=None):
     """C5 end to end through the public API: every step uploads this rank's WHOLE shard
     (its column blocks: offsets, columns, values -- the host copy is stored in the blocked
     layout, as a loaded matrix would be) and x0 from pinned host memory, runs the sharded
     Seer step (prep + k iterations with the exchange) and reads this rank's final x slice
-    back.  Device time over the steps, max over ranks; None (with the reason) when the
-    shard would not fit a pinned host copy."""
+    back.  Served two ways: serially, and -- the reported value -- as a two-deep pipeline
+    the way a serving loop would (a second ShardedSeer instance on its own device copy: step
+    i+1's shard streams over PCIe on a copy stream while step i computes), like the C2 e2e.
+    Device time over the steps, max over ranks; None (with the reason) when the shard would
+    not fit a pinned host copy."""
     import torch
     import torch.distributed as dist
-    blocks = run.blocks
-    tens = [t for B in blocks for t in (B.row_offsets, B.col_indices, B.values)]
-    nbytes = sum(t.numel() * t.element_size() for t in tens)
+    from paper_2403_17017_b200 import dist as kdist
+
+    def tensors(r):
+        return [t for B in r.blocks for t in (B.row_offsets, B.col_indices, B.values)]
+
+    tens0 = tensors(run)
+    nbytes = sum(t.numel() * t.element_size() for t in tens0)
     if nbytes > int(os.environ.get("KP_C5_E2E_MAX_BYTES", str(48 << 30))):
         return {"value": None, "unavailable": f"shard of {nbytes / 1e9:.1f} GB exceeds the pinned-host budget"}
     host = []
-    for t in tens:
+    for t in tens0:
         h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
         h.copy_(t)
         host.append(h)
     h_x = torch.empty(x0.shape, dtype=x0.dtype, pin_memory=True)
     h_x.copy_(x0)
-    d_x = torch.empty_like(x0)
     n_out = max(1, plan.local_rows)
     h_y = torch.empty(n_out, dtype=x0.dtype, pin_memory=True)
+    sl = slice(plan.rank * plan.r_max, plan.rank * plan.r_max + n_out)
 
-    def step():
-        for t, h in zip(tens, host):
+    def timed(fn, n):
+        fn(0)
+        fn(1)
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for i in range(n):
+            fn(i)
+        torch.cuda.current_stream().wait_stream(copy)
+        e1.record()
+        e1.synchronize()
+        t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64)
+        if backend == "nccl":
+            t = t.to(dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    copy = torch.cuda.Stream(device=dev)
+    d_x = [torch.empty_like(x0), torch.empty_like(x0)]
+
+    def serial(i):
+        for t, h in zip(tens0, host):
             t.copy_(h, non_blocking=True)
-        d_x.copy_(h_x, non_blocking=True)
-        out = run.step(d_x)
-        h_y.copy_(out[plan.rank * plan.r_max: plan.rank * plan.r_max + n_out], non_blocking=True)
+        d_x[0].copy_(h_x, non_blocking=True)
+        h_y.copy_(run.step(d_x[0])[sl], non_blocking=True)
 
-    step()
-    torch.cuda.synchronize()
-    dist.barrier()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(steps):
-        step()
-    e1.record()
-    e1.synchronize()
-    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], dtype=torch.float64)
+    t_serial = timed(serial, steps)
+    res = {"unit": "GB/s", "h2d_bytes_per_step": int(nbytes + h_x.numel() * h_x.element_size()),
+           "d2h_bytes_per_step": int(h_y.numel() * h_y.element_size()), "steps": steps,
+           "serial_ms_per_step": round(t_serial / steps * 1e3, 3),
+           "serial_value": round(steps * k * bytes_csr / t_serial / 1e9, 2)}
+    run2 = None
+    # a second instance needs another device copy of the blocks: decide on ALL ranks
+    # together (its exchange rendezvous is collective)
+    free = torch.cuda.mem_get_info(dev)[0]
+    okt = torch.tensor([1.0 if free > 2.5 * nbytes else 0.0], dtype=torch.float64)
     if backend == "nccl":
-        t = t.to(dev)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    total = float(t.item())
-    bi = nbytes + h_x.numel() * h_x.element_size()
-    return {"value": round(steps * k * bytes_csr / total / 1e9, 2), "unit": "GB/s",
-            "h2d_bytes_per_step": int(bi), "d2h_bytes_per_step": int(h_y.numel() * h_y.element_size()),
-            "ms_per_step": round(total / steps * 1e3, 3), "steps": steps,
-            "note": "per rank per step: its column-blocked shard + x0 H2D, prep + k iterations with the "
-                    "exchange, its final x slice D2H; device time, max over ranks"}
+        okt = okt.to(dev)
+    dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    if okt.item() < 1.0:
+        res["pipeline_error"] = "not enough free device memory for a second copy of the shard on every rank"
+    elif A is not None and dims is not None:
+        try:
+            run2 = kdist.ShardedSeer(None, A, plan, k, *dims, exchange=run.exchange, kernel=run.kernel,
+                                     col_slices=run.col_slices)
+        except Exception as exc:  # no room for a second device copy: serial only
+            res["pipeline_error"] = repr(exc)[:200]
+    if run2 is None:
+        res.update(value=res["serial_value"], ms_per_step=res["serial_ms_per_step"],
+                   note="per rank per step: its column-blocked shard + x0 H2D, prep + k iterations with the "
+                        "exchange, its final x slice D2H, in series; device time, max over ranks")
+        return res
+    runs, tens = [run, run2], [tens0, tensors(run2)]
+    comp = torch.cuda.current_stream()
+    freed = [torch.cuda.Event(), torch.cuda.Event()]
+    landed = [torch.cuda.Event(), torch.cuda.Event()]
+    for ev in freed:
+        ev.record(comp)
+
+    def pipelined(i):
+        s_ = i % 2
+        copy.wait_event(freed[s_])
+        with torch.cuda.stream(copy):
+            for t, h in zip(tens[s_], host):
+                t.copy_(h, non_blocking=True)
+            d_x[s_].copy_(h_x, non_blocking=True)
+        landed[s_].record(copy)
+        comp.wait_event(landed[s_])
+        h_y.copy_(runs[s_].step(d_x[s_])[sl], non_blocking=True)
+        freed[s_].record(comp)
+
+    t_pipe = timed(pipelined, steps)
+    del run2
+    res.update(value=round(steps * k * bytes_csr / t_pipe / 1e9, 2), ms_per_step=round(t_pipe / steps * 1e3, 3),
+               note="per rank per step: its column-blocked shard + x0 H2D (copy stream), prep + k iterations "
+                    "with the exchange, its final x slice D2H; two-deep pipeline over two device copies "
+                    "(serial: serial_*); device time, max over ranks")
+    return res
 
 
 # ------------------------------------------------------------------------ local launcher
