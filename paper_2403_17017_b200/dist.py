@@ -19,6 +19,8 @@ The communicator is torch.distributed (NCCL over NVLink on GPUs, gloo on CPU for
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 
@@ -357,9 +359,8 @@ class ShardedSeer:
         if self.exchange in ("nccl", "host"):
             self.bufs = [torch.zeros(plan.world * plan.r_max, dtype=dt, device=A.device) for _ in range(2)]
         # column blocking (merge-path kernels: the accumulating store is theirs); "auto" =
-        # when the padded x exceeds the L2 budget, env KP_COL_SLICES overrides
-        import os
-        S = os.environ.get("KP_COL_SLICES", col_slices)
+        # env KP_COL_SLICES if set, else when the padded x exceeds the L2 budget
+        S = os.environ.get("KP_COL_SLICES", "auto") if col_slices == "auto" else col_slices
         if S == "auto":
             l2 = int(getattr(torch.cuda.get_device_properties(A.device), "L2_cache_size", 0) or 126 << 20)
             S = auto_col_slices(plan.world * plan.r_max * A.values.element_size(), l2)
