@@ -127,6 +127,20 @@ __device__ __forceinline__ void st_y1(V *p, V v) {
 #endif
 }
 
+// x gathers of the merge kernels.  KP_MERGE_X_CG_F64 (A/B): fp64 gathers L2-only (.cg),
+// fp32 through L1 as everywhere else
+#ifndef KP_MERGE_X_CG_F64
+#define KP_MERGE_X_CG_F64 0
+#endif
+__device__ __forceinline__ float ld_x_merge(const float *p) { return ld_x(p); }
+__device__ __forceinline__ double ld_x_merge(const double *p) {
+#if KP_MERGE_X_CG_F64
+    return __ldcg(p);
+#else
+    return ld_x(p);
+#endif
+}
+
 template <typename V>
 struct YDst {
     V *y[KP_MAX_PEERS];
@@ -1196,7 +1210,7 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
             const bool own = lane + t * 32 < nz;
             if constexpr (kLateVals) vv[t] = own ? ld_stream(val + j0 + lane + t * 32) : V(0);
             else vv[t] = vn[t];
-            p[t] = own ? ld_x(x + cn[t]) : V(0);
+            p[t] = own ? ld_x_merge(x + cn[t]) : V(0);
         }
         // accumulating stores (kp_spmv_bcast_acc): the first 32 rows' acc values load here,
         // next to the gathers, instead of as a dependent load in front of each store

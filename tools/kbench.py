@@ -46,6 +46,8 @@ MATS = {
     "C2d": lambda d: (gen.config("C2", device=d), torch.float64),
     "band27d": lambda d: (gen.banded(4_000_000, 27, device=d), torch.float64),
     "pld": lambda d: (gen.powerlaw_rows(4_000_000, 16.0, 1.5, device=d), torch.float64),
+    "C3d": lambda d: (gen.config("C3", device=d), torch.float64),
+    "band2kd": lambda d: (gen.banded(65_536, 2048, device=d), torch.float64),
 }
 
 
