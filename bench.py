@@ -683,6 +683,7 @@ def _cpu_baseline(A, x, k, model, bytes_csr, seconds):
     than the budget is cut between SpMV iterations and counted by the iterations it ran)."""
     import numpy as np
     from oracle import oracle as orc
+    orc.use_all_cores()
     off32, col, val = A.to_host()
     xh = x.cpu().numpy()
     off64 = off32.astype(np.int64)
@@ -717,6 +718,7 @@ def run_reference(a):
     import torch
     import numpy as np
     from oracle import oracle as orc
+    orc.use_all_cores()
     name = a.workload
     k_default, dt_name, desc = CFG[name]
     k = a.iters or k_default
@@ -769,6 +771,7 @@ def run_reference_c5(a):
     import torch
     import numpy as np
     from oracle import oracle as orc
+    orc.use_all_cores()
     k_default, dt_name, desc = CFG["C5"]
     k = a.iters or k_default
     dev = "cuda" if torch.cuda.is_available() else "cpu"

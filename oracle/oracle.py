@@ -64,6 +64,8 @@ def lib() -> ctypes.CDLL:
         L.orc_tree_predict.argtypes = [p] * 6
         L.orc_tree_predict.restype = ctypes.c_int
         L.orc_threads.restype = ctypes.c_int
+        L.orc_set_threads.argtypes = [ctypes.c_int]
+        L.orc_set_threads.restype = None
         _LIB = L
     return _LIB
 
@@ -207,6 +209,14 @@ def csr_from_coo(n_rows: int, n_cols: int, rows, cols, vals):
 
 def threads() -> int:
     return int(lib().orc_threads())
+
+
+def use_all_cores() -> int:
+    """Run the CPU baseline on every core this process may use (launchers like torchrun set
+    OMP_NUM_THREADS=1 per rank; the CPU arm runs on one rank only).  Returns the count."""
+    n = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+    lib().orc_set_threads(int(n))
+    return threads()
 
 
 # --------------------------------------------------------------------------- trees

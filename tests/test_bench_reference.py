@@ -32,6 +32,14 @@ def test_reference_arm_c1():
     _check(_run(["--workload", "C1", "--steps", "2", "--warmup", "1"]), "C1")
 
 
+def test_reference_arm_uses_every_core_under_a_launcher(monkeypatch):
+    """torchrun exports OMP_NUM_THREADS=1 to each rank; the CPU arm (rank 0 only) must still
+    run on all the cores it may use."""
+    monkeypatch.setenv("OMP_NUM_THREADS", "1")
+    d = _run(["--workload", "C1", "--steps", "1", "--warmup", "1"])
+    assert d["cpu_baseline"]["cores"] == len(os.sched_getaffinity(0))
+
+
 @pytest.mark.parametrize("share", ["4", "16"])
 def test_reference_arm_c5_row_sample(share, monkeypatch):
     monkeypatch.setenv("KP_REF_C5_SAMPLE", share)
