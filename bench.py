@@ -1023,8 +1023,8 @@ def run_sharded(a):
 
 def _c5_e2e(run, plan, x0, k, bytes_csr, steps, backend, dev, A=None, dims=None):
     """C5 end to end through the public API: every step uploads this rank's WHOLE shard
-    (its column blocks: offsets, columns, values -- the host copy is stored in the blocked
-    layout, as a loaded matrix would be) and x0 from pinned host memory, runs the sharded
+    (its column blocks: offsets, columns, values and the compressed blocks' row ids -- the
+    host copy is stored in the blocked layout, as a loaded matrix would be) and x0 from pinned host memory, runs the sharded
     Seer step (prep + k iterations with the exchange) and reads this rank's final x slice
     back.  Served two ways: serially, and -- the reported value -- as a two-deep pipeline
     the way a serving loop would (a second ShardedSeer instance on its own device copy: step
@@ -1036,7 +1036,8 @@ def _c5_e2e(run, plan, x0, k, bytes_csr, steps, backend, dev, A=None, dims=None)
     from paper_2403_17017_b200 import dist as kdist
 
     def tensors(r):
-        return [t for B in r.blocks for t in (B.row_offsets, B.col_indices, B.values)]
+        return [t for B, rid in zip(r.blocks, r.block_rows)
+                for t in (B.row_offsets, B.col_indices, B.values) + ((rid,) if rid is not None else ())]
 
     tens0 = tensors(run)
     nbytes = sum(t.numel() * t.element_size() for t in tens0)

@@ -197,13 +197,17 @@ KP_API int kp_spmv_bcast(int32_t kernel, const kp_csr *A, const kp_prepared *P, 
                          const kp_peers *peers, void *d_ws, size_t ws_bytes, void *stream);
 /* kp_spmv_bcast with accumulation: every destination receives acc + A . x (d_acc: n_rows
  * entries of A->val_type, or NULL = kp_spmv_bcast).  d_acc may be the same buffer as
- * peers->y[peers->self].  The column-blocked iteration of a row shard whose x does not
- * fit in L2 (dist.ShardedSeer): A split into column slices A_0..A_{S-1}, y = A_0 x_0
- * accumulated slice by slice, the last slice's stores going to every rank -- each slice's
- * x gathers stay L2-resident.  Not part of the reference interface (a B200 layout
- * choice of the multi-GPU executor). */
+ * peers->y[peers->self].  d_rows (int32, A->n_rows entries, or NULL = identity): row r of A
+ * is row d_rows[r] of the destination and of acc -- a compressed-row block (only its
+ * non-empty rows) accumulating in place; requires one destination and d_acc == NULL or
+ * == that destination; rows not listed are left untouched.  The column-blocked iteration
+ * of a row shard whose x does not fit in L2 (dist.ShardedSeer): A split into column
+ * slices, y = A_0 x + ... + A_{S-1} x accumulated block by block, the last block's stores
+ * going to every rank.  Not part of the reference interface (a B200 layout choice of the
+ * multi-GPU executor). */
 KP_API int kp_spmv_bcast_acc(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x,
-                             const void *d_acc, const kp_peers *peers, void *d_ws, size_t ws_bytes, void *stream);
+                             const void *d_acc, const int32_t *d_rows, const kp_peers *peers, void *d_ws,
+                             size_t ws_bytes, void *stream);
 
 /* ------------------------------------------------------------ Seer plan (one CUDA graph) */
 /* The whole pipeline -- kp_seer_select, then the chosen kernel's kp_prepare and

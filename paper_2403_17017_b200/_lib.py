@@ -117,7 +117,7 @@ def load(require: bool = True):
         "kp_coo_workspace_bytes": (ctypes.c_int, [i64, i64, i64, P(sz)]),
         "kp_csr_from_coo": (ctypes.c_int, [i64, i64, p, p, p, i64, p, p, p, p, p, sz, p]),
         "kp_spmv_bcast": (ctypes.c_int, [i32, P(kp_csr), P(kp_prepared), p, P(kp_peers), p, sz, p]),
-        "kp_spmv_bcast_acc": (ctypes.c_int, [i32, P(kp_csr), P(kp_prepared), p, p, P(kp_peers), p, sz, p]),
+        "kp_spmv_bcast_acc": (ctypes.c_int, [i32, P(kp_csr), P(kp_prepared), p, p, p, P(kp_peers), p, sz, p]),
         "kp_mm_header": (ctypes.c_int, [ctypes.c_char_p, sz, P(kp_mm_info)]),
         "kp_mm_parse": (ctypes.c_int, [ctypes.c_char_p, sz, p, p, p, i64, i32, P(kp_mm_info)]),
         "kp_watchdog_start": (ctypes.c_int, [p, i64, i64, P(p)]),

@@ -149,7 +149,11 @@ struct YDst {
     // end), so acc is added once; the fix-up then adds carries onto y[self] as usual.
     // acc may alias y[self]: the same thread reads acc[r] before it stores y[.][r].
     const V *acc;
+    // compressed-row column blocks: row r of the matrix is row rid[r] of y / acc (null:
+    // identity).  Every access to y / acc by row index goes through row().
+    const int32_t *rid;
     int32_t n, self;
+    __device__ __forceinline__ int64_t row(int64_t r) const { return rid ? (int64_t)rid[r] : r; }
     __device__ __forceinline__ void put(int64_t i, V v) const {
         // fully unrolled with a predicate: a dynamic index into this by-value parameter
         // struct would force a local-memory copy of it
@@ -890,8 +894,12 @@ __global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__
         const bool started_here = below != 0;  // a head at or before this lane within the warp
         const bool run_end_here = next != r;
         if (r >= 0 && started_here && run_end_here) {
-            if constexpr (kB) dst.put(r, dst.y[dst.self][r] + inc.v);
-            else y[r] += inc.v;
+            if constexpr (kB) {
+                const int64_t rr = dst.row(r);
+                dst.put(rr, dst.y[dst.self][rr] + inc.v);
+            } else {
+                y[r] += inc.v;
+            }
         }
         // run open at the warp end that started in this warp: continue over later units
         const bool cont = (lane == 31) && r >= 0 && started_here && !run_end_here;
@@ -920,8 +928,12 @@ __global__ void __launch_bounds__(256) k_carry_fixup(const int32_t *__restrict__
             }
             acc = group_sum<32>(acc);
             if (lane == 31) {
-                if constexpr (kB) dst.put(rho, dst.y[dst.self][rho] + (inc.v + acc));
-                else y[rho] += inc.v + acc;
+                if constexpr (kB) {
+                    const int64_t rr = dst.row(rho);
+                    dst.put(rr, dst.y[dst.self][rr] + (inc.v + acc));
+                } else {
+                    y[rho] += inc.v + acc;
+                }
             }
         }
     }
@@ -1215,8 +1227,12 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
         // accumulating stores (kp_spmv_bcast_acc): the first 32 rows' acc values load here,
         // next to the gathers, instead of as a dependent load in front of each store
         V a_pre = V(0);
+        int32_t rr_pre = 0;  // this lane's first-round destination row (row map applied)
         if constexpr (kB) {
-            if (dst.acc && lane < nr) a_pre = ld_acc(dst.acc + r0 + lane);
+            if (lane < nr) {
+                rr_pre = (int32_t)dst.row(r0 + lane);
+                if (dst.acc) a_pre = ld_acc(dst.acc + rr_pre);
+            }
         }
         // next unit: its (col, val) window and its row-end probe, overlapping the gathers
         Probe nxt{0, 0, 0, cur.end_re};
@@ -1295,10 +1311,12 @@ __global__ void __launch_bounds__(kMergeWarps * 32, kMergeMinBlocks<V, kB>) k_cs
             if (base + lane < nr) {
                 V v = e > st ? prod[(e - 1) + ((e - 1) >> 5)] : V(0);
                 if (base + lane == 0) v += carry;
+                int64_t rr = r0 + base + lane;
                 if constexpr (kB) {
-                    if (dst.acc) v += base == 0 ? a_pre : ld_acc(dst.acc + r0 + base + lane);
+                    rr = base == 0 ? (int64_t)rr_pre : dst.row(rr);
+                    if (dst.acc) v += base == 0 ? a_pre : ld_acc(dst.acc + rr);
                 }
-                store_y(r0 + base + lane, v);
+                store_y(rr, v);
             }
         }
         const int e_last = (int)(cur.end_re - j0);
@@ -2140,7 +2158,8 @@ int launch_long_rows(int32_t kernel, const kp_csr *A, DeferWs *dw, const O *off,
 
 template <typename V, typename O>
 int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V *y, unsigned char *ws,
-           cudaStream_t s, const kp_peers *peers = nullptr, const V *acc = nullptr) {
+           cudaStream_t s, const kp_peers *peers = nullptr, const V *acc = nullptr,
+           const int32_t *rid = nullptr) {
     const O *off = reinterpret_cast<const O *>(A->row_offsets);
     const int32_t *col = A->col_indices;
     const V *val = reinterpret_cast<const V *>(A->values);
@@ -2262,6 +2281,7 @@ int spmv_t(int32_t kernel, const kp_csr *A, const kp_prepared *P, const V *x, V 
                 d.n = peers->n;
                 d.self = peers->self;
                 d.acc = acc;
+                d.rid = rid;
                 const int64_t *part = nullptr;
                 if (kernel == KP_CSR_MP) {
                     if (!P || !P->buf) return KP_EINVAL;
@@ -2418,11 +2438,11 @@ int64_t kp_debug_set_wave_warps(int64_t warps) {
 
 int kp_spmv_bcast(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x, const kp_peers *peers,
                   void *d_ws, size_t ws_bytes, void *stream) {
-    return kp_spmv_bcast_acc(kernel, A, P, d_x, nullptr, peers, d_ws, ws_bytes, stream);
+    return kp_spmv_bcast_acc(kernel, A, P, d_x, nullptr, nullptr, peers, d_ws, ws_bytes, stream);
 }
 
 int kp_spmv_bcast_acc(int32_t kernel, const kp_csr *A, const kp_prepared *P, const void *d_x, const void *d_acc,
-                      const kp_peers *peers, void *d_ws, size_t ws_bytes, void *stream) {
+                      const int32_t *d_rows, const kp_peers *peers, void *d_ws, size_t ws_bytes, void *stream) {
     KP_NVTX("kp_spmv_bcast");
     if (!valid_csr(A) || !peers || peers->n < 1 || peers->n > KP_MAX_PEERS || peers->self < 0 ||
         peers->self >= peers->n || (kernel != KP_CSR_MP && kernel != KP_CSR_WO) || (A->n_cols > 0 && !d_x))
@@ -2433,9 +2453,12 @@ int kp_spmv_bcast_acc(int32_t kernel, const kp_csr *A, const kp_prepared *P, con
     kp_spmv_workspace_bytes(kernel, A, &need);
     if (ws_bytes < need || (need && !d_ws)) return KP_ENOMEM;
     if (P && P->buf && P->kernel != kernel) return KP_EINVAL;
+    // a row map scatters into ONE destination, accumulating in place (or overwriting)
+    if (d_rows && (peers->n != 1 || (d_acc && d_acc != peers->y[0]))) return KP_EINVAL;
     cudaStream_t s = (cudaStream_t)stream;
     if (A->n_rows == 0) return KP_OK;
     const size_t yb = (size_t)A->n_rows * val_bytes(A);
+    if (A->nnz == 0 && d_rows) return d_acc ? KP_OK : KP_EINVAL;  // mapped rows += 0: nothing to do
     if (A->nnz == 0) {  // y = acc (or 0) everywhere
         for (int p = 0; p < peers->n; ++p) {
             if (!d_acc) KP_CUDA_TRY(cudaMemsetAsync(peers->y[p], 0, yb, s));
@@ -2447,13 +2470,13 @@ int kp_spmv_bcast_acc(int32_t kernel, const kp_csr *A, const kp_prepared *P, con
     if (A->val_type == KP_F32) {
         const float *acc = (const float *)d_acc;
         return A->off_type == KP_I32
-                   ? spmv_t<float, int32_t>(kernel, A, P, (const float *)d_x, nullptr, ws, s, peers, acc)
-                   : spmv_t<float, int64_t>(kernel, A, P, (const float *)d_x, nullptr, ws, s, peers, acc);
+                   ? spmv_t<float, int32_t>(kernel, A, P, (const float *)d_x, nullptr, ws, s, peers, acc, d_rows)
+                   : spmv_t<float, int64_t>(kernel, A, P, (const float *)d_x, nullptr, ws, s, peers, acc, d_rows);
     }
     const double *acc = (const double *)d_acc;
     return A->off_type == KP_I32
-               ? spmv_t<double, int32_t>(kernel, A, P, (const double *)d_x, nullptr, ws, s, peers, acc)
-               : spmv_t<double, int64_t>(kernel, A, P, (const double *)d_x, nullptr, ws, s, peers, acc);
+               ? spmv_t<double, int32_t>(kernel, A, P, (const double *)d_x, nullptr, ws, s, peers, acc, d_rows)
+               : spmv_t<double, int64_t>(kernel, A, P, (const double *)d_x, nullptr, ws, s, peers, acc, d_rows);
 }
 
 int kp_shard_partition(const void *d_off, int32_t off_type, int64_t n_rows, int32_t parts, int64_t *d_cuts,

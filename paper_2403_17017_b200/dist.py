@@ -132,18 +132,19 @@ def all_gather_slices(buf, plan: ShardPlan, group=None) -> None:
 
 # ---------------------------------------------------------------------- column blocking
 # A rank's SpMV gathers x over the WHOLE padded x (C5: 64M fp32 = 268 MB, twice the 126 MB
-# L2): on R-MAT every gather misses, and ncu counts 6.4x the algorithmic DRAM bytes
-# (profiles/ncu_C5_r01.md).  Column blocking keeps each gather window L2-resident: the
-# block is split once, at shard time, into S column slices A_0..A_{S-1} (each a CSR over
-# the same rows), and an iteration is y = A_0 x + ... + A_{S-1} x, accumulated slice by
-# slice in the merge kernel's own row stores (kp_spmv_bcast_acc; the last slice's stores
-# are the exchange).  Cost: S passes over the row bookkeeping (offsets, row ends) and
-# S - 1 reads of the accumulator.  Per-rank SpMV of C5 (profiles/shard_scaling_r02.json,
-# rank-emulated on one GPU): P = 1 10.20 -> 6.16 ms at S = 2 (6.16 at S = 3, 6.80 at 4);
-# P = 8 1.34 -> 0.88 ms at S = 2 (0.92 at 3, 1.04 at 4).  Two slices of 134 MB each beat
-# three that fit the 126 MB L2: R-MAT's gathers are skewed, so a slice's hot lines stay
-# resident while each extra slice costs a pass over the row bookkeeping.
-COL_SLICE_L2_FRACTION = 1.25  # an x slice may be this multiple of the L2 (measured sweep)
+# L2): on R-MAT nearly every gather misses, and ncu counts 6.1x the algorithmic DRAM bytes
+# (profiles/ncu_C5_blocked_r02.md).  Column blocking keeps each gather window closer to
+# L2-resident: the block is split once, at shard time, into S column slices A_0..A_{S-1}
+# (each a CSR over the same rows), and an iteration is y = A_0 x + ... + A_{S-1} x,
+# accumulated slice by slice in the merge kernel's own row stores (kp_spmv_bcast_acc; the
+# last slice's stores are the exchange).  R-MAT leaves most rows of a slice empty (C5: 60 %
+# of all rows are empty, 21-32 % have entries in a given slice at S = 6-2), so slices are
+# compressed-row blocks -- only their non-empty rows, scattered into the accumulator in
+# place through a row map -- except the last one when there are several ranks (its
+# full-row stores are the fused exchange).  Per-rank SpMV of C5 (shard_scaling, rank-
+# emulated on one GPU; profiles/shard_scaling_r02.txt): P = 1 10.4 -> 5.16 ms at S = 3
+# (5.14 at 4, 5.95 at 2); P = 8 1.31 -> 0.83 ms at S = 3 (0.85 at 4, 0.88 at 2).
+COL_SLICE_L2_FRACTION = 0.75  # an x slice may be this fraction of the L2 (measured sweep)
 MAX_COL_SLICES = 8
 
 
@@ -178,16 +179,38 @@ def split_columns(row_offsets, col_indices, values, lo: int, hi: int):
     return out, col_indices[idx], values[idx]
 
 
-def column_blocks(A, slices: int):
-    """DeviceCSR -> ``slices`` DeviceCSRs (same rows and n_cols), one per column range."""
+def compress_rows(row_offsets):
+    """(offsets over the non-empty rows only, int32 row ids of those rows) of a CSR's
+    offsets -- a compressed-row block: its merge pass skips the empty rows entirely."""
+    import torch
+    off = row_offsets.to(torch.int64)
+    ln = off[1:] - off[:-1]
+    keep = torch.nonzero(ln > 0).squeeze(1)
+    out = torch.zeros(keep.numel() + 1, dtype=torch.int64, device=off.device)
+    if keep.numel():
+        torch.cumsum(ln[keep], 0, out=out[1:])
+    return out, keep.to(torch.int32)
+
+
+def column_blocks(A, slices: int, compact: bool = True, compact_last: bool = False):
+    """DeviceCSR -> ``slices`` column blocks (same n_cols), one per column range, as a list
+    of (DeviceCSR, row ids).  With ``compact`` every block but the last keeps only its
+    non-empty rows (row ids: int32 tensor mapping them back; R-MAT C5: 21-32 % of the rows
+    per block); the last block keeps every row (row ids None), so its stores cover the
+    whole y -- they are the exchange -- unless ``compact_last`` (one rank: the accumulator
+    is copied to the next x instead)."""
     import torch
     from .device import DeviceCSR
     out = []
     b = col_slice_bounds(A.n_cols, slices)
     for s in range(slices):
         o, c, v = split_columns(A.row_offsets, A.col_indices, A.values, b[s], b[s + 1])
+        rid = None
+        if compact and (s < slices - 1 or compact_last):
+            o, rid = compress_rows(o)
+        n = o.numel() - 1
         o = o.to(torch.int32) if int(o[-1]) < 2**31 - 1 else o
-        out.append(DeviceCSR(A.n_rows, A.n_cols, o, c, v))
+        out.append((DeviceCSR(n, A.n_cols, o, c, v), rid))
     return out
 
 
@@ -327,7 +350,7 @@ class ShardedSeer:
     slice of the next x, in-place NCCL all-gather of the slices over NVLink)."""
 
     def __init__(self, model, A, plan: ShardPlan, k: int, n_rows: int, n_cols: int, nnz: int, group=None,
-                 exchange: str = "auto", kernel=None, col_slices="auto"):
+                 exchange: str = "auto", kernel=None, col_slices="auto", compact_blocks: bool = True):
         import torch
         from . import kernels
         from .features import decode_outcome
@@ -368,7 +391,14 @@ class ShardedSeer:
         if S < 1:
             raise ValueError("col_slices must be >= 1")
         self.col_slices = S if self.kernel in (kernels.CSR_MP, kernels.CSR_WO) and A.nnz > 0 else 1
-        self.blocks = column_blocks(A, self.col_slices) if self.col_slices > 1 else [A]
+        # one rank: every block compressed, the accumulator copied to the next x (a local
+        # copy); several ranks: the last block keeps all rows so that its stores are the
+        # fused exchange (no separate broadcast pass)
+        cb = (column_blocks(A, self.col_slices, compact=compact_blocks,
+                            compact_last=compact_blocks and plan.world == 1)
+              if self.col_slices > 1 else [(A, None)])
+        self.blocks = [B for B, _ in cb]
+        self.block_rows = [r for _, r in cb]
         self.acc = torch.empty(max(1, plan.local_rows), dtype=dt, device=A.device) if self.col_slices > 1 else None
 
     def _setup_fused(self, dt):
@@ -396,8 +426,10 @@ class ShardedSeer:
 
     def spmv_into(self, x, dests, self_index: int, Ps) -> None:
         """This rank's y = A x stored into ``dests`` (``dests[self_index]`` the local copy).
-        Column-blocked: the blocks accumulate into self.acc, the last block's stores (acc +
-        its part) go to the destinations.  Unblocked non-merge kernels: kp_spmv."""
+        Column-blocked: the blocks accumulate into self.acc (compressed-row blocks scatter
+        their non-empty rows into it in place), then either the last full-row block's stores
+        (acc + its part) go to the destinations, or -- one rank, every block compressed --
+        the accumulator is copied there.  Unblocked non-merge kernels: kp_spmv."""
         K = self._kernels
         if len(self.blocks) == 1 and self.kernel not in (K.CSR_MP, K.CSR_WO):
             K.spmv(self.A, x, self.kernel, y=dests[self_index], prepared=Ps[0])
@@ -405,11 +437,23 @@ class ShardedSeer:
                 if i != self_index:
                     d.copy_(dests[self_index])
             return
-        for s_, (B, Pb) in enumerate(zip(self.blocks[:-1], Ps[:-1])):
-            if s_ == 0:  # the first block has nothing to add: the plain kernel (kp_spmv)
+        if self.block_rows[0] is not None:  # compressed-row blocks add into a zeroed accumulator
+            self.acc.zero_()
+        last_compact = self.block_rows[-1] is not None
+        upto = len(self.blocks) if last_compact else len(self.blocks) - 1
+        for s_, (B, Pb, rid) in enumerate(zip(self.blocks[:upto], Ps[:upto], self.block_rows[:upto])):
+            if B.n_rows == 0:
+                continue
+            if rid is not None:  # only this block's non-empty rows, scattered in place
+                K.spmv_bcast(B, x, self.kernel, [self.acc], 0, prepared=Pb, acc=self.acc, rows=rid)
+            elif s_ == 0:  # the first block has nothing to add: the plain kernel (kp_spmv)
                 K.spmv(B, x, self.kernel, y=self.acc, prepared=Pb)
             else:
                 K.spmv_bcast(B, x, self.kernel, [self.acc], 0, prepared=Pb, acc=self.acc)
+        if last_compact:  # every block accumulated: y is the accumulator
+            for d in dests:
+                d[:self.plan.local_rows].copy_(self.acc[:self.plan.local_rows])
+            return
         K.spmv_bcast(self.blocks[-1], x, self.kernel, dests, self_index, prepared=Ps[-1],
                      acc=self.acc if len(self.blocks) > 1 else None)
 

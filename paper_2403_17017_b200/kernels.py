@@ -145,12 +145,14 @@ def check_vector(v, A, n: int, name: str, out: bool = False) -> None:
 
 
 def spmv_bcast(A, x, kernel, dests, self_index: int, *, prepared: Prepared | None = None, stream=None,
-               acc=None):
+               acc=None, rows=None):
     """kp_spmv_bcast: y = A.x written from the kernel's own epilogue into every tensor of
     ``dests`` (this rank's slice of each rank's next-x buffer; peer-mapped symmetric memory
     or local tensors), ``dests[self_index]`` being the local copy.  Merge-path kernels only.
     ``acc`` (n_rows elements, may be ``dests[self_index]``): y = acc + A.x instead
-    (kp_spmv_bcast_acc, the column-blocked iteration of dist.ShardedSeer)."""
+    (kp_spmv_bcast_acc, the column-blocked iteration of dist.ShardedSeer).  ``rows`` (int32,
+    n_rows entries): row r of A is row rows[r] of the single destination / acc (a
+    compressed-row block accumulating in place)."""
     torch = _lib.require_cuda()
     A = as_device(A)
     k = kernel_index(kernel)
@@ -167,6 +169,11 @@ def spmv_bcast(A, x, kernel, dests, self_index: int, *, prepared: Prepared | Non
     if acc is not None and (acc.dtype != A.values.dtype or acc.numel() < A.n_rows or not acc.is_contiguous()
                             or not acc.is_cuda):
         raise ValueError("acc needs n_rows contiguous elements of the matrix value dtype")
+    if rows is not None:
+        if rows.dtype != torch.int32 or rows.numel() != A.n_rows or not rows.is_contiguous() or not rows.is_cuda:
+            raise ValueError("rows needs n_rows contiguous int32 entries on the device")
+        if len(dests) != 1 or (acc is not None and acc.data_ptr() != dests[0].data_ptr()):
+            raise ValueError("a row map scatters into one destination, accumulating in place")
     pe = _lib.kp_peers()
     for i, d in enumerate(dests):
         pe.y[i] = d.data_ptr()
@@ -175,7 +182,8 @@ def spmv_bcast(A, x, kernel, dests, self_index: int, *, prepared: Prepared | Non
     P = ctypes.byref(prepared.struct) if prepared is not None else None
     with torch.cuda.device(A.device):
         _lib.check(_lib.load().kp_spmv_bcast_acc(k, ctypes.byref(A.struct), P, x.data_ptr(),
-                                                 0 if acc is None else acc.data_ptr(), ctypes.byref(pe),
+                                                 0 if acc is None else acc.data_ptr(),
+                                                 0 if rows is None else rows.data_ptr(), ctypes.byref(pe),
                                                  0 if ws is None else ws.data_ptr(), 0 if ws is None else ws.numel(),
                                                  _lib.stream_handle(stream, A.device)),
                    f"kp_spmv_bcast_acc[{KERNELS[k]}]")

@@ -14,7 +14,7 @@ def test_auto_col_slices():
     assert kdist.auto_col_slices(0, l2) == 1
     assert kdist.auto_col_slices(budget, l2) == 1
     assert kdist.auto_col_slices(budget + 1, l2) == 2
-    assert kdist.auto_col_slices(64 << 22, l2) == 2            # C5 fp32: 268 MB x
+    assert kdist.auto_col_slices(64 << 22, l2) == 3            # C5 fp32: 268 MB x
     assert kdist.auto_col_slices(1 << 40, l2) == kdist.MAX_COL_SLICES
 
 
@@ -53,3 +53,11 @@ def test_split_columns_partitions_and_sums(S):
             got[r] += v[o[r]:o[r + 1]] @ x[cr]
     assert total == cols.size
     np.testing.assert_allclose(got, want, rtol=1e-12, atol=1e-12)
+
+
+def test_compress_rows():
+    off = torch.tensor([0, 0, 3, 3, 3, 5, 6, 6], dtype=torch.int64)
+    o, rid = kdist.compress_rows(off)
+    assert o.tolist() == [0, 3, 5, 6] and rid.tolist() == [1, 4, 5] and rid.dtype == torch.int32
+    o, rid = kdist.compress_rows(torch.zeros(4, dtype=torch.int64))
+    assert o.tolist() == [0] and rid.numel() == 0

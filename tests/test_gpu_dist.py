@@ -245,9 +245,10 @@ def test_bcast_acc_matches_oracle(dtype, kern, mode, orc):
         L.kp_debug_set_wave_warps(prev)
 
 
+@pytest.mark.parametrize("compact", [True, False])
 @pytest.mark.parametrize("world", [1, 3])
 @pytest.mark.parametrize("S", [2, 3, 5])
-def test_column_blocks_loopback_matches_oracle(world, S, orc):
+def test_column_blocks_loopback_matches_oracle(world, S, compact, orc):
     """Column-blocked row shards (dist.column_blocks + accumulating stores, the last block's
     stores to every rank's next-x buffer), `world` simulated ranks on one GPU."""
     m = gen.config("C5", small=True, device="cuda")
@@ -260,28 +261,39 @@ def test_column_blocks_loopback_matches_oracle(world, S, orc):
     n = world * plan0.r_max
     nxt = [torch.full((n,), float("nan"), dtype=torch.float64, device="cuda") for _ in range(world)]
     for r, (A, plan, _) in enumerate(shards):
-        blocks = kdist.column_blocks(A, S)
-        assert sum(B.nnz for B in blocks) == A.nnz
+        blocks = kdist.column_blocks(A, S, compact=compact)
+        assert sum(B.nnz for B, _ in blocks) == A.nnz
+        assert (blocks[0][1] is not None) == compact and blocks[-1][1] is None
         xp = plan.pad(torch.from_numpy(x).cuda())
         acc = torch.empty(plan.local_rows, dtype=torch.float64, device="cuda")
-        for s, B in enumerate(blocks[:-1]):
-            kernels.spmv_bcast(B, xp, kernels.CSR_WO, [acc], 0, acc=acc if s else None)
+        if compact:
+            acc.zero_()
+        for s, (B, rid) in enumerate(blocks[:-1]):
+            if rid is not None:
+                assert B.n_rows == rid.numel() <= plan.local_rows
+                if B.n_rows:
+                    kernels.spmv_bcast(B, xp, kernels.CSR_WO if s % 2 else kernels.CSR_MP, [acc], 0, acc=acc,
+                                       rows=rid)
+            else:
+                kernels.spmv_bcast(B, xp, kernels.CSR_WO, [acc], 0, acc=acc if s else None)
         dests = [nxt[q][r * plan.r_max: r * plan.r_max + plan.local_rows] for q in range(world)]
-        kernels.spmv_bcast(blocks[-1], xp, kernels.CSR_MP, dests, r, acc=acc)
+        kernels.spmv_bcast(blocks[-1][0], xp, kernels.CSR_MP, dests, r, acc=acc)
     torch.cuda.synchronize()
     for q in range(world):
         ok, ratio = orc.spmv_check(plan0.unpad(nxt[q]).cpu().numpy(), yref, absy, 1e-12)
         assert ok, (world, S, q, ratio)
 
 
+@pytest.mark.parametrize("compact", [True, False])
 @pytest.mark.parametrize("S", [1, 3, 4])
 @pytest.mark.parametrize("kern", [kernels.CSR_WO, kernels.CSR_MP])
-def test_sharded_seer_column_blocked_power_iteration(S, kern, orc):
+def test_sharded_seer_column_blocked_power_iteration(S, kern, compact, orc):
     """ShardedSeer(col_slices=S) at world 1 (no process group: local exchange) == the
-    oracle's power iteration; S = 1 is the unblocked path."""
+    oracle's power iteration; S = 1 is the unblocked path; compressed-row or full blocks."""
     m = gen.config("C5", small=True, device="cuda")
     A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, m.n_cols, 0, 1, torch.float64)
-    run = kdist.ShardedSeer(_model(), A, plan, 3, m.n_rows, m.n_cols, m.nnz, kernel=kern, col_slices=S)
+    run = kdist.ShardedSeer(_model(), A, plan, 3, m.n_rows, m.n_cols, m.nnz, kernel=kern, col_slices=S,
+                            compact_blocks=compact)
     assert run.col_slices == S and len(run.blocks) == S
     x0 = torch.full((m.n_rows,), 1.0 / m.n_rows, dtype=torch.float64, device="cuda")
     got = run.step(x0).cpu().numpy()
@@ -346,3 +358,42 @@ def test_column_blocks_with_an_empty_block(kern, orc):
         for _ in range(2):
             ref, _ = orc.spmv_csr(off, col.astype(np.int32), val, ref)
         assert np.abs(got - ref).max() <= 1e-12 * max(1.0, np.abs(ref).max())
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+@pytest.mark.parametrize("kern", [kernels.CSR_WO, kernels.CSR_MP])
+def test_bcast_row_map_in_place(dtype, kern, orc):
+    """kp_spmv_bcast_acc with a row map: dest[rows[r]] += (A x)[r] in place, every other
+    row untouched -- with range-end carries through the fix-up (few resident warps)."""
+    from paper_2403_17017_b200 import _lib
+    L = _lib.load()
+    prev = L.kp_debug_set_wave_warps(7)
+    try:
+        m = gen.config("C5", small=True, device="cuda")
+        off, col, val = m.numpy()
+        rng = np.random.default_rng(17)
+        n_dest = m.n_rows * 3
+        rows = np.sort(rng.choice(n_dest, size=m.n_rows, replace=False)).astype(np.int32)
+        A = m.to_device_csr(dtype)
+        x = rng.uniform(0, 1, m.n_cols)
+        base = rng.normal(size=n_dest)
+        d = torch.from_numpy(base).to(dtype).cuda()
+        base = d.double().cpu().numpy()
+        xd = torch.from_numpy(x).to(dtype).cuda()
+        vv = val.astype(np.float32).astype(np.float64) if dtype == torch.float32 else val
+        xx = x.astype(np.float32).astype(np.float64) if dtype == torch.float32 else x
+        y, absy = orc.spmv_csr(off, col.astype(np.int32), vv, xx)
+        kernels.spmv_bcast(A, xd, kern, [d], 0, acc=d, rows=torch.from_numpy(rows).cuda())
+        got = d.double().cpu().numpy()
+        want = base.copy()
+        want[rows] += y
+        bound = np.zeros(n_dest)
+        bound[rows] = absy
+        ok, r = orc.spmv_check(got, want, bound + np.abs(base), 1e-5 if dtype == torch.float32 else 1e-12)
+        assert ok, r
+        untouched = np.setdiff1d(np.arange(n_dest), rows)
+        assert np.array_equal(got[untouched], base[untouched])
+        with pytest.raises(ValueError):  # a row map scatters into exactly one destination
+            kernels.spmv_bcast(A, xd, kern, [d, d], 0, acc=d, rows=torch.from_numpy(rows).cuda())
+    finally:
+        L.kp_debug_set_wave_warps(prev)
