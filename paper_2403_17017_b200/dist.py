@@ -437,22 +437,26 @@ class ShardedSeer:
                 if i != self_index:
                     d.copy_(dests[self_index])
             return
-        if self.block_rows[0] is not None:  # compressed-row blocks add into a zeroed accumulator
-            self.acc.zero_()
         last_compact = self.block_rows[-1] is not None
+        n = self.plan.local_rows
+        # one destination and every block compressed: accumulate straight into it
+        acc = dests[0][:max(1, n)] if last_compact and len(dests) == 1 else self.acc
+        if self.block_rows[0] is not None:  # compressed-row blocks add into a zeroed accumulator
+            acc.zero_()
         upto = len(self.blocks) if last_compact else len(self.blocks) - 1
         for s_, (B, Pb, rid) in enumerate(zip(self.blocks[:upto], Ps[:upto], self.block_rows[:upto])):
             if B.n_rows == 0:
                 continue
             if rid is not None:  # only this block's non-empty rows, scattered in place
-                K.spmv_bcast(B, x, self.kernel, [self.acc], 0, prepared=Pb, acc=self.acc, rows=rid)
+                K.spmv_bcast(B, x, self.kernel, [acc], 0, prepared=Pb, acc=acc, rows=rid)
             elif s_ == 0:  # the first block has nothing to add: the plain kernel (kp_spmv)
-                K.spmv(B, x, self.kernel, y=self.acc, prepared=Pb)
+                K.spmv(B, x, self.kernel, y=acc, prepared=Pb)
             else:
-                K.spmv_bcast(B, x, self.kernel, [self.acc], 0, prepared=Pb, acc=self.acc)
+                K.spmv_bcast(B, x, self.kernel, [acc], 0, prepared=Pb, acc=acc)
         if last_compact:  # every block accumulated: y is the accumulator
             for d in dests:
-                d[:self.plan.local_rows].copy_(self.acc[:self.plan.local_rows])
+                if d.data_ptr() != acc.data_ptr():
+                    d[:n].copy_(acc[:n])
             return
         K.spmv_bcast(self.blocks[-1], x, self.kernel, dests, self_index, prepared=Ps[-1],
                      acc=self.acc if len(self.blocks) > 1 else None)
