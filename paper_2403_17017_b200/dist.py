@@ -197,8 +197,8 @@ def column_blocks(A, slices: int, compact: bool = True, compact_last: bool = Fal
     of (DeviceCSR, row ids).  With ``compact`` every block but the last keeps only its
     non-empty rows (row ids: int32 tensor mapping them back; R-MAT C5: 21-32 % of the rows
     per block); the last block keeps every row (row ids None), so its stores cover the
-    whole y -- they are the exchange -- unless ``compact_last`` (one rank: the accumulator
-    is copied to the next x instead)."""
+    whole y -- they are the exchange -- unless ``compact_last`` (one rank: the blocks
+    accumulate straight into the next x)."""
     import torch
     from .device import DeviceCSR
     out = []
@@ -391,9 +391,9 @@ class ShardedSeer:
         if S < 1:
             raise ValueError("col_slices must be >= 1")
         self.col_slices = S if self.kernel in (kernels.CSR_MP, kernels.CSR_WO) and A.nnz > 0 else 1
-        # one rank: every block compressed, the accumulator copied to the next x (a local
-        # copy); several ranks: the last block keeps all rows so that its stores are the
-        # fused exchange (no separate broadcast pass)
+        # one rank: every block compressed, accumulating straight into the next x; several
+        # ranks: the last block keeps all rows so that its stores are the fused exchange
+        # (no separate broadcast pass)
         cb = (column_blocks(A, self.col_slices, compact=compact_blocks,
                             compact_last=compact_blocks and plan.world == 1)
               if self.col_slices > 1 else [(A, None)])
@@ -429,7 +429,7 @@ class ShardedSeer:
         Column-blocked: the blocks accumulate into self.acc (compressed-row blocks scatter
         their non-empty rows into it in place), then either the last full-row block's stores
         (acc + its part) go to the destinations, or -- one rank, every block compressed --
-        the accumulator is copied there.  Unblocked non-merge kernels: kp_spmv."""
+        the single destination is the accumulator.  Unblocked non-merge kernels: kp_spmv."""
         K = self._kernels
         if len(self.blocks) == 1 and self.kernel not in (K.CSR_MP, K.CSR_WO):
             K.spmv(self.A, x, self.kernel, y=dests[self_index], prepared=Ps[0])
