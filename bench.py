@@ -1013,7 +1013,8 @@ def run_sharded(a):
                          "algorithmic_bytes_per_launch": kb, "peak_source": peak_src,
                          "col_slices": run.col_slices, "ms": round(per * 1e3, 3),
                          "unblocked_ms": round(statistics.median(ts_unblocked) * 1e3, 3),
-                         "note": "rank 0's local SpMV (column-blocked when col_slices > 1: x slices L2-resident)"},
+                         "note": "rank 0's local SpMV (col_slices > 1: column blocks of the shard, compressed-row, "
+                                 "accumulated in the merge kernel's stores)"},
             "e2e": e2e, "gpu_launches": int(launches), "cpu_baseline": None, "clocks": clk,
         }), flush=True)
     dist.destroy_process_group()
