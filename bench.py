@@ -75,6 +75,7 @@ def _args():
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true", help="C5: skip the end-to-end (host-resident shard) leg")
+    ap.add_argument("--no-reorder", action="store_true", help="C5: keep the generator's vertex numbering")
     ap.add_argument("--no-configs", action="store_true", help="skip per_config (C1, C3, C4) and favourable")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--config-cpu-seconds", type=float, default=4.0)
@@ -882,14 +883,30 @@ def run_sharded(a):
     offh = m.row_offsets.cpu().numpy()
     samp = [(int(r), m.col_indices[offh[r]:offh[r + 1]].cpu().numpy(), m.values[offh[r]:offh[r + 1]].cpu().numpy())
             for r in rs]
-    A, plan, _ = kdist.shard_device(m.row_offsets, m.col_indices, m.values, C, rank, world, dtype)
-    del m
-    torch.cuda.empty_cache()
     t_gen = time.time() - t0
+    # vertex reordering at distribution time (dist.degree_order: hottest columns first, the
+    # iteration in the permuted space; parity below maps back to the original ids)
+    newid_np, t_reorder = None, 0.0
+    off_g, col_g, val_g = m.row_offsets, m.col_indices, m.values
+    if not a.no_reorder:
+        t0 = time.time()
+        order, newid = kdist.degree_order(m.col_indices, C)
+        off_g, col_g, val_g = kdist.permute_symmetric(m.row_offsets, m.col_indices, m.values, order, newid)
+        newid_np = newid.cpu().numpy()
+        del order, newid, m
+        torch.cuda.synchronize()
+        t_reorder = time.time() - t0
+    A, plan, _ = kdist.shard_device(off_g, col_g, val_g, C, rank, world, dtype)
+    del off_g, col_g, val_g
+    m = None
+    torch.cuda.empty_cache()
+    # a reordered shard gathers from a hot, L2-resident prefix of x: column blocking does
+    # not pay there (tools/probes/reorder_probe.py: 4.13 ms unblocked vs 4.20 blocked)
+    col_slices = 1 if newid_np is not None else "auto"
     model, model_src = _load_model()
     exchange = a.exchange if backend == "nccl" else "host"
     t0 = time.time()
-    run = kdist.ShardedSeer(model, A, plan, k, R, C, Z, exchange=exchange)
+    run = kdist.ShardedSeer(model, A, plan, k, R, C, Z, exchange=exchange, col_slices=col_slices)
     torch.cuda.synchronize()
     t_setup = time.time() - t0  # selection + column blocking + exchange rendezvous (once)
     kern = run.kernel
@@ -903,6 +920,8 @@ def run_sharded(a):
         x_out = run.step(x_in, iters=1).clone()
         xg_in = plan.unpad(x_in).double().cpu().numpy()
         xg_out = plan.unpad(x_out).double().cpu().numpy()
+        if newid_np is not None:  # permuted ids -> original ids: x[v] = x'[newid[v]]
+            xg_in, xg_out = xg_in[newid_np], xg_out[newid_np]
         errs = []
         for r, c, v in samp:
             vv = v.astype(npdt).astype(np.float64)
@@ -921,7 +940,7 @@ def run_sharded(a):
         dist.all_reduce(okt, op=dist.ReduceOp.MIN)
         if okt.item() < 1.0:
             fallback = f"fused exchange failed the pre-timing sampled-row parity (max err/bound {err0:.3g}); NCCL all-gather used"
-            run = kdist.ShardedSeer(model, A, plan, k, R, C, Z, exchange="nccl", kernel=kern)
+            run = kdist.ShardedSeer(model, A, plan, k, R, C, Z, exchange="nccl", kernel=kern, col_slices=col_slices)
     x0 = torch.full((world * plan.r_max,), 1.0 / R, dtype=dtype, device=dev)
     sv, so = 4 if dtype == torch.float32 else 8, 4
     bytes_csr = csr_bytes(R, C, Z, sv, so)
@@ -994,7 +1013,11 @@ def run_sharded(a):
                        "parallelism": f"row-sharded x{world} (nnz-balanced, y exchanged every iteration)",
                        "l2": "inputs larger than L2 (A: %.1f GB)" % (bytes_csr / 1e9), "model": model_src,
                        "byte_model": "nnz*(4+sv)+(R+1)*so+C*sv+R*sv per iteration, x counted once",
-                       "generation_s": round(t_gen, 1), "setup_s": round(t_setup, 2)},
+                       "generation_s": round(t_gen, 1), "setup_s": round(t_setup, 2),
+                       "reorder": None if newid_np is None else {
+                           "kind": "symmetric, vertices by descending in-degree (dist.degree_order), once at "
+                                   "distribution; the iteration runs in the permuted space, parity is checked "
+                                   "in the original ids", "seconds": round(t_reorder, 2)}},
             "comm": {"backend": backend, "nranks": dist.get_world_size(), "exchange": run.exchange,
                      "nccl_version": ".".join(map(str, torch.cuda.nccl.version())) if backend == "nccl" else None,
                      "watchdog": wstat if wd else None, "exchange_fallback": fallback,

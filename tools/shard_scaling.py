@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--reps", type=int, default=5)
     ap.add_argument("--out", default=None)
     ap.add_argument("--bcast", action="store_true", help="only measure the fused-exchange epilogue cost")
+    ap.add_argument("--no-reorder", action="store_true", help="keep the generator's vertex numbering")
     ap.add_argument("--col-slices", default="1,auto",
                     help="column blocking of each rank's SpMV (dist.ShardedSeer col_slices), comma list")
     a = ap.parse_args()
@@ -39,8 +40,15 @@ def main():
     kern = kernels.kernel_index(a.kernel)
     m = gen.config("C5", device="cuda")
     R, C, Z = m.n_rows, m.n_cols, m.nnz
+    if not a.no_reorder:  # as bench.py's C5 does at distribution time
+        order, newid = kdist.degree_order(m.col_indices, C)
+        m.row_offsets, m.col_indices, m.values = kdist.permute_symmetric(m.row_offsets, m.col_indices, m.values,
+                                                                        order, newid)
+        del order, newid
+        torch.cuda.empty_cache()
     flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-    res = {"matrix": "C5 R-MAT s26 ef16", "rows": R, "nnz": Z, "kernel": a.kernel, "parts": {}}
+    res = {"matrix": "C5 R-MAT s26 ef16", "rows": R, "nnz": Z, "kernel": a.kernel, "reordered": not a.no_reorder,
+           "parts": {}}
     slices = a.col_slices.split(",")
     for P in [int(v) for v in a.parts.split(",")]:
         times = {S: [] for S in slices}
