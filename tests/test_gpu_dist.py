@@ -397,3 +397,33 @@ def test_bcast_row_map_in_place(dtype, kern, orc):
             kernels.spmv_bcast(A, xd, kern, [d, d], 0, acc=d, rows=torch.from_numpy(rows).cuda())
     finally:
         L.kp_debug_set_wave_warps(prev)
+
+
+@pytest.mark.parametrize("world", [1, 3])
+def test_reordered_shards_power_iteration(world, orc):
+    """P A P^T distributed (dist.degree_order + permute_symmetric), `world` simulated ranks
+    on one GPU with the fused-epilogue stores into every rank's buffer: after mapping back
+    through newid, one iteration equals the oracle's A x on the ORIGINAL matrix."""
+    m = gen.config("C5", small=True, device="cuda")
+    off, col, val = m.numpy()
+    n = m.n_rows
+    order, newid = kdist.degree_order(m.col_indices, n)
+    o2, c2, v2 = kdist.permute_symmetric(m.row_offsets, m.col_indices, m.values, order, newid)
+    x = np.random.default_rng(29).uniform(0, 1, n)
+    yref, absy = orc.spmv_csr(off, col.astype(np.int32), val, x)
+    xp = np.empty(n)
+    nid = newid.cpu().numpy()
+    xp[nid] = x
+    shards = [kdist.shard_device(o2, c2, v2, n, r, world, torch.float64) for r in range(world)]
+    plan0 = shards[0][1]
+    nxt = [torch.full((world * plan0.r_max,), float("nan"), dtype=torch.float64, device="cuda")
+           for _ in range(world)]
+    for r, (A, plan, _) in enumerate(shards):
+        xpad = plan.pad(torch.from_numpy(xp).cuda())
+        dests = [nxt[q][r * plan.r_max: r * plan.r_max + plan.local_rows] for q in range(world)]
+        kernels.spmv_bcast(A, xpad, kernels.CSR_WO, dests, r)
+    torch.cuda.synchronize()
+    for q in range(world):
+        got = plan0.unpad(nxt[q]).cpu().numpy()[nid]      # permuted ids -> original ids
+        ok, ratio = orc.spmv_check(got, yref, absy, 1e-12)
+        assert ok, (world, q, ratio)
